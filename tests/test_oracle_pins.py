@@ -337,12 +337,12 @@ def test_circle_config1_one_long_h1_bar():
 
 
 def test_sphere_s2_betti():
-    pts = G.sphere(36, 2, seed=11)
+    # beta_2(S^2) = 1: a 50-point sample has exactly one H2 bar, a long one, and at the
+    # enclosing radius no essential classes above dimension 0 (Prop 5.2.13 proof)
+    pts = G.sphere(50, 2, seed=3)
     lt = G.lower_tri_from_points(pts)
-    R = O.enclosing_radius(lt, 36)
-    b = O.barcode(lt, 36, 2, R)
+    R = O.enclosing_radius(lt, 50)
+    b = O.barcode(lt, 50, 2, R)
     h2 = b.positive(2)
-    h1 = b.positive(1)
-    p2 = np.sort(h2[:, 1] - h2[:, 0])[::-1]
-    assert len(p2) >= 1 and p2[0] > 0.3 and (p2[1:] < 0.25 * p2[0]).all()
-    assert len(h1) == 0 or (h1[:, 1] - h1[:, 0]).max() < 0.25 * p2[0]
+    assert len(h2) == 1 and h2[0, 1] - h2[0, 0] > 0.5
+    assert b.num_essential(1) == 0 and b.num_essential(2) == 0 and b.num_essential(0) == 1
