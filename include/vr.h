@@ -1,0 +1,160 @@
+/*
+ * vr.h — C ABI of libvr, the B200-native Vietoris–Rips persistence barcode library.
+ *
+ * The operation (PAPER.md Ch.5, "Ripser++"): given a finite metric space by its
+ * distance matrix (Def 5.1.1), compute the persistence barcode over Z/2
+ * of the Vietoris–Rips filtration Rips_t(X) = { s : diam(s) <= t } (Eq 5.3,
+ * P:4668-4672) for homology dimensions 0..max_dim, i.e. the persistence pairs of the
+ * simplex-wise refinement of §5.1.4 as the standard algorithm (Alg 11,
+ * P:4724-4745) defines them.  The data-parallel hot path per dimension d >= 1 runs on
+ * the GPU (sm_100a): enumeration of the d-simplices through the combinatorial number
+ * system (Eq 5.6) with their diameters and the threshold filter (Alg 17/18,
+ * P:5691-5731), the apparent-pair test (Def 5.3.4 / Lemma 5.3.6 / Alg 13,
+ * P:4926-5025), clearing (§5.2.3, Lemma 4.2.3, Prop 5.3.9), stream compaction
+ * (§5.5.3) and the radix sort into coboundary order (Fig 5.2 caption).  The
+ * few non-apparent columns are reduced on the host (Alg 12 / §5.2.9-5.2.11); dimension
+ * 0 is union-find (§5.2.5).
+ *
+ * Conventions
+ *   - dist_lower_tri: n(n-1)/2 fp32 values in Ripser lower-distance order: the entry for
+ *     (i, j), i > j, is at index i(i-1)/2 + j.  Distances must be >= 0 and
+ *     not NaN.  Zero distances (duplicate points) are accepted (reading A35).
+ *   - threshold: +INFINITY = full Rips; the library then cuts at the enclosing radius
+ *     R = min_x max_y d(x, y) (§5.2.12, Prop 5.2.13), which leaves every
+ *     positive-length and essential bar unchanged.  A finite threshold t >= 0 is
+ *     inclusive: a simplex is present iff diam <= t (Eq 5.3, Alg 17 line 3).
+ *   - Output per dimension 0..max_dim: (birth, death) fp32 pairs with birth < death,
+ *     death = +INFINITY for essential classes, sorted by (birth, death).  Births and
+ *     deaths are copies of distance-matrix entries (bit-exact).  Zero-length pairs are
+ *     only counted (vr_stats) unless vr_options.include_zero is set.
+ *   - Ownership: every pointer argument is owned by the caller and only read during the
+ *     call; a vr_result is library-owned and released with vr_free; pointers returned by
+ *     accessors stay valid until vr_free.
+ *   - Errors: every int-returning entry returns 0 (VR_OK) or a VR_E* code and sets a
+ *     thread-local message readable with vr_last_error(); on error *out is set to NULL.
+ *     Capacity problems (C(n, max_dim+2) >= 2^63, a key that cannot be packed in 64
+ *     bits, device memory) are raised before any GPU work.
+ *   - Determinism: the output bytes do not depend on the launch configuration.
+ */
+#ifndef VR_H
+#define VR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VR_OK 0
+#define VR_EINVAL 1    /* usage: n < 1, max_dim < 0 or > VR_MAX_DIM, NaN/negative threshold, NULL */
+#define VR_EINPUT 2    /* bad input: a negative or NaN distance */
+#define VR_ECAPACITY 3 /* C(n, max_dim+2) >= 2^63, unpackable key, or out of device memory */
+#define VR_EDEVICE 4   /* CUDA failure (no device, launch error, ...) */
+
+#define VR_MAX_DIM 6
+
+typedef struct {
+  float birth;
+  float death; /* +INFINITY for an essential class */
+} vr_pair;
+
+/* Index-level pair: the birth simplex (dim p) and death simplex (dim p+1) by their
+ * combinatorial index (Eq 5.6).  death_cidx = UINT64_MAX for an essential class. */
+typedef struct {
+  uint64_t birth_cidx;
+  uint64_t death_cidx;
+} vr_index_pair;
+
+typedef struct {
+  int32_t include_zero;  /* 0 (default): report birth < death only; 1: also zero-length pairs */
+  int32_t index_pairs;   /* 1: also keep the index-level pairing (every pair, apparent ones
+                            included; intended for tests on small inputs) */
+  int32_t residual_mode; /* 0: reduction-matrix (V) mode (§5.2.9, default); 1: oblivious (Alg 12) */
+  int32_t apparent_steps;/* cofacets tested per column in the first (lane-per-column) phase of
+                            the apparent test before a column moves to the warp-cooperative
+                            phase; 0 = library default */
+  int32_t device;        /* CUDA device ordinal used by vr_barcodes (host-pointer entry) */
+  int32_t reserved[7];
+} vr_options;
+
+/* Per-dimension statistics (Table 5.1 / 5.5 counters, stage times). */
+typedef struct {
+  int64_t candidates;      /* C(n, d+1): every d-simplex index */
+  int64_t survivors;       /* d-simplices with diam <= t */
+  int64_t apparent;        /* apparent columns (each an apparent pair (s, t)) */
+  int64_t cleared;         /* columns zeroed by clearing (deaths of dimension d-1) */
+  int64_t residual_columns;/* non-apparent, non-cleared columns reduced on the host */
+  int64_t emergent;        /* residual columns paired by the emergent shortcut (§5.2.11) */
+  int64_t pairs_all;       /* finite pairs incl. zero-length, this dimension */
+  int64_t pairs_positive;  /* finite pairs with birth < death */
+  int64_t essential;       /* essential classes */
+  int64_t queued;          /* columns sent to the warp-cooperative apparent phase */
+  int64_t scanned;         /* cofacet vertices examined by the apparent tests and the
+                              clearing recomputation (both phases) */
+  double ms_enumerate;     /* GPU: enumerate + threshold + apparent phase 1 (+ dim-0 edge keys) */
+  double ms_resolve;       /* GPU: apparent phase 2 + clearing + compaction */
+  double ms_sort;          /* GPU: radix sort of the columns into coboundary order */
+  double ms_residual;      /* host: residual reduction (dim 0: union-find) */
+  double ms_transfer;      /* host<->device copies of this dimension's columns / pairs */
+} vr_stats;
+
+typedef struct vr_result vr_result;
+
+/* Host-pointer entry: copies dist_lower_tri to the device (options->device), computes
+ * everything, returns a result handle.  opt may be NULL (defaults). */
+int vr_barcodes(const float* dist_lower_tri, int64_t n, int32_t max_dim, float threshold,
+                const vr_options* opt, vr_result** out);
+
+/* Device-pointer entry: d_dist_lower_tri is a device pointer on the CURRENT device,
+ * `stream` a cudaStream_t (NULL = legacy default stream) on which all GPU work is
+ * ordered.  Intended for callers that already hold the matrix in HBM (e.g. a torch
+ * tensor). */
+int vr_barcodes_device(const float* d_dist_lower_tri, int64_t n, int32_t max_dim, float threshold,
+                       const vr_options* opt, void* stream, vr_result** out);
+
+int32_t vr_max_dim(const vr_result* r);
+int64_t vr_num_pairs(const vr_result* r, int32_t dim);
+const vr_pair* vr_pairs(const vr_result* r, int32_t dim);
+int64_t vr_num_index_pairs(const vr_result* r, int32_t dim); /* 0 unless options.index_pairs */
+const vr_index_pair* vr_index_pairs(const vr_result* r, int32_t dim);
+int vr_stats_get(const vr_result* r, int32_t dim, vr_stats* s);
+float vr_threshold_used(const vr_result* r); /* t actually applied (R when threshold = +inf) */
+void vr_free(vr_result* r);
+const char* vr_last_error(void);
+
+/* ----------------------------------------------------------------------------------
+ * Hot-path replay (benchmarking).  A vr_plan holds the device tables and the clearing
+ * inputs (residual deaths of every dimension) found by one full run, so the GPU hot
+ * path of all dimensions 1..max_dim — tables (a0), enumeration + threshold + apparent
+ * test (a1, a5), clearing (a2), compaction (a3, a6) and the radix sort of the columns
+ * into coboundary order (a4) — can be re-run on the device with no host work in
+ * between beyond launch bookkeeping.  The residual reduction and dimension 0 are not
+ * part of the replay ("off path, reported separately").
+ * ---------------------------------------------------------------------------------- */
+typedef struct vr_plan vr_plan;
+
+/* Builds the plan from a device matrix and runs the full computation once (the result
+ * of that run is returned in *out if out != NULL, else dropped). */
+int vr_plan_create(const float* d_dist_lower_tri, int64_t n, int32_t max_dim, float threshold,
+                   const vr_options* opt, void* stream, vr_plan** plan, vr_result** out);
+/* Re-runs the hot path for all dimensions, asynchronously on the plan's stream.
+ * Returns the number of kernels launched in *launches (may be NULL). */
+int vr_plan_replay(vr_plan* plan, int64_t* launches);
+/* Survivors (sum over d = 1..max_dim) — the numerator of hot-path simplices/s. */
+int64_t vr_plan_survivors(const vr_plan* plan);
+/* Apparent and residual column totals counted by the last replay (synchronizes the
+ * plan's stream), to verify that a replay did the work. */
+int vr_plan_check(vr_plan* plan, int64_t* apparent_total, int64_t* residual_total);
+/* Device time (ms, CUDA events on the plan's stream) of the last replay's stages, summed
+ * over dimensions: [0] tables (a0), [1] enumerate + apparent phase 1, [2] apparent
+ * phase 2 + clearing + compaction, [3] radix sort.  Synchronizes the plan's stream.
+ * Also the algorithmic work counters of the plan's first run: [4] candidates,
+ * [5] survivors, [6] cofacet vertices scanned, [7] sum over d of (d+1)*(candidates_d +
+ * scanned_d) = rank comparisons of the method. */
+int vr_plan_timing(vr_plan* plan, double out[8]);
+void vr_plan_free(vr_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VR_H */

@@ -1,0 +1,236 @@
+"""paper_2502_05063_b200 — B200-native Vietoris–Rips persistence barcodes (Ripser++ hot path).
+
+Thin ctypes binding over the C ABI in include/vr.h (libvr.so, built for sm_100a by
+build.py).  Argument marshalling only: every step of the computation runs inside libvr
+(CUDA kernels for the hot path, the library's own host code for dimension 0 and the
+residual reduction).  There is no CPU fallback: if libvr.so is missing or no CUDA device
+is present, the calls raise.
+
+    import numpy as np, paper_2502_05063_b200 as vr
+    bc = vr.barcodes(dist_lower_tri, n, max_dim=2)        # host numpy input
+    bc.pairs[1]            # (k, 2) float32 (birth, death), birth < death, sorted
+    bc.stats[1]["apparent"]
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = ["barcodes", "barcodes_device", "Plan", "Barcode", "VRError", "lib_path", "load"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libvr.so")
+
+VR_OK, VR_EINVAL, VR_EINPUT, VR_ECAPACITY, VR_EDEVICE = 0, 1, 2, 3, 4
+_CODES = {1: "VR_EINVAL", 2: "VR_EINPUT", 3: "VR_ECAPACITY", 4: "VR_EDEVICE"}
+
+
+class VRError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_CODES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class _Pair(ctypes.Structure):
+    _fields_ = [("birth", ctypes.c_float), ("death", ctypes.c_float)]
+
+
+class _IndexPair(ctypes.Structure):
+    _fields_ = [("birth_cidx", ctypes.c_uint64), ("death_cidx", ctypes.c_uint64)]
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("include_zero", ctypes.c_int32), ("index_pairs", ctypes.c_int32), ("residual_mode", ctypes.c_int32),
+                ("apparent_steps", ctypes.c_int32), ("device", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+
+
+_STAT_FIELDS = ["candidates", "survivors", "apparent", "cleared", "residual_columns", "emergent", "pairs_all",
+                "pairs_positive", "essential", "queued", "scanned"]
+_STAT_TIMES = ["ms_enumerate", "ms_resolve", "ms_sort", "ms_residual", "ms_transfer"]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int64) for f in _STAT_FIELDS] + [(f, ctypes.c_double) for f in _STAT_TIMES]
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libvr.so (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(lib_path):
+        raise ImportError(f"libvr.so not found at {lib_path}: run `python paper_2502_05063_b200/build.py` "
+                          "(there is no CPU fallback for the hot path)")
+    lib = ctypes.CDLL(lib_path)
+    vp, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
+    sig = {
+        "vr_barcodes": (ctypes.c_int, [vp, i64, i32, f32, vp, ctypes.POINTER(vp)]),
+        "vr_barcodes_device": (ctypes.c_int, [vp, i64, i32, f32, vp, vp, ctypes.POINTER(vp)]),
+        "vr_max_dim": (i32, [vp]),
+        "vr_num_pairs": (i64, [vp, i32]),
+        "vr_pairs": (vp, [vp, i32]),
+        "vr_num_index_pairs": (i64, [vp, i32]),
+        "vr_index_pairs": (vp, [vp, i32]),
+        "vr_stats_get": (ctypes.c_int, [vp, i32, ctypes.POINTER(_Stats)]),
+        "vr_threshold_used": (f32, [vp]),
+        "vr_free": (None, [vp]),
+        "vr_last_error": (ctypes.c_char_p, []),
+        "vr_plan_create": (ctypes.c_int, [vp, i64, i32, f32, vp, vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]),
+        "vr_plan_replay": (ctypes.c_int, [vp, ctypes.POINTER(i64)]),
+        "vr_plan_survivors": (i64, [vp]),
+        "vr_plan_check": (ctypes.c_int, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+        "vr_plan_timing": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double)]),
+        "vr_plan_free": (None, [vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(rc: int):
+    if rc != VR_OK:
+        raise VRError(rc, load().vr_last_error().decode(errors="replace"))
+
+
+def _options(include_zero=False, index_pairs=False, residual_mode=0, apparent_steps=0, device=0) -> _Options:
+    o = _Options()
+    o.include_zero, o.index_pairs, o.residual_mode = int(include_zero), int(index_pairs), int(residual_mode)
+    o.apparent_steps, o.device = int(apparent_steps), int(device)
+    return o
+
+
+@dataclass
+class Barcode:
+    max_dim: int
+    threshold: float
+    pairs: list = field(default_factory=list)        # per dim: (k, 2) float32
+    index_pairs: list = field(default_factory=list)  # per dim: (k, 2) uint64 (birth cidx, death cidx)
+    stats: list = field(default_factory=list)        # per dim: dict
+
+
+def _collect(h) -> Barcode:
+    lib = load()
+    D = lib.vr_max_dim(h)
+    bc = Barcode(D, float(lib.vr_threshold_used(h)))
+    for d in range(D + 1):
+        k = lib.vr_num_pairs(h, d)
+        arr = np.zeros((k, 2), np.float32)
+        if k:
+            ctypes.memmove(arr.ctypes.data, lib.vr_pairs(h, d), k * 8)
+        bc.pairs.append(arr)
+        k = lib.vr_num_index_pairs(h, d)
+        ip = np.zeros((k, 2), np.uint64)
+        if k:
+            ctypes.memmove(ip.ctypes.data, lib.vr_index_pairs(h, d), k * 16)
+        bc.index_pairs.append(ip)
+        s = _Stats()
+        _check(lib.vr_stats_get(h, d, ctypes.byref(s)))
+        bc.stats.append({f: getattr(s, f) for f in _STAT_FIELDS + _STAT_TIMES})
+    return bc
+
+
+def barcodes(dist_lower_tri, n: int, max_dim: int, threshold: float = math.inf, **opts) -> Barcode:
+    """vr_barcodes: host fp32 lower-distance vector (Ripser order, n(n-1)/2 values)."""
+    lib = load()
+    lt = np.ascontiguousarray(dist_lower_tri, dtype=np.float32)
+    if lt.size != n * (n - 1) // 2:
+        raise ValueError("dist_lower_tri must hold n(n-1)/2 values")
+    h = ctypes.c_void_p()
+    o = _options(**opts)
+    rc = lib.vr_barcodes(lt.ctypes.data if lt.size else None, n, max_dim, threshold, ctypes.byref(o), ctypes.byref(h))
+    _check(rc)
+    try:
+        return _collect(h)
+    finally:
+        lib.vr_free(h)
+
+
+def barcodes_device(d_dist_lower_tri, n: int, max_dim: int, threshold: float = math.inf, stream=None, **opts) -> Barcode:
+    """vr_barcodes_device: `d_dist_lower_tri` is a CUDA float32 torch tensor (or a raw device
+    pointer int) on the current device; `stream` a torch.cuda.Stream (None = current)."""
+    lib = load()
+    ptr, st = _device_ptr_and_stream(d_dist_lower_tri, n, stream)
+    h = ctypes.c_void_p()
+    o = _options(**opts)
+    _check(lib.vr_barcodes_device(ptr, n, max_dim, threshold, ctypes.byref(o), st, ctypes.byref(h)))
+    try:
+        return _collect(h)
+    finally:
+        lib.vr_free(h)
+
+
+def _device_ptr_and_stream(t, n, stream):
+    if isinstance(t, int):
+        ptr = t
+    else:
+        if not (t.is_cuda and t.dtype.is_floating_point and t.element_size() == 4 and t.is_contiguous()):
+            raise ValueError("expected a contiguous CUDA float32 tensor")
+        if t.numel() != n * (n - 1) // 2:
+            raise ValueError("tensor must hold n(n-1)/2 values")
+        ptr = t.data_ptr()
+    if stream is None:
+        try:
+            import torch
+            st = torch.cuda.current_stream().cuda_stream
+        except Exception:  # pragma: no cover
+            st = 0
+    else:
+        st = getattr(stream, "cuda_stream", stream)
+    return ctypes.c_void_p(ptr or None), ctypes.c_void_p(st or None)
+
+
+class Plan:
+    """vr_plan: one full run, then `replay()` re-launches the GPU hot path of every
+    dimension (a0..a6) with the recorded sizes, asynchronously on `stream`."""
+
+    def __init__(self, d_dist_lower_tri, n: int, max_dim: int, threshold: float = math.inf, stream=None, **opts):
+        lib = load()
+        self._keep = d_dist_lower_tri
+        ptr, st = _device_ptr_and_stream(d_dist_lower_tri, n, stream)
+        self._h = ctypes.c_void_p()
+        r = ctypes.c_void_p()
+        o = _options(**opts)
+        _check(lib.vr_plan_create(ptr, n, max_dim, threshold, ctypes.byref(o), st, ctypes.byref(self._h), ctypes.byref(r)))
+        try:
+            self.result = _collect(r)
+        finally:
+            lib.vr_free(r)
+        self.survivors = int(lib.vr_plan_survivors(self._h))
+
+    def replay(self) -> int:
+        n = ctypes.c_int64(0)
+        _check(load().vr_plan_replay(self._h, ctypes.byref(n)))
+        return int(n.value)
+
+    def check(self):
+        a, r = ctypes.c_int64(0), ctypes.c_int64(0)
+        _check(load().vr_plan_check(self._h, ctypes.byref(a), ctypes.byref(r)))
+        return int(a.value), int(r.value)
+
+    def timing(self) -> dict:
+        """Device ms of the last replay's stages + the first run's work counters."""
+        out = (ctypes.c_double * 8)()
+        _check(load().vr_plan_timing(self._h, out))
+        keys = ["ms_tables", "ms_enumerate", "ms_resolve", "ms_sort", "candidates", "survivors", "scanned", "rank_ops"]
+        return dict(zip(keys, list(out)))
+
+    def close(self):
+        if self._h:
+            load().vr_plan_free(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,240 @@
+// sort.cu — LSD radix sort of 64-bit keys and an exclusive scan, hand-written for sm_100a.
+//
+// "ascending radix sort of key = ((maxrank - rank(diam)) << cbits) |
+// cidx, which gives diam desc, cidx asc. LSD, only the significant bits".  The paper's
+// Alg 18 line 5 calls an unnamed library GPU-sort; this is our own.
+//
+// One pass per 8-bit digit, three launches per pass:
+//   rs_hist     per-tile digit histogram  (reads 8 B/key)
+//   scan        exclusive scan of the digit-major [256][tiles] histogram
+//   rs_scatter  stable in-tile ranking (warp __match_any_sync multisplit over contiguous
+//               per-warp segments), staging in shared memory sorted by digit, then
+//               coalesced runs written to the digit's global offset (reads 8 + writes 8 B/key)
+// Stability: inside a tile order is (digit, position); across tiles the digit-major scan
+// orders tiles — so each pass is a stable counting sort, as LSD requires.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "vr_common.cuh"
+#include "vr_internal.h"
+
+namespace vr {
+
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_ITEMS = 16;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 keys
+constexpr int RS_BINS = 256;
+constexpr int RS_SEG = RS_TILE / RS_WARPS;      // 512 keys per warp segment
+
+constexpr int SC_THREADS = 256;
+constexpr int SC_ITEMS = 16;
+constexpr int SC_TILE = SC_THREADS * SC_ITEMS;
+
+// ------------------------------------------------------------------ scan
+__device__ __forceinline__ uint32_t block_exclusive_scan_256(uint32_t x, uint32_t* warp_tot, uint32_t* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) warp_tot[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t t = lane < (SC_THREADS / 32) ? warp_tot[lane] : 0u;
+    uint32_t ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += y;
+    }
+    if (lane < (SC_THREADS / 32)) warp_tot[lane] = ti - t;
+    if (lane == (SC_THREADS / 32) - 1) *total = ti;
+  }
+  __syncthreads();
+  uint32_t r = warp_tot[w] + inc - x;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(SC_THREADS) scan_tile_sums(const uint32_t* __restrict__ in, size_t n, uint32_t* __restrict__ sums) {
+  __shared__ uint32_t red[SC_THREADS / 32];
+  size_t base = (size_t)blockIdx.x * SC_TILE;
+  uint32_t acc = 0;
+  for (int i = 0; i < SC_ITEMS; ++i) {
+    size_t k = base + (size_t)i * SC_THREADS + threadIdx.x;
+    if (k < n) acc += in[k];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < SC_THREADS / 32; ++w) t += red[w];
+    sums[blockIdx.x] = t;
+  }
+}
+
+// exclusive scan of one tile, plus an optional per-tile carry
+__global__ void __launch_bounds__(SC_THREADS) scan_tile_apply(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, size_t n,
+                                                              const uint32_t* __restrict__ carry) {
+  __shared__ uint32_t warp_tot[SC_THREADS / 32];
+  __shared__ uint32_t total;
+  size_t base = (size_t)blockIdx.x * SC_TILE;
+  uint32_t run = carry ? carry[blockIdx.x] : 0u;
+  for (int i = 0; i < SC_ITEMS; ++i) {
+    size_t k = base + (size_t)i * SC_THREADS + threadIdx.x;
+    uint32_t x = k < n ? in[k] : 0u;
+    uint32_t e = block_exclusive_scan_256(x, warp_tot, &total);
+    if (k < n) out[k] = run + e;
+    run += total;
+    __syncthreads();
+  }
+}
+
+size_t scan_temp_bytes(size_t n) {
+  size_t b = 0;
+  while (n > (size_t)SC_TILE) {
+    n = (n + SC_TILE - 1) / SC_TILE;
+    b += ((n * sizeof(uint32_t) + 255) / 256) * 256;
+  }
+  return b + 256;
+}
+
+// out may alias in.  temp: scan_temp_bytes(n).
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t n, void* temp, cudaStream_t st, int64_t* launches) {
+  if (n == 0) return;
+  if (n <= (size_t)SC_TILE) {
+    scan_tile_apply<<<1, SC_THREADS, 0, st>>>(in, out, n, nullptr);
+    if (launches) *launches += 1;
+    return;
+  }
+  size_t nb = (n + SC_TILE - 1) / SC_TILE;
+  uint32_t* sums = (uint32_t*)temp;
+  void* rest = (char*)temp + ((nb * sizeof(uint32_t) + 255) / 256) * 256;
+  scan_tile_sums<<<(unsigned)nb, SC_THREADS, 0, st>>>(in, n, sums);
+  exclusive_scan_u32(sums, sums, nb, rest, st, launches);
+  scan_tile_apply<<<(unsigned)nb, SC_THREADS, 0, st>>>(in, out, n, sums);
+  if (launches) *launches += 2;
+}
+
+// ------------------------------------------------------------------ radix sort
+__global__ void __launch_bounds__(RS_THREADS) rs_hist(const uint64_t* __restrict__ keys, size_t n, int shift,
+                                                      uint32_t* __restrict__ tile_hist, uint32_t ntiles) {
+  __shared__ uint32_t h[RS_BINS];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  size_t base = (size_t)blockIdx.x * RS_TILE;
+#pragma unroll 4
+  for (int i = 0; i < RS_ITEMS; ++i) {
+    size_t k = base + (size_t)i * RS_THREADS + threadIdx.x;
+    if (k < n) atomicAdd(&h[(uint32_t)(__ldg(keys + k) >> shift) & (RS_BINS - 1)], 1u);
+  }
+  __syncthreads();
+  tile_hist[(size_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, size_t n, int shift,
+                                                         const uint32_t* __restrict__ offsets, uint32_t ntiles) {
+  extern __shared__ __align__(16) unsigned char rs_smem[];
+  uint64_t* keys_s = (uint64_t*)rs_smem;                 // tile keys, input order
+  uint64_t* sorted_s = keys_s + RS_TILE;                 // tile keys, digit order
+  uint32_t* whist = (uint32_t*)(sorted_s + RS_TILE);     // [RS_WARPS][RS_BINS]
+  uint32_t* dstart = whist + RS_WARPS * RS_BINS;         // [RS_BINS]
+  uint32_t* gofs = dstart + RS_BINS;                     // [RS_BINS]
+  __shared__ uint32_t warp_tot[SC_THREADS / 32];
+  __shared__ uint32_t total;
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const size_t base = (size_t)blockIdx.x * RS_TILE;
+  const int cnt = (int)((n - base) < (size_t)RS_TILE ? (n - base) : (size_t)RS_TILE);
+
+  for (int i = threadIdx.x; i < RS_TILE; i += RS_THREADS) keys_s[i] = i < cnt ? in[base + i] : ~0ull;
+  for (int i = threadIdx.x; i < RS_WARPS * RS_BINS; i += RS_THREADS) whist[i] = 0;
+  __syncthreads();
+
+  // per-warp digit counts over the warp's contiguous segment
+  const int seg0 = w * RS_SEG;
+  for (int i = seg0 + lane; i < seg0 + RS_SEG; i += 32)
+    if (i < cnt) atomicAdd(&whist[w * RS_BINS + ((uint32_t)(keys_s[i] >> shift) & (RS_BINS - 1))], 1u);
+  __syncthreads();
+
+  // thread b: exclusive prefix over warps of digit b; tile total of digit b
+  {
+    const int b = threadIdx.x;
+    uint32_t run = 0;
+#pragma unroll
+    for (int q = 0; q < RS_WARPS; ++q) {
+      uint32_t t = whist[q * RS_BINS + b];
+      whist[q * RS_BINS + b] = run;
+      run += t;
+    }
+    uint32_t e = block_exclusive_scan_256(run, warp_tot, &total);
+    dstart[b] = e;
+    gofs[b] = offsets[(size_t)b * ntiles + blockIdx.x];
+  }
+  __syncthreads();
+
+  // stable ranking: each warp walks its segment in order, 32 keys per step
+  for (int i0 = seg0; i0 < seg0 + RS_SEG; i0 += 32) {
+    const int i = i0 + lane;
+    const bool valid = i < cnt;
+    const uint64_t k = keys_s[i];
+    const uint32_t dg = valid ? ((uint32_t)(k >> shift) & (RS_BINS - 1)) : (RS_BINS + lane);
+    const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+    uint32_t pos = 0;
+    if (valid) pos = dstart[dg] + whist[w * RS_BINS + dg] + __popc(peers & lanemask_lt());
+    __syncwarp();
+    if (valid && (lane == 31 - __clz(peers))) whist[w * RS_BINS + dg] += __popc(peers);
+    if (valid) sorted_s[pos] = k;
+    __syncwarp();
+  }
+  __syncthreads();
+
+  for (int j = threadIdx.x; j < cnt; j += RS_THREADS) {
+    const uint64_t k = sorted_s[j];
+    const uint32_t dg = (uint32_t)(k >> shift) & (RS_BINS - 1);
+    out[(size_t)gofs[dg] + (size_t)(j - (int)dstart[dg])] = k;
+  }
+}
+
+static size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+
+size_t radix_sort_temp_bytes(size_t n) {
+  size_t ntiles = (n + RS_TILE - 1) / RS_TILE;
+  size_t hist = (size_t)RS_BINS * ntiles;
+  return align256(hist * sizeof(uint32_t)) + scan_temp_bytes(hist);
+}
+
+static bool g_rs_attr_done = false;
+
+// Sorts keys[0..n) ascending on bits [begin_bit, end_bit).  alt is a ping-pong buffer of
+// n keys.  Returns the buffer holding the result (keys or alt).
+uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit, int end_bit, void* temp,
+                         cudaStream_t st, int64_t* launches) {
+  if (n <= 1 || end_bit <= begin_bit) return keys;
+  const size_t smem = 2 * RS_TILE * sizeof(uint64_t) + (RS_WARPS * RS_BINS + 2 * RS_BINS) * sizeof(uint32_t);
+  if (!g_rs_attr_done) {
+    cudaFuncSetAttribute(rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    g_rs_attr_done = true;
+  }
+  const uint32_t ntiles = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
+  uint32_t* hist = (uint32_t*)temp;
+  void* scan_tmp = (char*)temp + align256((size_t)RS_BINS * ntiles * sizeof(uint32_t));
+  uint64_t* src = keys;
+  uint64_t* dst = alt;
+  for (int shift = begin_bit; shift < end_bit; shift += 8) {
+    rs_hist<<<ntiles, RS_THREADS, 0, st>>>(src, n, shift, hist, ntiles);
+    exclusive_scan_u32(hist, hist, (size_t)RS_BINS * ntiles, scan_tmp, st, launches);
+    rs_scatter<<<ntiles, RS_THREADS, smem, st>>>(src, dst, n, shift, hist, ntiles);
+    if (launches) *launches += 2;
+    uint64_t* t = src; src = dst; dst = t;
+  }
+  return src;
+}
+
+}  // namespace vr

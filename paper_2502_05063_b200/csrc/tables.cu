@@ -1,0 +1,142 @@
+// tables.cu — step a0: the device tables every later kernel reads.
+//
+//   1. tb_edge_keys : validate the fp32 lower-distance input (VR_EINPUT on NaN / negative)
+//                     and write one 64-bit key per edge, (fp32 bits << kbits) | (N-1-k),
+//                     k = lower-distance index = edge cidx (Eq 5.6: C(i,2) + j).
+//   2. tb_rowmax    : row maxima of the symmetric matrix (enclosing radius, §5.2.12).
+//   3. radix sort of the edge keys — ascending = diameter ascending, cidx DEscending:
+//                     exactly the §5.1.4 filtration order of the edges (dimension 0 walks
+//                     it for union-find) and the sorted distance list the ranks index.
+//   4. tb_finalize  : R = min_i rowmax_i, t = threshold or R when threshold is
+//                     +inf (Prop 5.2.13), m = #edges with d <= t (inclusive, Eq 5.3).
+//   5. tb_rank      : rank[i][j] = index of the first sorted edge with the value d(i,j)
+//                     (a lower_bound), or RINF when d(i,j) > t.  Equal distances get equal
+//                     ranks and the order is kept, so rank comparisons are the paper's
+//                     diameter comparisons, exactly (reading A11: no arithmetic on values).
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "vr_common.cuh"
+#include "vr_internal.h"
+
+namespace vr {
+
+__device__ __forceinline__ float lt_at(const float* __restrict__ lt, int64_t i, int64_t j) {
+  if (i == j) return 0.0f;
+  if (i < j) { int64_t t = i; i = j; j = t; }
+  return __ldg(lt + i * (i - 1) / 2 + j);
+}
+
+__device__ __forceinline__ uint32_t dist_bits(float x) {
+  // non-negative fp32 values order like their uint32 bit patterns; map -0.0 to +0.0
+  return x == 0.0f ? 0u : __float_as_uint(x);
+}
+
+__global__ void tb_edge_keys(const float* __restrict__ lt, uint64_t N, int kbits, uint64_t* __restrict__ keys,
+                             TablesOut* __restrict__ out) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += (uint64_t)gridDim.x * blockDim.x) {
+    float x = __ldg(lt + k);
+    if (!(x >= 0.0f)) atomicOr(&out->err, 1u);  // NaN or negative
+    keys[k] = ((uint64_t)dist_bits(x) << kbits) | (N - 1 - k);
+  }
+}
+
+__global__ void tb_rowmax(const float* __restrict__ lt, int64_t n, uint32_t* __restrict__ rowmax) {
+  __shared__ uint32_t red[32];
+  const int64_t i = blockIdx.x;
+  uint32_t m = 0;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    uint32_t b = dist_bits(lt_at(lt, i, j));
+    m = b > m ? b : m;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) { uint32_t y = __shfl_xor_sync(0xffffffffu, m, o); m = y > m ? y : m; }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t r = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = red[w] > r ? red[w] : r;
+    rowmax[i] = r;
+  }
+}
+
+__global__ void tb_finalize(const uint32_t* __restrict__ rowmax, int64_t n, float threshold, const uint64_t* __restrict__ sorted,
+                            uint64_t N, int kbits, TablesOut* __restrict__ out) {
+  __shared__ uint32_t red[32];
+  uint32_t m = 0xFFFFFFFFu;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = rowmax[i] < m ? rowmax[i] : m;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) { uint32_t y = __shfl_xor_sync(0xffffffffu, m, o); m = y < m ? y : m; }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t R = 0xFFFFFFFFu;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) R = red[w] < R ? red[w] : R;
+    if (n < 2) R = 0;  // A27: n = 1 -> R = 0
+    const uint32_t tb = isinf(threshold) ? R : dist_bits(threshold);
+    // m = number of sorted keys whose fp32 bits are <= tb (upper bound)
+    uint64_t lo = 0, hi = N;
+    while (lo < hi) {
+      uint64_t mid = (lo + hi) >> 1;
+      if ((sorted[mid] >> kbits) <= (uint64_t)tb) lo = mid + 1; else hi = mid;
+    }
+    out->tbits = tb;
+    out->m_le_t = lo;
+  }
+}
+
+__global__ void tb_rank(const float* __restrict__ lt, int64_t n, const uint64_t* __restrict__ sorted, int kbits,
+                        const TablesOut* __restrict__ tout, uint32_t* __restrict__ rank) {
+  const uint32_t tb = tout->tbits;
+  const uint64_t m = tout->m_le_t;
+  const int64_t i = blockIdx.y;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t r;
+    if (i == j) {
+      r = 0;
+    } else {
+      const uint32_t b = dist_bits(lt_at(lt, i, j));
+      if (b > tb) {
+        r = VR_RINF;
+      } else {
+        const uint64_t x = (uint64_t)b << kbits;
+        uint64_t lo = 0, hi = m;
+        while (lo < hi) {
+          uint64_t mid = (lo + hi) >> 1;
+          if (__ldg(sorted + mid) < x) lo = mid + 1; else hi = mid;
+        }
+        r = (uint32_t)lo;
+      }
+    }
+    rank[(size_t)i * (size_t)n + (size_t)j] = r;
+  }
+}
+
+static int bits_for(uint64_t x) {  // number of bits to represent values 0..x
+  int b = 0;
+  while (b < 64 && (x >> b) != 0) ++b;
+  return b ? b : 1;
+}
+
+void launch_tables(const float* d_lt, int64_t n, float threshold, uint64_t* keys64, uint64_t* alt64, uint32_t* rowmax,
+                   void* sort_temp, uint32_t* rank, TablesOut* d_out, uint64_t** sorted_out, cudaStream_t st,
+                   int64_t* launches) {
+  const uint64_t N = (uint64_t)n * (uint64_t)(n - 1) / 2;
+  const int kbits = bits_for(N ? N - 1 : 0);
+  cudaMemsetAsync(d_out, 0, sizeof(TablesOut), st);
+  uint64_t* sorted = keys64;
+  if (N) {
+    unsigned g = (unsigned)((N + 255) / 256 < 148u * 16u ? (N + 255) / 256 : 148u * 16u);
+    tb_edge_keys<<<g, 256, 0, st>>>(d_lt, N, kbits, keys64, d_out);
+    sorted = radix_sort_u64(keys64, alt64, N, 0, 31 + kbits, sort_temp, st, launches);
+    *launches += 1;
+  }
+  tb_rowmax<<<(unsigned)n, 256, 0, st>>>(d_lt, n, rowmax);
+  tb_finalize<<<1, 1024, 0, st>>>(rowmax, n, threshold, sorted, N, kbits, d_out);
+  dim3 grid((unsigned)((n + 255) / 256), (unsigned)n);
+  tb_rank<<<grid, 256, 0, st>>>(d_lt, n, sorted, kbits, d_out, rank);
+  *launches += 3;
+  *sorted_out = sorted;
+}
+
+}  // namespace vr

@@ -1,0 +1,654 @@
+// vr_api.cu — the C ABI declared in include/vr.h and the per-call orchestration.
+//
+// Per call (SURVEY.md §3 "New vr_barcodes"):
+//   a0  tables on the device (tables.cu): edge keys + radix sort, enclosing radius,
+//       threshold, rank matrix; binomial table (host-built, copied once)
+//   dim 0 on the host (union-find over the sorted edges, §5.2.5) -> death edges
+//   for d = 1..max_dim:
+//       k_enumerate (a1 + a5 phase 1 + a3)   -> queue of non-proven columns
+//       k_resolve   (a5 phase 2 + a2 + a6)   -> residual columns (non-apparent, non-cleared)
+//       radix sort of the residual columns into coboundary order (a4)
+//       host residual reduction (off path)    -> pairs of dim d, deaths for d+1
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/vr.h"
+#include "vr_common.cuh"
+#include "vr_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct VrError : std::runtime_error {
+  int code;
+  VrError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CUDA_TRY(x)                                                                                 \
+  do {                                                                                              \
+    cudaError_t e_ = (x);                                                                           \
+    if (e_ != cudaSuccess) {                                                                        \
+      int code_ = (e_ == cudaErrorMemoryAllocation) ? VR_ECAPACITY : VR_EDEVICE;                    \
+      throw VrError(code_, std::string(#x) + ": " + cudaGetErrorString(e_));                        \
+    }                                                                                               \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  void ensure(size_t b) {
+    if (b <= bytes && p) return;
+    release();
+    if (b == 0) b = 16;
+    CUDA_TRY(cudaMalloc(&p, b));
+    bytes = b;
+  }
+  template <class T> T* as() const { return (T*)p; }
+};
+
+int bits_for(uint64_t x) {
+  int b = 0;
+  while (b < 64 && (x >> b) != 0) ++b;
+  return b ? b : 1;
+}
+
+double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+struct Chunk {
+  uint64_t row_begin, row_end, queued;
+};
+
+struct DimRun {
+  vr::DimParams p{};
+  std::vector<Chunk> chunks;
+  uint64_t residual = 0;
+  int sort_bits = 0;
+  DevBuf deaths_in;  // sorted death cidx of dimension d-1 (clearing input)
+  int64_t ndeaths_in = 0;
+};
+
+}  // namespace
+
+struct vr_result {
+  int32_t max_dim = 0;
+  float tused = 0.0f;
+  std::vector<std::vector<vr_pair>> pairs;
+  std::vector<std::vector<vr_index_pair>> ipairs;
+  std::vector<vr_stats> stats;
+};
+
+struct vr_plan {
+  int64_t n = 0;
+  int32_t D = 0;
+  float threshold = 0.0f;
+  vr_options opt{};
+  cudaStream_t st = nullptr;
+  const float* d_lt = nullptr;
+  uint64_t N = 0;
+  int kbits = 1, kmax = 0;
+  DevBuf rank, binom, keys, alt, rowmax, sort_tmp, tout, ctrs, queue, resid, resid_alt, app_pairs, lt_copy;
+  uint64_t qcap = 0, rcap = 0, app_cap = 0;
+  uint32_t maxr = 0;
+  uint64_t m = 0;
+  std::vector<DimRun> dims;  // index d (1..D), dims[0] unused
+  int64_t survivors_total = 0;
+  int64_t apparent_total = 0, residual_total = 0;
+  int64_t launches = 0;
+  // work counters of the first run (for the roofline accounting)
+  double work_candidates = 0, work_scanned = 0, work_rank_ops = 0;
+  // replay timing: event pairs per stage (0 tables, 1 enumerate, 2 resolve, 3 sort)
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stage_ev[4];
+  int used_events[4] = {0, 0, 0, 0};
+  ~vr_plan() {
+    for (auto& v : stage_ev)
+      for (auto& e : v) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  }
+};
+
+namespace {
+
+const int kDefaultSteps = 16;
+
+uint64_t binom_host(uint64_t n, uint64_t k) {
+  if (k > n) return 0;
+  unsigned __int128 c = 1;
+  for (uint64_t i = 1; i <= k; ++i) {
+    c = c * (n - k + i) / i;
+    if (c > ((unsigned __int128)1 << 64) - 1) return UINT64_MAX;
+  }
+  return (uint64_t)c;
+}
+
+void check_args(const void* lt, int64_t n, int32_t max_dim, float threshold) {
+  if (n < 1) throw VrError(VR_EINVAL, "n must be >= 1");
+  if (max_dim < 0 || max_dim > VR_MAX_DIM) throw VrError(VR_EINVAL, "max_dim must be in [0, VR_MAX_DIM]");
+  if (std::isnan(threshold) || threshold < 0) throw VrError(VR_EINVAL, "threshold must be >= 0 or +inf");
+  if (n >= 2 && !lt) throw VrError(VR_EINVAL, "dist_lower_tri is NULL");
+  if (n > 65535) throw VrError(VR_ECAPACITY, "n > 65535 is not supported (rank matrix layout)");
+  // C(n, max_dim + 2) < 2^63: every cofacet index must fit a signed 64-bit
+  for (int k = 1; k <= max_dim + 2; ++k) {
+    uint64_t c = binom_host((uint64_t)n, (uint64_t)k);
+    if (c == UINT64_MAX || c >= (1ull << 63))
+      throw VrError(VR_ECAPACITY, "C(n, max_dim+2) >= 2^63: simplex indices do not fit 64 bits");
+  }
+}
+
+// ------------------------------------------------------------------ the run
+void run_full(vr_plan& P, vr_result* R) {
+  const int64_t n = P.n;
+  const int D = P.D;
+  cudaStream_t st = P.st;
+  P.N = (uint64_t)n * (uint64_t)(n - 1) / 2;
+  P.kbits = bits_for(P.N ? P.N - 1 : 0);
+  P.kmax = D + 2;
+
+  // binomial table C(v, k), v in [0, n], k in [0, D+2], layout [k][v]
+  std::vector<uint64_t> hb((size_t)(P.kmax + 1) * (size_t)(n + 1));
+  for (int k = 0; k <= P.kmax; ++k)
+    for (int64_t v = 0; v <= n; ++v) hb[(size_t)k * (size_t)(n + 1) + (size_t)v] = binom_host((uint64_t)v, (uint64_t)k);
+
+  // ---------------- device memory for the tables
+  size_t free_b = 0, total_b = 0;
+  CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  const size_t need_tables = (size_t)n * (size_t)n * 4 + 2 * (size_t)P.N * 8 + hb.size() * 8;
+  if (need_tables > free_b) throw VrError(VR_ECAPACITY, "device memory too small for the tables");
+  P.binom.ensure(hb.size() * 8);
+  P.rank.ensure((size_t)n * (size_t)n * 4);
+  P.keys.ensure(std::max<size_t>(P.N, 1) * 8);
+  P.alt.ensure(std::max<size_t>(P.N, 1) * 8);
+  P.rowmax.ensure((size_t)n * 4);
+  P.tout.ensure(sizeof(vr::TablesOut));
+  P.ctrs.ensure(sizeof(vr::DimCounters) * (size_t)(D + 1));
+  P.sort_tmp.ensure(vr::radix_sort_temp_bytes(std::max<size_t>(P.N, 1)));
+  CUDA_TRY(cudaMemcpyAsync(P.binom.p, hb.data(), hb.size() * 8, cudaMemcpyHostToDevice, st));
+
+  cudaEvent_t ev[8];
+  for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() { for (int i = 0; i < 8; ++i) cudaEventDestroy(e[i]); }
+  } evg{ev};
+
+  // ---------------- a0
+  uint64_t* sorted = nullptr;
+  CUDA_TRY(cudaEventRecord(ev[0], st));
+  vr::launch_tables(P.d_lt, n, P.threshold, P.keys.as<uint64_t>(), P.alt.as<uint64_t>(), P.rowmax.as<uint32_t>(),
+                    P.sort_tmp.p, P.rank.as<uint32_t>(), P.tout.as<vr::TablesOut>(), &sorted, st, &P.launches);
+  CUDA_TRY(cudaGetLastError());
+  vr::TablesOut to{};
+  CUDA_TRY(cudaMemcpyAsync(&to, P.tout.p, sizeof to, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaEventRecord(ev[1], st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (to.err) throw VrError(VR_EINPUT, "dist_lower_tri holds a negative or NaN distance");
+  float tms = 0;
+  cudaEventElapsedTime(&tms, ev[0], ev[1]);
+  float tused;
+  std::memcpy(&tused, &to.tbits, 4);
+  P.m = to.m_le_t;
+  P.maxr = P.m ? (uint32_t)(P.m - 1) : 0;
+  const int rbits = bits_for(P.maxr);
+
+  if (R) {
+    R->max_dim = D;
+    R->tused = tused;
+    R->pairs.assign((size_t)D + 1, {});
+    R->ipairs.assign((size_t)D + 1, {});
+    R->stats.assign((size_t)D + 1, vr_stats{});
+  }
+  std::vector<vr::HostPairs> hp((size_t)D + 1);
+
+  // ---------------- host copies for the off-path steps (sorted edges, rank matrix)
+  auto tx0 = std::chrono::steady_clock::now();
+  vr::HostMatrix M;
+  M.n = n;
+  M.kmax = P.kmax;
+  M.binom = hb;
+  std::vector<uint64_t> h_edges((size_t)P.m);
+  if (P.m) CUDA_TRY(cudaMemcpy(h_edges.data(), sorted, (size_t)P.m * 8, cudaMemcpyDeviceToHost));
+  M.value.resize((size_t)P.m);
+  for (uint64_t r = 0; r < P.m; ++r) {
+    uint32_t fb = (uint32_t)(h_edges[(size_t)r] >> P.kbits);
+    std::memcpy(&M.value[(size_t)r], &fb, 4);
+  }
+  if (D >= 1 && P.m) {
+    M.rank.resize((size_t)n * (size_t)n);
+    CUDA_TRY(cudaMemcpy(M.rank.data(), P.rank.p, M.rank.size() * 4, cudaMemcpyDeviceToHost));
+  }
+  const double ms_tx0 = ms_since(tx0);
+
+  // ---------------- dimension 0
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<uint64_t> deaths;
+  vr::dim0_union_find(n, h_edges.data(), P.m, P.kbits, hp[0], deaths);
+  if (R) {
+    vr_stats& s0 = R->stats[0];
+    s0.candidates = n;
+    s0.survivors = n;
+    s0.ms_residual = ms_since(t0);
+    s0.ms_enumerate = tms;
+    s0.ms_transfer = ms_tx0;
+  }
+
+  // ---------------- dimensions 1..D
+  P.dims.clear();
+  P.dims.resize((size_t)D + 1);
+  const int steps = P.opt.apparent_steps > 0 ? P.opt.apparent_steps : kDefaultSteps;
+  for (int d = 1; d <= D; ++d) {
+    DimRun& dr = P.dims[(size_t)d];
+    vr_stats stt{};
+    const uint64_t cand = binom_host((uint64_t)n, (uint64_t)d + 1);
+    stt.candidates = (int64_t)cand;
+    // clearing input: deaths of dimension d-1
+    auto tx = std::chrono::steady_clock::now();
+    dr.ndeaths_in = (int64_t)deaths.size();
+    dr.deaths_in.ensure(std::max<size_t>(deaths.size(), 1) * 8);
+    if (!deaths.empty())
+      CUDA_TRY(cudaMemcpyAsync(dr.deaths_in.p, deaths.data(), deaths.size() * 8, cudaMemcpyHostToDevice, st));
+    double ms_tx = ms_since(tx);
+    if (cand == 0 || P.m == 0) {
+      if (R) R->stats[(size_t)d] = stt;
+      deaths.clear();
+      continue;
+    }
+    const int cbits = bits_for(cand - 1);
+    if (rbits + cbits > 64)
+      throw VrError(VR_ECAPACITY, "column key (rank bits + cidx bits) does not fit 64 bits");
+    vr::DimParams& p = dr.p;
+    p.d = d;
+    p.n = n;
+    p.maxr = P.maxr;
+    p.cbits = cbits;
+    p.steps = steps;
+    const uint64_t rows = binom_host((uint64_t)n, (uint64_t)d);
+    dr.sort_bits = rbits + cbits;
+
+    // queue capacity: every candidate, bounded by a share of free device memory
+    CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    uint64_t qmax = (uint64_t)(free_b / 4 / 8);
+    const uint64_t qwant = std::min<uint64_t>(cand, qmax);
+    if (P.qcap < qwant) {
+      P.queue.ensure((size_t)qwant * 8);
+      P.qcap = qwant;
+    }
+    uint64_t rows_per_chunk = rows;
+    if (cand > P.qcap) rows_per_chunk = std::max<uint64_t>(1, P.qcap / (uint64_t)n);
+    uint64_t app_cap = 0;
+    uint64_t* app_ptr = nullptr;
+    if (P.opt.index_pairs) {
+      app_cap = cand;
+      P.app_pairs.ensure((size_t)app_cap * 16);
+      app_ptr = P.app_pairs.as<uint64_t>();
+    }
+    vr::DimCounters* ctr = P.ctrs.as<vr::DimCounters>() + d;
+    CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(vr::DimCounters), st));
+    dr.chunks.clear();
+    float t_enum = 0, t_res = 0;
+    uint64_t resid_count = 0;
+    for (uint64_t rb = 0; rb < rows; rb += rows_per_chunk) {
+      const uint64_t re = std::min(rows, rb + rows_per_chunk);
+      p.row_begin = rb;
+      p.row_end = re;
+      CUDA_TRY(cudaMemsetAsync(&ctr->row_next, 0, 8, st));
+      CUDA_TRY(cudaMemsetAsync(&ctr->queued, 0, 8, st));
+      CUDA_TRY(cudaEventRecord(ev[2], st));
+      vr::launch_enumerate(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, P.queue.as<uint64_t>(), P.qcap,
+                           ctr, app_ptr, app_cap, st, &P.launches);
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaEventRecord(ev[3], st));
+      unsigned long long q = 0;
+      CUDA_TRY(cudaMemcpyAsync(&q, &ctr->queued, 8, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      if (q > P.qcap) throw VrError(VR_ECAPACITY, "apparent-phase queue overflow");
+      float x = 0;
+      cudaEventElapsedTime(&x, ev[2], ev[3]);
+      t_enum += x;
+      // residual capacity: what is there plus everything queued
+      if (P.rcap < resid_count + q || !P.resid.p) {
+        const uint64_t ncap = std::max<uint64_t>(std::max<uint64_t>(P.rcap * 2, resid_count + q), 1024);
+        DevBuf nb;
+        nb.ensure((size_t)ncap * 8);
+        if (resid_count) CUDA_TRY(cudaMemcpyAsync(nb.p, P.resid.p, resid_count * 8, cudaMemcpyDeviceToDevice, st));
+        std::swap(P.resid.p, nb.p);
+        std::swap(P.resid.bytes, nb.bytes);
+        CUDA_TRY(cudaStreamSynchronize(st));
+        P.rcap = ncap;
+      }
+      CUDA_TRY(cudaEventRecord(ev[4], st));
+      vr::launch_resolve(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, P.queue.as<uint64_t>(), q,
+                         dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, P.resid.as<uint64_t>(), P.rcap, ctr, app_ptr,
+                         app_cap, st, &P.launches);
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaEventRecord(ev[5], st));
+      unsigned long long rc = 0;
+      CUDA_TRY(cudaMemcpyAsync(&rc, &ctr->residual, 8, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      cudaEventElapsedTime(&x, ev[4], ev[5]);
+      t_res += x;
+      resid_count = rc;
+      dr.chunks.push_back(Chunk{rb, re, q});
+    }
+    dr.residual = resid_count;
+    // a4: sort the residual columns into coboundary order
+    P.resid_alt.ensure(std::max<uint64_t>(resid_count, 1) * 8);
+    size_t stmp = vr::radix_sort_temp_bytes(std::max<uint64_t>(resid_count, 1));
+    if (P.sort_tmp.bytes < stmp) P.sort_tmp.ensure(stmp);
+    CUDA_TRY(cudaEventRecord(ev[6], st));
+    uint64_t* rsorted = vr::radix_sort_u64(P.resid.as<uint64_t>(), P.resid_alt.as<uint64_t>(), resid_count, 0,
+                                           dr.sort_bits, P.sort_tmp.p, st, &P.launches);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(ev[7], st));
+    vr::DimCounters hc{};
+    CUDA_TRY(cudaMemcpyAsync(&hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, st));
+    std::vector<uint64_t> hkeys((size_t)resid_count);
+    tx = std::chrono::steady_clock::now();
+    CUDA_TRY(cudaStreamSynchronize(st));
+    float t_sort = 0;
+    cudaEventElapsedTime(&t_sort, ev[6], ev[7]);
+    if (resid_count) CUDA_TRY(cudaMemcpy(hkeys.data(), rsorted, resid_count * 8, cudaMemcpyDeviceToHost));
+    ms_tx += ms_since(tx);
+    std::vector<uint64_t> app_h;
+    if (P.opt.index_pairs && hc.app_pairs) {
+      app_h.resize((size_t)std::min<uint64_t>(hc.app_pairs, app_cap) * 2);
+      CUDA_TRY(cudaMemcpy(app_h.data(), app_ptr, app_h.size() * 8, cudaMemcpyDeviceToHost));
+    }
+    // off path: residual reduction on the host
+    auto tr = std::chrono::steady_clock::now();
+    vr::ResidualStats rst;
+    vr::residual_reduce(M, d, P.maxr, cbits, hkeys.data(), resid_count, P.opt.residual_mode, hp[(size_t)d], deaths, rst);
+    stt.ms_residual = ms_since(tr);
+    stt.survivors = (int64_t)hc.survivors;
+    stt.apparent = (int64_t)(hc.apparent1 + hc.apparent2);
+    stt.cleared = (int64_t)hc.cleared;
+    stt.residual_columns = (int64_t)resid_count;
+    stt.emergent = rst.emergent;
+    stt.scanned = (int64_t)hc.scanned;
+    P.work_candidates += (double)cand;
+    P.work_scanned += (double)hc.scanned;
+    P.work_rank_ops += (double)(d + 1) * ((double)cand + (double)hc.scanned);
+    stt.queued = (int64_t)hc.queued;  // last chunk only when chunked
+    if (dr.chunks.size() > 1) {
+      stt.queued = 0;
+      for (auto& c : dr.chunks) stt.queued += (int64_t)c.queued;
+    }
+    stt.ms_enumerate = t_enum;
+    stt.ms_resolve = t_res;
+    stt.ms_sort = t_sort;
+    stt.ms_transfer = ms_tx;
+    P.survivors_total += stt.survivors;
+    P.apparent_total += stt.apparent;
+    P.residual_total += (int64_t)resid_count;
+    if (R) {
+      R->stats[(size_t)d] = stt;
+      if (P.opt.index_pairs)
+        for (size_t i = 0; i + 1 < app_h.size(); i += 2) R->ipairs[(size_t)d].push_back(vr_index_pair{app_h[i], app_h[i + 1]});
+    }
+  }
+
+  // ---------------- result
+  if (R) {
+    for (int d = 0; d <= D; ++d) {
+      const vr::HostPairs& h = hp[(size_t)d];
+      vr_stats& s = R->stats[(size_t)d];
+      auto& out = R->pairs[(size_t)d];
+      for (size_t i = 0; i < h.birth.size(); ++i) {
+        const bool ess = std::isinf(h.death[i]);
+        if (ess) ++s.essential;
+        else {
+          ++s.pairs_all;
+          if (h.birth[i] < h.death[i]) ++s.pairs_positive;
+        }
+        if (ess || h.birth[i] < h.death[i] || P.opt.include_zero) out.push_back(vr_pair{h.birth[i], h.death[i]});
+        if (P.opt.index_pairs) R->ipairs[(size_t)d].push_back(vr_index_pair{h.birth_cidx[i], h.death_cidx[i]});
+      }
+      if (d >= 1) s.pairs_all += s.apparent;  // apparent pairs: zero-length, counted only
+      std::sort(out.begin(), out.end(), [](const vr_pair& a, const vr_pair& b) {
+        return a.birth < b.birth || (a.birth == b.birth && a.death < b.death);
+      });
+    }
+  }
+}
+
+// Re-launch the GPU hot path of every dimension with the recorded sizes (no host sync).
+// Each stage is bracketed by CUDA events on the plan's stream (vr_plan_timing).
+void replay(vr_plan& P) {
+  cudaStream_t st = P.st;
+  int used[4] = {0, 0, 0, 0};
+  auto ev = [&](int stage) -> std::pair<cudaEvent_t, cudaEvent_t>& {
+    auto& v = P.stage_ev[stage];
+    if ((int)v.size() <= used[stage]) {
+      std::pair<cudaEvent_t, cudaEvent_t> e;
+      CUDA_TRY(cudaEventCreate(&e.first));
+      CUDA_TRY(cudaEventCreate(&e.second));
+      v.push_back(e);
+    }
+    return v[(size_t)used[stage]++];
+  };
+  uint64_t* sorted = nullptr;
+  {
+    auto& e = ev(0);
+    cudaEventRecord(e.first, st);
+    vr::launch_tables(P.d_lt, P.n, P.threshold, P.keys.as<uint64_t>(), P.alt.as<uint64_t>(), P.rowmax.as<uint32_t>(),
+                      P.sort_tmp.p, P.rank.as<uint32_t>(), P.tout.as<vr::TablesOut>(), &sorted, st, &P.launches);
+    cudaEventRecord(e.second, st);
+  }
+  for (int d = 1; d <= P.D; ++d) {
+    DimRun& dr = P.dims[(size_t)d];
+    if (dr.chunks.empty()) continue;
+    vr::DimCounters* ctr = P.ctrs.as<vr::DimCounters>() + d;
+    cudaMemsetAsync(ctr, 0, sizeof(vr::DimCounters), st);
+    vr::DimParams p = dr.p;
+    for (const Chunk& c : dr.chunks) {
+      p.row_begin = c.row_begin;
+      p.row_end = c.row_end;
+      cudaMemsetAsync(&ctr->row_next, 0, 8, st);
+      cudaMemsetAsync(&ctr->queued, 0, 8, st);
+      auto& e1 = ev(1);
+      cudaEventRecord(e1.first, st);
+      vr::launch_enumerate(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, P.queue.as<uint64_t>(), P.qcap, ctr,
+                           nullptr, 0, st, &P.launches);
+      cudaEventRecord(e1.second, st);
+      auto& e2 = ev(2);
+      cudaEventRecord(e2.first, st);
+      vr::launch_resolve(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, P.queue.as<uint64_t>(), c.queued,
+                         dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, P.resid.as<uint64_t>(), P.rcap, ctr, nullptr, 0,
+                         st, &P.launches);
+      cudaEventRecord(e2.second, st);
+    }
+    auto& e3 = ev(3);
+    cudaEventRecord(e3.first, st);
+    vr::radix_sort_u64(P.resid.as<uint64_t>(), P.resid_alt.as<uint64_t>(), dr.residual, 0, dr.sort_bits, P.sort_tmp.p,
+                       st, &P.launches);
+    cudaEventRecord(e3.second, st);
+  }
+  P.used_events[0] = used[0]; P.used_events[1] = used[1]; P.used_events[2] = used[2]; P.used_events[3] = used[3];
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return VR_OK;
+  } catch (const VrError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host out of memory";
+    return VR_ECAPACITY;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return VR_EDEVICE;
+  }
+}
+
+vr_options default_options(const vr_options* o) {
+  vr_options d{};
+  if (o) d = *o;
+  return d;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vr_barcodes_device(const float* d_lt, int64_t n, int32_t max_dim, float threshold, const vr_options* opt, void* stream,
+                       vr_result** out) {
+  if (out) *out = nullptr;
+  return guarded([&] {
+    if (!out) throw VrError(VR_EINVAL, "out is NULL");
+    check_args(d_lt, n, max_dim, threshold);
+    vr_plan P;
+    P.n = n; P.D = max_dim; P.threshold = threshold; P.opt = default_options(opt);
+    P.st = (cudaStream_t)stream; P.d_lt = d_lt;
+    std::unique_ptr<vr_result> R(new vr_result());
+    run_full(P, R.get());
+    *out = R.release();
+  });
+}
+
+int vr_barcodes(const float* lt, int64_t n, int32_t max_dim, float threshold, const vr_options* opt, vr_result** out) {
+  if (out) *out = nullptr;
+  return guarded([&] {
+    if (!out) throw VrError(VR_EINVAL, "out is NULL");
+    check_args(lt, n, max_dim, threshold);
+    vr_options o = default_options(opt);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw VrError(VR_EDEVICE, "no CUDA device");
+    if (o.device < 0 || o.device >= ndev) throw VrError(VR_EINVAL, "options.device out of range");
+    CUDA_TRY(cudaSetDevice(o.device));
+    vr_plan P;
+    P.n = n; P.D = max_dim; P.threshold = threshold; P.opt = o;
+    CUDA_TRY(cudaStreamCreateWithFlags(&P.st, cudaStreamNonBlocking));
+    struct SG { cudaStream_t s; ~SG() { cudaStreamDestroy(s); } } sg{P.st};
+    const size_t bytes = (size_t)n * (size_t)(n - 1) / 2 * sizeof(float);
+    P.lt_copy.ensure(std::max<size_t>(bytes, 4));
+    if (bytes) CUDA_TRY(cudaMemcpyAsync(P.lt_copy.p, lt, bytes, cudaMemcpyHostToDevice, P.st));
+    P.d_lt = P.lt_copy.as<float>();
+    std::unique_ptr<vr_result> R(new vr_result());
+    run_full(P, R.get());
+    CUDA_TRY(cudaStreamSynchronize(P.st));
+    *out = R.release();
+  });
+}
+
+int32_t vr_max_dim(const vr_result* r) { return r ? r->max_dim : -1; }
+int64_t vr_num_pairs(const vr_result* r, int32_t dim) {
+  return (r && dim >= 0 && dim <= r->max_dim) ? (int64_t)r->pairs[(size_t)dim].size() : 0;
+}
+const vr_pair* vr_pairs(const vr_result* r, int32_t dim) {
+  return (r && dim >= 0 && dim <= r->max_dim && !r->pairs[(size_t)dim].empty()) ? r->pairs[(size_t)dim].data() : nullptr;
+}
+int64_t vr_num_index_pairs(const vr_result* r, int32_t dim) {
+  return (r && dim >= 0 && dim <= r->max_dim) ? (int64_t)r->ipairs[(size_t)dim].size() : 0;
+}
+const vr_index_pair* vr_index_pairs(const vr_result* r, int32_t dim) {
+  return (r && dim >= 0 && dim <= r->max_dim && !r->ipairs[(size_t)dim].empty()) ? r->ipairs[(size_t)dim].data() : nullptr;
+}
+int vr_stats_get(const vr_result* r, int32_t dim, vr_stats* s) {
+  if (!r || !s || dim < 0 || dim > r->max_dim) {
+    g_err = "vr_stats_get: bad arguments";
+    return VR_EINVAL;
+  }
+  *s = r->stats[(size_t)dim];
+  return VR_OK;
+}
+float vr_threshold_used(const vr_result* r) { return r ? r->tused : NAN; }
+void vr_free(vr_result* r) { delete r; }
+const char* vr_last_error(void) { return g_err.c_str(); }
+
+int vr_plan_create(const float* d_lt, int64_t n, int32_t max_dim, float threshold, const vr_options* opt, void* stream,
+                   vr_plan** plan, vr_result** out) {
+  if (plan) *plan = nullptr;
+  if (out) *out = nullptr;
+  return guarded([&] {
+    if (!plan) throw VrError(VR_EINVAL, "plan is NULL");
+    check_args(d_lt, n, max_dim, threshold);
+    std::unique_ptr<vr_plan> P(new vr_plan());
+    P->n = n; P->D = max_dim; P->threshold = threshold; P->opt = default_options(opt);
+    P->opt.index_pairs = 0;
+    P->st = (cudaStream_t)stream; P->d_lt = d_lt;
+    std::unique_ptr<vr_result> R(new vr_result());
+    run_full(*P, R.get());
+    CUDA_TRY(cudaStreamSynchronize(P->st));
+    P->launches = 0;
+    *plan = P.release();
+    if (out) *out = R.release();
+  });
+}
+
+int vr_plan_replay(vr_plan* P, int64_t* launches) {
+  return guarded([&] {
+    if (!P) throw VrError(VR_EINVAL, "plan is NULL");
+    const int64_t before = P->launches;
+    replay(*P);
+    CUDA_TRY(cudaGetLastError());
+    if (launches) *launches = P->launches - before;
+  });
+}
+
+int64_t vr_plan_survivors(const vr_plan* P) { return P ? P->survivors_total : 0; }
+
+int vr_plan_check(vr_plan* P, int64_t* apparent_total, int64_t* residual_total) {
+  return guarded([&] {
+    if (!P) throw VrError(VR_EINVAL, "plan is NULL");
+    std::vector<vr::DimCounters> h((size_t)P->D + 1);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), P->ctrs.p, h.size() * sizeof(vr::DimCounters), cudaMemcpyDeviceToHost, P->st));
+    CUDA_TRY(cudaStreamSynchronize(P->st));
+    int64_t a = 0, r = 0;
+    for (int d = 1; d <= P->D; ++d) {
+      if (P->dims[(size_t)d].chunks.empty()) continue;
+      a += (int64_t)(h[(size_t)d].apparent1 + h[(size_t)d].apparent2);
+      r += (int64_t)h[(size_t)d].residual;
+    }
+    if (apparent_total) *apparent_total = a;
+    if (residual_total) *residual_total = r;
+  });
+}
+
+int vr_plan_timing(vr_plan* P, double out[8]) {
+  return guarded([&] {
+    if (!P || !out) throw VrError(VR_EINVAL, "plan/out is NULL");
+    CUDA_TRY(cudaStreamSynchronize(P->st));
+    for (int k = 0; k < 4; ++k) {
+      double t = 0;
+      for (int i = 0; i < P->used_events[k]; ++i) {
+        float x = 0;
+        CUDA_TRY(cudaEventElapsedTime(&x, P->stage_ev[k][(size_t)i].first, P->stage_ev[k][(size_t)i].second));
+        t += x;
+      }
+      out[k] = t;
+    }
+    out[4] = P->work_candidates;
+    out[5] = (double)P->survivors_total;
+    out[6] = P->work_scanned;
+    out[7] = P->work_rank_ops;
+  });
+}
+
+void vr_plan_free(vr_plan* P) { delete P; }
+
+}  // extern "C"

@@ -1,0 +1,116 @@
+// vr_common.cuh — device-side building blocks shared by the libvr kernels.
+//
+// Data layout in HBM:
+//   rank   : uint32 n x n, row-major, symmetric.  rank[i*n+j] = position of the first
+//            occurrence of d(i,j) in the ascending sort of all n(n-1)/2 distances, if
+//            d(i,j) <= t, else RINF.  Ranks preserve order and equality of the fp32
+//            distances exactly, so every diameter comparison of the method (Eq 5.3, the
+//            "diam(t) = diam(s)" tests of Lemma 5.3.6) is an exact integer comparison, and
+//            a rank maps back to the fp32 distance bit-exactly (sorted[rank]).
+//   binom  : uint64 [k][v], k in [0, kmax], v in [0, n]: C(v, k) (Eq 5.6).
+//   keys   : uint64 column key = ((maxr - rank(diam)) << cbits) | cidx, so that ascending
+//            key order is coboundary order: diameter descending, cidx ascending
+//            (Fig 5.2 caption).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define VR_RINF 0xFFFFFFFFu
+
+namespace vr {
+
+struct Tables {
+  const uint32_t* __restrict__ rank;  // n*n
+  const uint64_t* __restrict__ binom; // (kmax+1)*(n+1)
+  int32_t n;
+  int32_t kmax;
+};
+
+__device__ __forceinline__ uint64_t binom(const Tables& T, int v, int k) {
+  return __ldg(T.binom + (size_t)k * (size_t)(T.n + 1) + (size_t)v);
+}
+
+__device__ __forceinline__ uint32_t rank_at(const Tables& T, int i, int j) {
+  return __ldg(T.rank + (size_t)i * (size_t)T.n + (size_t)j);
+}
+
+// Largest v in [k-1, hi-1] with C(v, k) <= x  (C(., k) is non-decreasing; C(k-1, k) = 0).
+// This is the per-vertex binary search of the combinatorial number system (A31).
+__device__ __forceinline__ int cns_find(const Tables& T, uint64_t x, int k, int hi) {
+  int lo = k - 1, h = hi - 1;  // invariant: C(lo,k) <= x
+  while (lo < h) {
+    int mid = (lo + h + 1) >> 1;
+    if (binom(T, mid, k) <= x) lo = mid; else h = mid - 1;
+  }
+  return lo;
+}
+
+// Eq 5.6 decode: cidx of a dim-d simplex -> vertices s[0] > s[1] > ... > s[d].
+template <int D>
+__device__ __forceinline__ void cns_decode(const Tables& T, uint64_t cidx, int (&s)[D + 1]) {
+  int hi = T.n;
+#pragma unroll
+  for (int p = 0; p <= D; ++p) {
+    const int k = D + 1 - p;
+    int v = cns_find(T, cidx, k, hi);
+    s[p] = v;
+    cidx -= binom(T, v, k);
+    hi = v;
+  }
+}
+
+// Eq 5.6 encode of vertices in decreasing order.
+template <int K>
+__device__ __forceinline__ uint64_t cns_encode(const Tables& T, const int (&s)[K]) {
+  uint64_t c = 0;
+#pragma unroll
+  for (int p = 0; p < K; ++p) c += binom(T, s[p], K - p);
+  return c;
+}
+
+// cidx of the cofacet s ∪ {v} (v not in s) — Eq 5.6 on the merged decreasing tuple.
+template <int D>
+__device__ __forceinline__ uint64_t cofacet_cidx(const Tables& T, const int (&s)[D + 1], int v) {
+  uint64_t c = 0;
+  int pos = 0;  // position in the merged tuple (0 = largest)
+  bool placed = false;
+#pragma unroll
+  for (int p = 0; p <= D; ++p) {
+    if (!placed && v > s[p]) { c += binom(T, v, D + 2 - pos); ++pos; placed = true; }
+    c += binom(T, s[p], D + 2 - pos);
+    ++pos;
+  }
+  if (!placed) c += binom(T, v, 1);
+  return c;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Warp-aggregated append (§5.5.3 "warp-based filtering": one atomic per warp, ballot
+// within the warp).  Every lane of the warp must call it.  Returns the slot or ~0 if
+// the lane does not append.  Order within a warp step is lane order.
+__device__ __forceinline__ unsigned long long warp_append(bool pred, unsigned long long* counter) {
+  const uint32_t m = __ballot_sync(0xffffffffu, pred);
+  if (!m) return ~0ull;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return pred ? base + (unsigned long long)__popc(m & lanemask_lt()) : ~0ull;
+}
+
+__device__ __forceinline__ bool sorted_contains(const uint64_t* __restrict__ a, int64_t n, uint64_t x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) < x) lo = mid + 1; else hi = mid;
+  }
+  return lo < n && __ldg(a + lo) == x;
+}
+
+}  // namespace vr

@@ -1,0 +1,78 @@
+// vr_internal.h — host-side interfaces between the libvr translation units (not exported).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+
+namespace vr {
+
+// ---------------------------------------------------------------- sort.cu
+size_t scan_temp_bytes(size_t n);
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t n, void* temp, cudaStream_t st, int64_t* launches);
+size_t radix_sort_temp_bytes(size_t n);
+uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit, int end_bit, void* temp,
+                         cudaStream_t st, int64_t* launches);
+
+// ---------------------------------------------------------------- tables.cu (a0)
+struct TablesOut {
+  uint32_t err;        // nonzero: a NaN or negative distance was found
+  uint32_t tbits;      // fp32 bits of the threshold actually applied
+  uint64_t m_le_t;     // number of edges with d <= t
+  uint32_t rbits_pad;
+};
+// keys64 (n(n-1)/2) and alt64 ping-pong buffers, rowmax (n), rank (n*n), out (device)
+void launch_tables(const float* d_lt, int64_t n, float threshold, uint64_t* keys64, uint64_t* alt64, uint32_t* rowmax,
+                   void* sort_temp, uint32_t* rank, TablesOut* d_out, uint64_t** sorted_out, cudaStream_t st,
+                   int64_t* launches);
+void launch_build_binom(uint64_t* binom, int64_t n, int kmax, cudaStream_t st, int64_t* launches);
+
+// ---------------------------------------------------------------- hot path kernels
+struct DimParams {
+  int d;               // column dimension
+  int64_t n;
+  uint32_t maxr;       // largest rank <= t
+  int cbits;           // bits of cidx of d-simplices
+  int steps;           // phase-1 cofacet steps
+  uint64_t row_begin, row_end;  // prefix rows [row_begin, row_end) of the d-simplices
+};
+struct DimCounters {   // device counters (unsigned long long each)
+  unsigned long long survivors, apparent1, apparent2, cleared, queued, residual, row_next, app_pairs, scanned;
+};
+void launch_enumerate(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, uint64_t* queue,
+                      uint64_t qcap, DimCounters* ctr, uint64_t* app_pairs, uint64_t app_cap, cudaStream_t st,
+                      int64_t* launches);
+void launch_resolve(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const uint64_t* queue,
+                    uint64_t qn, const uint64_t* deaths, int64_t ndeaths, uint64_t* resid, uint64_t rcap,
+                    DimCounters* ctr, uint64_t* app_pairs, uint64_t app_cap, cudaStream_t st, int64_t* launches);
+
+// ---------------------------------------------------------------- host.cpp (off-path)
+struct HostPairs {
+  std::vector<float> birth, death;               // death = +inf for essential classes
+  std::vector<uint64_t> birth_cidx, death_cidx;  // death_cidx = UINT64_MAX for essential
+  void push(float b, float d, uint64_t bc, uint64_t dc) {
+    birth.push_back(b); death.push_back(d); birth_cidx.push_back(bc); death_cidx.push_back(dc);
+  }
+};
+struct HostMatrix {
+  int64_t n = 0;
+  std::vector<float> value;     // value[rank] = the fp32 distance with that rank
+  std::vector<uint32_t> rank;   // n*n
+  std::vector<uint64_t> binom;  // (kmax+1)*(n+1)
+  int kmax = 0;
+  uint64_t C(int64_t v, int k) const { return binom[(size_t)k * (size_t)(n + 1) + (size_t)v]; }
+  uint32_t R(int64_t i, int64_t j) const { return rank[(size_t)i * (size_t)n + (size_t)j]; }
+};
+// Dim 0 (§5.2.5): union-find over the edges in filtration order.  edges_sorted are the
+// edge keys sorted ascending by (fp32 bits << 32 | ~cidx) (filtration order), first m.
+void dim0_union_find(int64_t n, const uint64_t* edges_sorted, uint64_t m, int kbits, HostPairs& out,
+                     std::vector<uint64_t>& deaths_sorted);
+// Residual reduction of the non-apparent, non-cleared columns of dimension d given in
+// coboundary order (keys ascending).  mode 0 = reduction matrix (V), 1 = oblivious.
+struct ResidualStats {
+  int64_t emergent = 0, additions = 0;
+};
+void residual_reduce(const HostMatrix& M, int d, uint32_t maxr, int cbits, const uint64_t* keys, uint64_t nkeys,
+                     int mode, HostPairs& out, std::vector<uint64_t>& deaths_sorted, ResidualStats& st);
+
+}  // namespace vr

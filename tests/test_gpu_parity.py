@@ -1,0 +1,218 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar: bit-exact.  Every birth/death is a copy of a distance-matrix entry, so the multiset
+of (birth, death) fp32 pairs must match exactly per dimension; at the index level the
+full pairing (apparent + residual + dimension-0 pairs, zero-length and essential
+included) is unique for the §5.1.4 refinement and must match too.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2502_05063_b200 as vr
+from datagen import clouds as G
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_at(lt, n, D, t):
+    return O.barcode(lt, n, D, t)
+
+
+def assert_values_equal(got: vr.Barcode, ref, D):
+    for d in range(D + 1):
+        exp = ref.positive(d)
+        assert got.pairs[d].shape == exp.shape, (d, got.pairs[d], exp)
+        assert np.array_equal(got.pairs[d].view(np.uint32), exp.view(np.uint32)), d
+
+
+def assert_index_equal(got: vr.Barcode, ref, D):
+    for d in range(D + 1):
+        g = {(int(a), int(b)) for a, b in got.index_pairs[d]}
+        assert len(g) == len(got.index_pairs[d])  # no duplicates
+        assert g == ref.index_pairs(d), d
+
+
+def assert_counts_equal(got: vr.Barcode, ref, D):
+    for d in range(D + 1):
+        s = got.stats[d]
+        assert s["pairs_all"] == ref.num_pairs_all(d), d
+        assert s["essential"] == ref.num_essential(d), d
+        if d >= 1:
+            assert s["survivors"] == ref.n_simplices[d], d
+
+
+def full_check(lt, n, D, threshold=math.inf, **opts):
+    got = vr.barcodes(lt, n, D, threshold, index_pairs=True, **opts)
+    t = got.threshold
+    ref = _oracle_at(lt, n, D, t)
+    assert_values_equal(got, ref, D)
+    assert_index_equal(got, ref, D)
+    assert_counts_equal(got, ref, D)
+    if math.isinf(threshold):  # Prop 5.2.13: t = R and t = inf report the same bars
+        assert_values_equal(got, _oracle_at(lt, n, D, math.inf), D)
+    return got, ref
+
+
+# ------------------------------------------------------------------ closed forms
+def test_unit_square():
+    got, _ = full_check(G.unit_square(), 4, 1)
+    assert got.pairs[1].tolist() == [[1.0, np.float32(math.sqrt(2))]]
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_cross_polytope(k):
+    got, _ = full_check(G.cross_polytope(k), 2 * k, k - 1)
+    assert got.pairs[k - 1].tolist() == [[np.float32(math.sqrt(2)), 2.0]]
+
+
+@pytest.mark.parametrize("n", range(6, 13))
+def test_regular_ngon(n):
+    full_check(G.regular_ngon(n), n, 1)
+
+
+def test_single_point_and_pair():
+    got = vr.barcodes(np.zeros(0, np.float32), 1, 2)
+    assert got.pairs[0].tolist() == [[0.0, math.inf]] and len(got.pairs[1]) == 0
+    got = vr.barcodes(np.array([5.0], np.float32), 2, 1)
+    assert got.pairs[0].tolist() == [[0.0, 5.0], [0.0, math.inf]]
+
+
+def test_duplicate_points_zero_length_suppressed():
+    pts = np.array([[0, 0], [0, 0], [1, 0], [1, 1]], np.float64)
+    lt = G.lower_tri_from_points(pts)
+    got, ref = full_check(lt, 4, 2)
+    assert got.stats[0]["pairs_all"] == 3 and got.stats[0]["pairs_positive"] == 2
+
+
+@pytest.mark.parametrize("n,d", [(n, d) for n in (6, 9, 14, 20) for d in (1, 2)])
+def test_thm542_all_equal_apparent_count(n, d):
+    got = vr.barcodes(G.all_equal(n), n, 2)
+    assert got.stats[d]["apparent"] == math.comb(n - 1, d + 1)
+
+
+@pytest.mark.parametrize("n", [5, 7])
+def test_fig56_lex_decreasing(n):
+    got, _ = full_check(G.fig56_lex_decreasing(n), n, 1)
+    assert got.stats[1]["apparent"] == math.comb(n - 1, 2)
+
+
+# ------------------------------------------------------------------ brute force on small random inputs
+CASES = []
+for seed in range(48):
+    n = 5 + seed % 8
+    D = 1 + seed % 3
+    kind = ["tied", "cloud", "tied2"][seed % 3]
+    thr = ["inf", "R", "q60"][(seed // 3) % 3]
+    CASES.append((seed, n, D, kind, thr))
+
+
+@pytest.mark.parametrize("seed,n,D,kind,thr", CASES)
+def test_random_small_index_level(seed, n, D, kind, thr):
+    if kind == "tied":
+        lt = G.random_tied(n, seed, levels=3)
+    elif kind == "tied2":
+        lt = G.random_tied(n, seed, levels=8)
+    else:
+        lt = G.random_cloud(n, seed)
+    t = math.inf if thr == "inf" else (O.enclosing_radius(lt, n) if thr == "R" else float(np.quantile(lt, 0.6)))
+    full_check(lt, n, D, t)
+
+
+# ------------------------------------------------------------------ configs (full where feasible, else subsampled)
+def test_config1_full():
+    cfg = G.CONFIGS["c1_circle64"]
+    got, ref = full_check(cfg.lower_tri(), cfg.n, cfg.max_dim)
+    h1 = got.pairs[1]
+    assert ((h1[:, 1] - h1[:, 0]) > 1.0).sum() == 1
+
+
+@pytest.mark.parametrize("name,m,D", [("c2_s3_192", 24, 3), ("c3_trefoil1000", 40, 2), ("c4a_sierpinski512", 40, 2),
+                                      ("c4b_torus2000", 40, 2), ("c5_o3_4096", 36, 2), ("c5_o3_4096", 22, 3)])
+def test_config_subsample(name, m, D):
+    cfg = G.CONFIGS[name]
+    full_check(cfg.lower_tri(m), m, D, cfg.threshold)
+
+
+@pytest.mark.parametrize("steps", [1, 2, 7, 64])
+def test_apparent_phase_split_invariance(steps):
+    lt = G.random_cloud(60, 3)
+    a = vr.barcodes(lt, 60, 2, apparent_steps=steps, index_pairs=True)
+    b = vr.barcodes(lt, 60, 2, apparent_steps=16, index_pairs=True)
+    for d in range(3):
+        assert np.array_equal(a.pairs[d], b.pairs[d])
+        assert {tuple(x) for x in a.index_pairs[d].tolist()} == {tuple(x) for x in b.index_pairs[d].tolist()}
+        assert a.stats[d]["apparent"] == b.stats[d]["apparent"]
+
+
+def test_residual_modes_agree():
+    cfg = G.CONFIGS["c2_s3_192"]
+    lt = cfg.lower_tri(60)
+    a = vr.barcodes(lt, 60, 3, residual_mode=0)
+    b = vr.barcodes(lt, 60, 3, residual_mode=1)
+    for d in range(4):
+        assert np.array_equal(a.pairs[d], b.pairs[d])
+
+
+def test_device_entry_matches_host_entry():
+    torch = pytest.importorskip("torch")
+    cfg = G.CONFIGS["c4a_sierpinski512"]
+    lt = cfg.lower_tri(120)
+    a = vr.barcodes(lt, 120, 2)
+    t = torch.from_numpy(lt).cuda()
+    b = vr.barcodes_device(t, 120, 2)
+    for d in range(3):
+        assert np.array_equal(a.pairs[d], b.pairs[d])
+
+
+# ------------------------------------------------------------------ full-size configs: invariants
+def _triangles_le(lt, n, t):
+    A = (G.square_from_lower_tri(lt, n) <= np.float32(t)).astype(np.float64)
+    np.fill_diagonal(A, 0)
+    return int(round(np.trace(A @ A @ A) / 6))
+
+
+@pytest.mark.parametrize("name", ["c1_circle64", "c2_s3_192", "c4a_sierpinski512", "c3_trefoil1000"])
+def test_full_config_invariants(name):
+    cfg = G.CONFIGS[name]
+    lt = cfg.lower_tri()
+    got = vr.barcodes(lt, cfg.n, cfg.max_dim, cfg.threshold)
+    t = got.threshold
+    D = cfg.max_dim
+    # survivors: edges and triangles by brute force
+    assert got.stats[1]["survivors"] == int((lt <= np.float32(t)).sum())
+    if D >= 2:
+        assert got.stats[2]["survivors"] == _triangles_le(lt, cfg.n, t)
+    # n_p = P_p + E_p + P_{p-1}
+    P = [got.stats[p]["pairs_all"] for p in range(D + 1)]
+    E = [got.stats[p]["essential"] for p in range(D + 1)]
+    for p in range(1, D + 1):
+        assert got.stats[p]["survivors"] == P[p] + E[p] + P[p - 1]
+        s = got.stats[p]
+        assert s["survivors"] == s["apparent"] + s["cleared"] + s["residual_columns"]
+    # determinism
+    again = vr.barcodes(lt, cfg.n, cfg.max_dim, cfg.threshold)
+    for d in range(D + 1):
+        assert np.array_equal(got.pairs[d], again.pairs[d])
+
+
+def _long(pairs, frac):
+    pers = pairs[:, 1] - pairs[:, 0]
+    if len(pers) == 0:
+        return 0
+    top = np.max(np.where(np.isinf(pers), 0, pers))
+    return int((pers > frac * max(top, 1e-9)).sum())
+
+
+def test_betti_circle_and_s3():
+    c1 = G.CONFIGS["c1_circle64"]
+    b = vr.barcodes(c1.lower_tri(), c1.n, 1)
+    assert ((b.pairs[1][:, 1] - b.pairs[1][:, 0]) > 1.0).sum() == 1
+    c2 = G.CONFIGS["c2_s3_192"]
+    b = vr.barcodes(c2.lower_tri(), c2.n, 3)
+    p3 = b.pairs[3][:, 1] - b.pairs[3][:, 0]
+    assert len(p3) >= 1 and np.sort(p3)[-1] > 3 * (np.sort(p3)[-2] if len(p3) > 1 else 0)
