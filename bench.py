@@ -246,13 +246,22 @@ def run_ours(args, rank, world, local_rank):
         pass
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     alu_peak = 148 * 4 * 16 * sm_mhz * 1e6 / 1e12  # T int-ops/s
-    dom = max(("ms_enumerate", "ms_resolve", "ms_sort", "ms_tables"), key=lambda k: per[k])
-    enum_ops = tm["rank_ops"]
-    achieved = enum_ops / (per["ms_enumerate"] / 1000.0) / 1e12 if per["ms_enumerate"] > 0 else None
-    roof = {"bound": "alu", "kernel": "k_enumerate", "achieved": achieved, "peak": alu_peak, "unit": "Tops/s",
+    # both hot kernels are gathers over the L2-resident rank matrix followed by integer
+    # max/compare chains; their algorithmic work is the method's rank comparisons
+    kern = {
+        "k_enumerate": (tm["rank_ops_enumerate"], per["ms_enumerate"]),
+        "k_resolve": (tm["rank_ops_resolve"], per["ms_resolve"]),
+    }
+    dom = max(kern, key=lambda k: kern[k][1])
+    ops, ms = kern[dom]
+    achieved = ops / (ms / 1000.0) / 1e12 if ms > 0 else None
+    roof = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": alu_peak, "unit": "Tops/s",
             "frac": (achieved / alu_peak) if achieved else None, "traffic": None,
-            "ops_per_launch_set": enum_ops, "dominant_stage": dom,
-            "peak_source": "derived: 148 SM x 64 ALU lanes/clk x sm_max_mhz (MEASURED_PEAKS.json)"}
+            "ops_per_step": ops, "ms_per_step": ms,
+            "all": {k: {"ops": o, "ms": m, "tops": (o / (m / 1000.0) / 1e12) if m > 0 else None}
+                    for k, (o, m) in kern.items()},
+            "peak_source": "derived: 148 SM x 64 ALU lanes/clk x sm_max_mhz (MEASURED_PEAKS.json); "
+                           "work = rank comparisons (d+1 per candidate and per scanned cofacet vertex)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,

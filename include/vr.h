@@ -149,9 +149,11 @@ int vr_plan_check(vr_plan* plan, int64_t* apparent_total, int64_t* residual_tota
  * over dimensions: [0] tables (a0), [1] enumerate + apparent phase 1, [2] apparent
  * phase 2 + clearing + compaction, [3] radix sort.  Synchronizes the plan's stream.
  * Also the algorithmic work counters of the plan's first run: [4] candidates,
- * [5] survivors, [6] cofacet vertices scanned, [7] sum over d of (d+1)*(candidates_d +
- * scanned_d) = rank comparisons of the method. */
-int vr_plan_timing(vr_plan* plan, double out[8]);
+ * [5] survivors, [6] cofacet vertices scanned (both phases), [7] rank comparisons of
+ * the enumerate kernel, sum over d of (d+1)*(candidates_d + phase-1 scanned_d), [8] rank
+ * comparisons of the resolve kernel, sum over d of (d+1)*(phase-2 scanned_d)
+ * (DESIGN.md "Roofline"). */
+int vr_plan_timing(vr_plan* plan, double out[9]);
 void vr_plan_free(vr_plan* plan);
 
 #ifdef __cplusplus

@@ -219,9 +219,10 @@ class Plan:
 
     def timing(self) -> dict:
         """Device ms of the last replay's stages + the first run's work counters."""
-        out = (ctypes.c_double * 8)()
+        out = (ctypes.c_double * 9)()
         _check(load().vr_plan_timing(self._h, out))
-        keys = ["ms_tables", "ms_enumerate", "ms_resolve", "ms_sort", "candidates", "survivors", "scanned", "rank_ops"]
+        keys = ["ms_tables", "ms_enumerate", "ms_resolve", "ms_sort", "candidates", "survivors", "scanned",
+                "rank_ops_enumerate", "rank_ops_resolve"]
         return dict(zip(keys, list(out)))
 
     def close(self):

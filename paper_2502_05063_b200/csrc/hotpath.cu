@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(HP_THREADS) k_resolve(Tables T, DimParams p, c
   if (lane == 0) {
     if (app_acc) atomicAdd(&ctr->apparent2, app_acc);
     if (clr_acc) atomicAdd(&ctr->cleared, clr_acc);
-    if (scan_acc) atomicAdd(&ctr->scanned, scan_acc);
+    if (scan_acc) atomicAdd(&ctr->scanned2, scan_acc);
   }
 }
 

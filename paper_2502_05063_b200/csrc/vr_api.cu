@@ -12,6 +12,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -120,7 +122,7 @@ struct vr_plan {
   int64_t apparent_total = 0, residual_total = 0;
   int64_t launches = 0;
   // work counters of the first run (for the roofline accounting)
-  double work_candidates = 0, work_scanned = 0, work_rank_ops = 0;
+  double work_candidates = 0, work_scanned = 0, work_rank_ops = 0, work_scanned2 = 0, work_rank_ops2 = 0;
   // replay timing: event pairs per stage (0 tables, 1 enumerate, 2 resolve, 3 sort)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stage_ev[4];
   int used_events[4] = {0, 0, 0, 0};
@@ -155,6 +157,28 @@ void check_args(const void* lt, int64_t n, int32_t max_dim, float threshold) {
     uint64_t c = binom_host((uint64_t)n, (uint64_t)k);
     if (c == UINT64_MAX || c >= (1ull << 63))
       throw VrError(VR_ECAPACITY, "C(n, max_dim+2) >= 2^63: simplex indices do not fit 64 bits");
+  }
+}
+
+// Debug aid: write the inputs of residual_reduce for dimension d (tools/residual_bench).
+void dump_residual(const char* dir, const vr::HostMatrix& M, int d, uint32_t maxr, int cbits,
+                   const std::vector<uint64_t>& keys) {
+  std::string base = std::string(dir) + "/";
+  auto wr = [&](const std::string& f, const void* p, size_t b) {
+    FILE* fp = std::fopen((base + f).c_str(), "wb");
+    if (!fp) return;
+    std::fwrite(p, 1, b, fp);
+    std::fclose(fp);
+  };
+  if (d == 1) {
+    wr("rank.bin", M.rank.data(), M.rank.size() * 4);
+    wr("values.bin", M.value.data(), M.value.size() * 4);
+  }
+  wr("keys_d" + std::to_string(d) + ".bin", keys.data(), keys.size() * 8);
+  FILE* fp = std::fopen((base + "meta_d" + std::to_string(d) + ".txt").c_str(), "w");
+  if (fp) {
+    std::fprintf(fp, "%lld %d %u %d %d\n", (long long)M.n, d, maxr, cbits, M.kmax);
+    std::fclose(fp);
   }
 }
 
@@ -386,10 +410,13 @@ void run_full(vr_plan& P, vr_result* R) {
     stt.cleared = (int64_t)hc.cleared;
     stt.residual_columns = (int64_t)resid_count;
     stt.emergent = rst.emergent;
-    stt.scanned = (int64_t)hc.scanned;
+    stt.scanned = (int64_t)(hc.scanned + hc.scanned2);
     P.work_candidates += (double)cand;
     P.work_scanned += (double)hc.scanned;
+    P.work_scanned2 += (double)hc.scanned2;
     P.work_rank_ops += (double)(d + 1) * ((double)cand + (double)hc.scanned);
+    P.work_rank_ops2 += (double)(d + 1) * (double)hc.scanned2;
+    if (const char* dump = std::getenv("VR_DUMP_RESIDUAL")) dump_residual(dump, M, d, P.maxr, cbits, hkeys);
     stt.queued = (int64_t)hc.queued;  // last chunk only when chunked
     if (dr.chunks.size() > 1) {
       stt.queued = 0;
@@ -629,7 +656,7 @@ int vr_plan_check(vr_plan* P, int64_t* apparent_total, int64_t* residual_total) 
   });
 }
 
-int vr_plan_timing(vr_plan* P, double out[8]) {
+int vr_plan_timing(vr_plan* P, double out[9]) {
   return guarded([&] {
     if (!P || !out) throw VrError(VR_EINVAL, "plan/out is NULL");
     CUDA_TRY(cudaStreamSynchronize(P->st));
@@ -644,8 +671,9 @@ int vr_plan_timing(vr_plan* P, double out[8]) {
     }
     out[4] = P->work_candidates;
     out[5] = (double)P->survivors_total;
-    out[6] = P->work_scanned;
+    out[6] = P->work_scanned + P->work_scanned2;
     out[7] = P->work_rank_ops;
+    out[8] = P->work_rank_ops2;
   });
 }
 

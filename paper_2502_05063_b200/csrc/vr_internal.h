@@ -37,7 +37,7 @@ struct DimParams {
   uint64_t row_begin, row_end;  // prefix rows [row_begin, row_end) of the d-simplices
 };
 struct DimCounters {   // device counters (unsigned long long each)
-  unsigned long long survivors, apparent1, apparent2, cleared, queued, residual, row_next, app_pairs, scanned;
+  unsigned long long survivors, apparent1, apparent2, cleared, queued, residual, row_next, app_pairs, scanned, scanned2;
 };
 void launch_enumerate(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, uint64_t* queue,
                       uint64_t qcap, DimCounters* ctr, uint64_t* app_pairs, uint64_t app_cap, cudaStream_t st,

@@ -91,13 +91,15 @@ def test_duplicate_points_zero_length_suppressed():
 
 @pytest.mark.parametrize("n,d", [(n, d) for n in (6, 9, 14, 20) for d in (1, 2)])
 def test_thm542_all_equal_apparent_count(n, d):
-    got = vr.barcodes(G.all_equal(n), n, 2)
+    got = vr.barcodes(G.all_equal(n), n, 2, 1.0)
     assert got.stats[d]["apparent"] == math.comb(n - 1, d + 1)
 
 
 @pytest.mark.parametrize("n", [5, 7])
 def test_fig56_lex_decreasing(n):
-    got, _ = full_check(G.fig56_lex_decreasing(n), n, 1)
+    # §5.4.3 is a statement about the FULL Rips filtration: threshold = the max distance
+    lt = G.fig56_lex_decreasing(n)
+    got, _ = full_check(lt, n, 1, float(lt.max()))
     assert got.stats[1]["apparent"] == math.comb(n - 1, 2)
 
 

@@ -1,0 +1,57 @@
+// residual_bench.cpp — time libvr's host residual reduction on inputs dumped by a GPU run
+// (VR_DUMP_RESIDUAL=<dir>).  Diagnostics only.
+//   g++ -O3 -std=c++17 -I paper_2502_05063_b200/csrc tools/residual_bench.cpp \
+//       paper_2502_05063_b200/csrc/host.cpp -o /tmp/residual_bench && /tmp/residual_bench <dir> <d> [mode]
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "vr_internal.h"
+
+template <class T>
+static std::vector<T> rd(const std::string& f) {
+  std::vector<T> v;
+  FILE* fp = std::fopen(f.c_str(), "rb");
+  if (!fp) { std::perror(f.c_str()); std::exit(1); }
+  std::fseek(fp, 0, SEEK_END);
+  long b = std::ftell(fp);
+  std::fseek(fp, 0, SEEK_SET);
+  v.resize((size_t)b / sizeof(T));
+  if (std::fread(v.data(), 1, (size_t)b, fp) != (size_t)b) std::exit(2);
+  std::fclose(fp);
+  return v;
+}
+
+int main(int argc, char** argv) {
+  std::string dir = argv[1];
+  int d = std::atoi(argv[2]);
+  int mode = argc > 3 ? std::atoi(argv[3]) : 0;
+  long long n; int dd, cbits, kmax; unsigned maxr;
+  FILE* fp = std::fopen((dir + "/meta_d" + std::to_string(d) + ".txt").c_str(), "r");
+  if (std::fscanf(fp, "%lld %d %u %d %d", &n, &dd, &maxr, &cbits, &kmax) != 5) return 3;
+  std::fclose(fp);
+  vr::HostMatrix M;
+  M.n = n; M.kmax = kmax;
+  M.rank = rd<uint32_t>(dir + "/rank.bin");
+  M.value = rd<float>(dir + "/values.bin");
+  M.binom.resize((size_t)(kmax + 1) * (size_t)(n + 1));
+  for (int k = 0; k <= kmax; ++k)
+    for (long long v = 0; v <= n; ++v) {
+      unsigned __int128 c = 1;
+      if (k > v) c = 0;
+      else for (int i = 1; i <= k; ++i) c = c * (unsigned __int128)(v - k + i) / (unsigned)i;
+      M.binom[(size_t)k * (size_t)(n + 1) + (size_t)v] = (uint64_t)c;
+    }
+  auto keys = rd<uint64_t>(dir + "/keys_d" + std::to_string(d) + ".bin");
+  vr::HostPairs hp; std::vector<uint64_t> deaths; vr::ResidualStats st;
+  auto t0 = std::chrono::steady_clock::now();
+  vr::residual_reduce(M, d, maxr, cbits, keys.data(), keys.size(), mode, hp, deaths, st);
+  double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  size_t pos = 0;
+  for (size_t i = 0; i < hp.birth.size(); ++i) pos += hp.birth[i] < hp.death[i];
+  std::printf("d=%d columns=%zu emergent=%lld additions=%lld pairs=%zu positive=%zu ms=%.1f\n", d, keys.size(),
+              (long long)st.emergent, (long long)st.additions, hp.birth.size(), pos, ms);
+  return 0;
+}
