@@ -22,6 +22,10 @@
 //                     only zeros to the left of f (Def 5.3.4), so no column left of f can
 //                     ever have its pivot there.
 #include <algorithm>
+#include <functional>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cmath>
 #include <cstdint>
@@ -84,11 +88,6 @@ struct Entry {
   uint64_t cidx;
   bool operator==(const Entry& o) const { return r == o.r && cidx == o.cidx; }
 };
-// priority_queue top = the pivot: smallest rank, then largest cidx
-struct PivotLess {
-  bool operator()(const Entry& a, const Entry& b) const { return a.r > b.r || (a.r == b.r && a.cidx < b.cidx); }
-};
-using Heap = std::priority_queue<Entry, std::vector<Entry>, PivotLess>;
 
 struct Ctx {
   const HostMatrix& M;
@@ -110,9 +109,12 @@ struct Ctx {
       hi = lo;
     }
   }
-  // coboundary of the d-simplex s in lex-decreasing order (Alg 14, reading A2), with ranks
+  // coboundary of the d-simplex s in lex-decreasing order (Alg 14, reading A2), with ranks.
+  // The rank matrix is symmetric, so R[v][s_q] is read as the contiguous row R[s_q][.].
   template <class F>
   void cofacets(const int* s, uint64_t cidx, uint32_t rs, F&& emit) const {
+    const uint32_t* rows[16];
+    for (int q = 0; q <= d; ++q) rows[q] = &M.rank[(size_t)s[q] * (size_t)M.n];
     uint64_t below = cidx, above = 0;
     int k = d + 1, j = 0;
     for (int64_t v = M.n - 1; v >= 0; --v) {
@@ -123,18 +125,18 @@ struct Ctx {
       }
       if (v < 0) break;
       uint32_t r = rs;
-      const uint32_t* row = &M.rank[(size_t)v * (size_t)M.n];
-      for (int q = 0; q <= d; ++q) r = std::max(r, row[s[q]]);
+      for (int q = 0; q <= d; ++q) r = std::max(r, rows[q][v]);
       if (r == VR_RINF_H) continue;
       if (!emit(Entry{r, above + M.C(v, k + 1) + below})) return;
     }
   }
-  // first v (descending) not in S (K vertices) with max_{w in S} R[v][w] <= r, or -1
+  // first v (descending) not in S (K vertices) with max_{w in S} R[w][v] <= r, or -1
   int64_t first_equal_cofacet_vertex(const int* S, int K, uint32_t r) const {
+    const uint32_t* rows[16];
+    for (int q = 0; q < K; ++q) rows[q] = &M.rank[(size_t)S[q] * (size_t)M.n];
     for (int64_t v = M.n - 1; v >= 0; --v) {
-      const uint32_t* row = &M.rank[(size_t)v * (size_t)M.n];
       bool ok = true;
-      for (int q = 0; q < K && ok; ++q) ok = (v != S[q]) && row[S[q]] <= r;
+      for (int q = 0; q < K && ok; ++q) ok = (v != S[q]) && rows[q][v] <= r;
       if (ok) return v;
     }
     return -1;
@@ -173,122 +175,276 @@ struct Ctx {
   }
 };
 
-bool pop_pivot(Heap& h, Entry& out) {
-  while (!h.empty()) {
-    Entry e = h.top();
-    h.pop();
-    if (!h.empty() && h.top() == e) {
-      h.pop();
-      continue;
+// Open-addressing hash map uint64 -> int64 (linear probing; key ~0 = empty).
+struct U64Map {
+  std::vector<uint64_t> k;
+  std::vector<int64_t> v;
+  size_t n = 0, mask = 0;
+  explicit U64Map(size_t cap = 1024) { rehash(cap); }
+  static uint64_t h(uint64_t x) {
+    x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull; x ^= x >> 33;
+    return x;
+  }
+  void rehash(size_t cap) {
+    size_t c = 16;
+    while (c < cap * 2) c <<= 1;
+    std::vector<uint64_t> ok = std::move(k);
+    std::vector<int64_t> ov = std::move(v);
+    k.assign(c, ~0ull);
+    v.assign(c, 0);
+    mask = c - 1;
+    n = 0;
+    for (size_t i = 0; i < ok.size(); ++i)
+      if (ok[i] != ~0ull) put(ok[i], ov[i]);
+  }
+  bool get(uint64_t key, int64_t& out) const {
+    for (size_t i = h(key) & mask;; i = (i + 1) & mask) {
+      if (k[i] == key) { out = v[i]; return true; }
+      if (k[i] == ~0ull) return false;
     }
-    out = e;
+  }
+  void put(uint64_t key, int64_t val) {
+    if ((n + 1) * 2 > k.size()) rehash(k.size());
+    for (size_t i = h(key) & mask;; i = (i + 1) & mask) {
+      if (k[i] == key) { v[i] = val; return; }
+      if (k[i] == ~0ull) { k[i] = key; v[i] = val; ++n; return; }
+    }
+  }
+};
+
+template <class K> inline int bitlen(K x);
+template <> inline int bitlen<uint64_t>(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
+template <> inline int bitlen<unsigned __int128>(unsigned __int128 x) {
+  const uint64_t hi = (uint64_t)(x >> 64), lo = (uint64_t)x;
+  return hi ? 128 - __builtin_clzll(hi) : (lo ? 64 - __builtin_clzll(lo) : 0);
+}
+
+// Monotone radix heap over packed (rank, ~cidx) row keys, with Z/2 cancellation, for the
+// reduction-matrix mode.  Valid because the pivot of the working column never decreases
+// in row order: each added column R_k = sum of the coboundaries of V_k has the current
+// pivot as its minimum, so whatever it pushes below the pivot occurs an even number of
+// times and cancels — such pushes are dropped, which keeps every key >= `last`.
+template <class K>
+struct RadixHeap {
+  static constexpr int NB = (int)sizeof(K) * 8 + 1;
+  std::vector<K> b[NB];
+  K last = 0;
+  size_t sz = 0;
+  int cb;
+  K mask;
+  RadixHeap(uint32_t, int cbits) : cb(cbits), mask(cbits >= (int)sizeof(K) * 8 ? ~(K)0 : (((K)1 << cbits) - 1)) {}
+  void push(uint32_t r, uint64_t c) {
+    const K x = ((K)r << cb) | (mask - (K)c);
+    if (x < last) return;  // below the pivot: cancels within the added column
+    b[bitlen<K>(x ^ last)].push_back(x);
+    ++sz;
+  }
+  void clear() {
+    for (auto& v : b) v.clear();
+    last = 0;
+    sz = 0;
+  }
+  bool settle() {
+    if (sz == 0) return false;
+    if (!b[0].empty()) return true;
+    int i = 1;
+    while (b[i].empty()) ++i;
+    K m = b[i][0];
+    for (K x : b[i]) m = x < m ? x : m;
+    last = m;
+    for (K x : b[i]) b[bitlen<K>(x ^ last)].push_back(x);
+    b[i].clear();
     return true;
   }
-  return false;
-}
-bool get_pivot(Heap& h, Entry& out) {
-  if (!pop_pivot(h, out)) return false;
-  h.push(out);
-  return true;
-}
+  bool pivot(uint32_t& r, uint64_t& c) {
+    while (settle()) {
+      const size_t n0 = b[0].size();
+      if (n0 & 1) {
+        if (n0 > 1) { b[0].resize(1); sz -= n0 - 1; }
+        r = (uint32_t)(last >> cb);
+        c = (uint64_t)(mask - (last & mask));
+        return true;
+      }
+      sz -= n0;
+      b[0].clear();
+    }
+    return false;
+  }
+};
 
-}  // namespace
+// Binary heap over packed (rank, ~cidx) keys for the oblivious mode (Alg 12 adds raw
+// coboundaries D_k, whose entries can lie below the current pivot: not monotone).
+template <class K>
+struct BinHeap {
+  std::vector<K> h;
+  int cb;
+  K mask;
+  BinHeap(uint32_t, int cbits) : cb(cbits), mask(cbits >= (int)sizeof(K) * 8 ? ~(K)0 : (((K)1 << cbits) - 1)) {}
+  void push(uint32_t r, uint64_t c) {
+    h.push_back(((K)r << cb) | (mask - (K)c));
+    std::push_heap(h.begin(), h.end(), std::greater<K>());
+  }
+  void clear() { h.clear(); }
+  bool pivot(uint32_t& r, uint64_t& c) {
+    while (!h.empty()) {
+      K m = h.front();
+      std::pop_heap(h.begin(), h.end(), std::greater<K>());
+      h.pop_back();
+      if (!h.empty() && h.front() == m) {
+        std::pop_heap(h.begin(), h.end(), std::greater<K>());
+        h.pop_back();
+        continue;
+      }
+      h.push_back(m);
+      std::push_heap(h.begin(), h.end(), std::greater<K>());
+      r = (uint32_t)(m >> cb);
+      c = (uint64_t)(mask - (m & mask));
+      return true;
+    }
+    return false;
+  }
+};
 
-void residual_reduce(const HostMatrix& M, int d, uint32_t maxr, int cbits, const uint64_t* keys, uint64_t nkeys, int mode,
-                     HostPairs& out, std::vector<uint64_t>& deaths_sorted, ResidualStats& st) {
+template <class HeapT>
+void residual_reduce_t(const HostMatrix& M, int d, uint32_t maxr, int cbits, const uint64_t* keys, uint64_t nkeys,
+                       int mode, HeapT& W, HostPairs& out, std::vector<uint64_t>& deaths_sorted, ResidualStats& st) {
   Ctx cx(M, d);
   const uint64_t cmask = cbits >= 64 ? ~0ull : ((1ull << cbits) - 1);
-  struct Col {
-    uint64_t cidx;
-    uint32_t r;
-    std::vector<Entry> V;  // reduction column (simplices whose coboundaries sum to R_j), incl. itself
-  };
-  std::vector<Col> cols;
-  std::unordered_map<uint64_t, int64_t> pivot_col;  // row cidx -> index into cols
+  auto colkey = [&](uint32_t r, uint64_t c) -> uint64_t { return ((uint64_t)(maxr - r) << cbits) | c; };
+  // stored reduction columns V_k (column keys), pool-allocated
+  std::vector<uint64_t> vpool;
+  std::vector<std::pair<uint64_t, uint32_t>> vcol;  // (offset, length) per residual column with a pivot
+  U64Map pivot_col((size_t)nkeys + 16);             // row cidx -> index into vcol
+  U64Map app_memo(1024);                            // row cidx -> apparent partner cidx or -1
+  std::vector<uint64_t> work_v;
   deaths_sorted.clear();
   int s[16], f[16];
+
+  auto apparent_of = [&](const Entry& e) -> int64_t {
+    int64_t a;
+    if (app_memo.get(e.cidx, a)) return a;
+    a = cx.apparent_partner(e.cidx, e.r);
+    app_memo.put(e.cidx, a);
+    return a;
+  };
+  auto push_coboundary = [&](uint64_t cidx, uint32_t r) {
+    ++st.coboundaries;
+    cx.decode(cidx, d + 1, f);
+    cx.cofacets(f, cidx, r, [&](const Entry& e) { W.push(e.r, e.cidx); return true; });
+  };
 
   for (uint64_t c = 0; c < nkeys; ++c) {
     const uint64_t key = keys[c];
     const uint32_t rs = maxr - (uint32_t)(key >> cbits);
     const uint64_t sc = key & cmask;
     cx.decode(sc, d + 1, s);
-
-    auto claimed = [&](const Entry& e, int64_t& col, int64_t& app) {
-      auto it = pivot_col.find(e.cidx);
-      if (it != pivot_col.end()) { col = it->second; app = -1; return true; }
-      int64_t a = cx.apparent_partner(e.cidx, e.r);
-      if (a >= 0) { col = -1; app = a; return true; }
-      return false;
-    };
-
-    Heap W;
-    std::vector<Entry> work_v;  // reduction column under construction (Z/2, cancelled at the end)
-    work_v.push_back(Entry{rs, sc});
-    // initial coboundary with the emergent check on the first equal-diameter cofacet
+    W.clear();
+    work_v.clear();
+    work_v.push_back(key);
+    // initial coboundary; emergent check on the first equal-diameter cofacet (§5.2.11)
     bool check = true, emergent = false;
-    Entry piv{0, 0};
+    Entry first{0, 0};
     cx.cofacets(s, sc, rs, [&](const Entry& e) {
       if (check && e.r == rs) {
-        int64_t col, app;
-        if (!claimed(e, col, app)) { piv = e; emergent = true; return false; }
+        int64_t col;
+        if (!pivot_col.get(e.cidx, col) && apparent_of(e) < 0) { first = e; emergent = true; return false; }
         check = false;
       }
-      W.push(e);
+      W.push(e.r, e.cidx);
       return true;
     });
-    bool have = emergent;
-    if (!emergent) have = get_pivot(W, piv);
-    if (emergent) ++st.emergent;
-    while (have && !emergent) {
-      int64_t col, app;
-      if (!claimed(piv, col, app)) break;
-      ++st.additions;
-      auto add_simplex = [&](uint64_t cidx, uint32_t r) {
-        cx.decode(cidx, d + 1, f);
-        cx.cofacets(f, cidx, r, [&](const Entry& e) { W.push(e); return true; });
-      };
-      if (col >= 0) {
-        const Col& K = cols[(size_t)col];
+    const float birth = M.value[rs];
+    if (emergent) {
+      ++st.emergent;
+      out.push(birth, M.value[first.r], sc, first.cidx);
+      deaths_sorted.push_back(first.cidx);
+      pivot_col.put(first.cidx, (int64_t)vcol.size());
+      vcol.push_back({vpool.size(), 1});
+      vpool.push_back(key);
+      continue;
+    }
+    Entry pe{0, 0};
+    bool have = W.pivot(pe.r, pe.cidx);
+    while (have) {
+      int64_t col;
+      if (pivot_col.get(pe.cidx, col)) {
+        const auto& vc = vcol[(size_t)col];
         if (mode == 0) {
-          for (const Entry& e : K.V) { add_simplex(e.cidx, e.r); work_v.push_back(e); }
+          for (uint32_t q = 0; q < vc.second; ++q) {
+            const uint64_t vk = vpool[vc.first + q];
+            push_coboundary(vk & cmask, maxr - (uint32_t)(vk >> cbits));
+            work_v.push_back(vk);
+          }
         } else {
-          add_simplex(K.cidx, K.r);
+          const uint64_t vk = vpool[vc.first];  // the column's own simplex (first entry)
+          push_coboundary(vk & cmask, maxr - (uint32_t)(vk >> cbits));
         }
       } else {
+        const int64_t a = apparent_of(pe);
+        if (a < 0) break;  // unclaimed pivot
         int fv[16];
-        cx.decode((uint64_t)app, d + 1, fv);
+        cx.decode((uint64_t)a, d + 1, fv);
         const uint32_t fr = cx.diam_rank(fv);
-        add_simplex((uint64_t)app, fr);
-        if (mode == 0) work_v.push_back(Entry{fr, (uint64_t)app});
+        push_coboundary((uint64_t)a, fr);
+        if (mode == 0) work_v.push_back(colkey(fr, (uint64_t)a));
       }
-      have = get_pivot(W, piv);
+      ++st.additions;
+      have = W.pivot(pe.r, pe.cidx);
     }
-    const float birth = M.value[rs];
     if (have) {
-      const float death = M.value[piv.r];
-      out.push(birth, death, sc, piv.cidx);
-      deaths_sorted.push_back(piv.cidx);
-      Col K{sc, rs, {}};
-      if (mode == 0 && !emergent) {
-        // Z/2-cancel the reduction column
-        std::sort(work_v.begin(), work_v.end(), [](const Entry& a, const Entry& b) { return a.cidx < b.cidx; });
-        for (size_t i = 0; i < work_v.size();) {
+      out.push(birth, M.value[pe.r], sc, pe.cidx);
+      deaths_sorted.push_back(pe.cidx);
+      pivot_col.put(pe.cidx, (int64_t)vcol.size());
+      const size_t off = vpool.size();
+      if (mode == 0 && work_v.size() > 1) {
+        // Z/2-cancel the reduction column; keep the column's own simplex first
+        std::sort(work_v.begin() + 1, work_v.end());
+        vpool.push_back(key);
+        for (size_t i = 1; i < work_v.size();) {
           size_t j = i;
-          while (j < work_v.size() && work_v[j].cidx == work_v[i].cidx) ++j;
-          if ((j - i) & 1) K.V.push_back(work_v[i]);
+          while (j < work_v.size() && work_v[j] == work_v[i]) ++j;
+          if (((j - i) & 1) && work_v[i] != key) vpool.push_back(work_v[i]);
           i = j;
         }
       } else {
-        K.V.push_back(Entry{rs, sc});
+        vpool.push_back(key);
       }
-      pivot_col.emplace(piv.cidx, (int64_t)cols.size());
-      cols.push_back(std::move(K));
+      vcol.push_back({off, (uint32_t)(vpool.size() - off)});
     } else {
       out.push(birth, INFINITY, sc, UINT64_MAX);  // zero column: essential class
     }
   }
   std::sort(deaths_sorted.begin(), deaths_sorted.end());
+}
+
+}  // namespace
+
+void residual_reduce(const HostMatrix& M, int d, uint32_t maxr, int cbits, const uint64_t* keys, uint64_t nkeys, int mode,
+                     HostPairs& out, std::vector<uint64_t>& deaths_sorted, ResidualStats& st) {
+  // row keys pack (rank, ~cofacet cidx): 64 bits when they fit, else 128
+  const uint64_t cof = M.C(M.n, d + 2);
+  int cb = 1;
+  while (cb < 64 && (cof >> cb) != 0) ++cb;
+  int rb = 1;
+  while (rb < 32 && (maxr >> rb) != 0) ++rb;
+  using u128 = unsigned __int128;
+  if (rb + cb <= 64) {
+    if (mode == 0) {
+      RadixHeap<uint64_t> W(maxr, cb);
+      residual_reduce_t(M, d, maxr, cbits, keys, nkeys, mode, W, out, deaths_sorted, st);
+    } else {
+      BinHeap<uint64_t> W(maxr, cb);
+      residual_reduce_t(M, d, maxr, cbits, keys, nkeys, mode, W, out, deaths_sorted, st);
+    }
+  } else {
+    if (mode == 0) {
+      RadixHeap<u128> W(maxr, cb);
+      residual_reduce_t(M, d, maxr, cbits, keys, nkeys, mode, W, out, deaths_sorted, st);
+    } else {
+      BinHeap<u128> W(maxr, cb);
+      residual_reduce_t(M, d, maxr, cbits, keys, nkeys, mode, W, out, deaths_sorted, st);
+    }
+  }
 }
 
 }  // namespace vr

@@ -1,6 +1,6 @@
 // residual_bench.cpp — time libvr's host residual reduction on inputs dumped by a GPU run
 // (VR_DUMP_RESIDUAL=<dir>).  Diagnostics only.
-//   g++ -O3 -std=c++17 -I paper_2502_05063_b200/csrc tools/residual_bench.cpp \
+//   g++ -O3 -std=c++17 -I /usr/local/cuda/include -I paper_2502_05063_b200/csrc tools/residual_bench.cpp
 //       paper_2502_05063_b200/csrc/host.cpp -o /tmp/residual_bench && /tmp/residual_bench <dir> <d> [mode]
 #include <chrono>
 #include <cstdio>
@@ -51,7 +51,17 @@ int main(int argc, char** argv) {
   double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   size_t pos = 0;
   for (size_t i = 0; i < hp.birth.size(); ++i) pos += hp.birth[i] < hp.death[i];
-  std::printf("d=%d columns=%zu emergent=%lld additions=%lld pairs=%zu positive=%zu ms=%.1f\n", d, keys.size(),
-              (long long)st.emergent, (long long)st.additions, hp.birth.size(), pos, ms);
+  if (const char* c = std::getenv("VR_COL")) {
+    size_t i = (size_t)std::atoll(c);
+    std::printf("col %zu: birth %.7g death %.7g bcidx %llu dcidx %llu\n", i, hp.birth[i], hp.death[i],
+                (unsigned long long)hp.birth_cidx[i], (unsigned long long)hp.death_cidx[i]);
+    uint64_t cm = (1ull << cbits) - 1;
+    std::printf("key rank %u\n", maxr - (unsigned)(keys[i] >> cbits));
+    (void)cm;
+  }
+  std::printf("d=%d mode=%d columns=%zu emergent=%lld additions=%lld coboundaries=%lld pairs=%zu positive=%zu ms=%.1f\n",
+              d, mode, keys.size(), (long long)st.emergent, (long long)st.additions, (long long)st.coboundaries,
+              hp.birth.size(), pos, ms);
   return 0;
 }
+// (debug) print the pair produced by a given column: VR_COL=<index>
