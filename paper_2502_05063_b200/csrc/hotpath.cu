@@ -7,25 +7,33 @@
 // independently"), not on the column's position in the sorted order; and apparent
 // columns are never cleared (Prop 5.3.9 argument).  So this design runs the
 // apparent test INSIDE the enumeration, and only the few columns that are not apparent
-// travel further (DESIGN.md "What differs from the paper"):
+// travel further (DESIGN.md §6):
 //
-//   k_enumerate<D>  (a1 + a5 phase 1 + a3)
-//       one warp per "row" = a fixed upper-vertex prefix (v_D > ... > v_1); the 32 lanes
-//       take consecutive v_0, so the d-simplices of a row have consecutive cidx (Eq 5.6)
-//       and every distance read R[v_i][v_0] is a coalesced row segment.  Per lane:
-//       diameter rank = max pairwise rank, threshold (diam <= t, inclusive), then the
-//       Lemma 5.3.6 scan over cofacet vertices v = n-1, n-2, ... (lex-decreasing
-//       cofacets, Alg 14) for at most `steps` candidates, all lanes in lock-step on the
-//       same v (broadcast loads of R[v][v_i], one coalesced load of R[v][v_0]).  Lanes
-//       proven apparent are counted; every other survivor is appended (warp-aggregated,
-//       §5.5.3) to the queue.
+//   k_enumerate<D>  (a1 + a2 + a5 phase 1 + a3)
+//       one warp per "row" = a fixed upper-vertex prefix (u_D > ... > u_1); the 32 lanes
+//       take consecutive v_0 < u_1, so the d-simplices of a row have consecutive cidx
+//       (Eq 5.6) and every rank read R[u_i][v_0] is a coalesced row segment.  Per lane:
+//       diameter rank = max pairwise rank, threshold (diam <= t, inclusive, Eq 5.3),
+//       clearing (one bit of the dimension's clearing bitmap — the deaths of dimension
+//       d-1, Lemma 4.2.3), then Lemma 5.3.6 over the cofacet vertices v = n-1, n-2, ...
+//       (lex-decreasing cofacets, Alg 14) for at most `steps` vertices.  The prefix part
+//       of every new-edge maximum, max_i R[u_i][v], is precomputed once per row for a
+//       32-vertex window, one value per lane, and broadcast with __shfl_sync, so a scan
+//       step costs one coalesced load R[v][v_0] per warp.  Condition 2 (no lex-smaller
+//       facet of t with the same diameter) is evaluated once per chunk after the scan.
+//       Apparent columns are counted and mark their cofacet in the next dimension's
+//       clearing bitmap; non-apparent ones go straight to the residual list; columns
+//       whose equal-diameter cofacet lies beyond the window go to the phase-2 queue with
+//       their vertices (warp-aggregated appends, §5.5.3).
 //
-//   k_resolve<D>    (a5 phase 2 + a2 + a6)
-//       one warp per queued column: the full Lemma 5.3.6 test with the 32 lanes testing
-//       32 cofacet vertices per step (ballot, the lowest set lane = the lex-greatest
-//       equal-diameter cofacet); then clearing for non-apparent columns (the column is a
-//       death of dimension d-1: in the sorted residual-death list, or the apparent
-//       cofacet of its youngest facet, recomputed); survivors are the residual columns.
+//   k_resolve<D>    (a5 phase 2 + a6)
+//       one warp per queued column, resuming the Lemma 5.3.6 scan where phase 1 stopped,
+//       32 cofacet vertices per step (ballot; the lowest set lane = the lex-greatest
+//       equal-diameter cofacet).  Fallback when a clearing bitmap would be too large:
+//       phase 1 queues every non-proven column and phase 2 decides clearing by
+//       recomputation (the column is the apparent cofacet of its youngest facet) plus a
+//       binary search in the dimension-(d-1) residual deaths.
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -38,12 +46,30 @@ constexpr int HP_THREADS = 256;
 
 __device__ __forceinline__ uint32_t umax(uint32_t a, uint32_t b) { return a > b ? a : b; }
 
+__device__ __forceinline__ bool bit_test(const uint32_t* __restrict__ bm, uint64_t i) {
+  return (__ldg(bm + (i >> 5)) >> (i & 31)) & 1u;
+}
+__device__ __forceinline__ void bit_set(uint32_t* bm, uint64_t i) { atomicOr(bm + (i >> 5), 1u << (i & 31)); }
+
+template <int D>
+__device__ __forceinline__ uint4 pack_vertices(const int (&s)[D + 1]) {
+  uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int i = 0; i <= D; ++i) w[i >> 1] |= (uint32_t)s[i] << ((i & 1) * 16);
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+template <int D>
+__device__ __forceinline__ void unpack_vertices(uint4 p, int (&s)[D + 1]) {
+  const uint32_t w[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+  for (int i = 0; i <= D; ++i) s[i] = (int)((w[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu);
+}
+
 // ------------------------------------------------------------------ phase 1: enumerate
 template <int D>
-__device__ __forceinline__ void process_row(const Tables& T, const DimParams& p, const int (&u)[D + 2], uint64_t* queue,
-                                            uint64_t qcap, DimCounters* ctr, uint64_t* app_pairs, uint64_t app_cap,
+__device__ __forceinline__ void process_row(const Tables& T, const DimParams& p, const HotBuffers& B, const int (&u)[D + 2],
                                             unsigned long long& surv_acc, unsigned long long& app_acc,
-                                            unsigned long long& scan_acc) {
+                                            unsigned long long& scan_acc, unsigned long long& clr_acc) {
   const int lane = threadIdx.x & 31;
   const int n = T.n;
   const int v1 = u[1];
@@ -67,6 +93,20 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
   uint64_t cbase = 0;
 #pragma unroll
   for (int i = 1; i <= D; ++i) cbase += binom(T, u[i], i + 1);
+  // window of the first 32 cofacet vertices v = n-1-lane: mup = max_i R[u_i][v]
+  // (RINF for a prefix vertex, so the warp skips it)
+  uint32_t mup0;
+  {
+    const int v = n - 1 - lane;
+    uint32_t m = VR_RINF;
+    if (v >= 0) {
+      m = 0;
+#pragma unroll
+      for (int i = 1; i <= D; ++i) m = (v == u[i]) ? VR_RINF : umax(m, rank_at(T, u[i], v));
+    }
+    mup0 = m;
+  }
+  const int steps = p.steps;
 
   for (int base = 0; base < v1; base += 32) {
     const int v0 = base + lane;
@@ -82,90 +122,102 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
     const uint32_t msurv = __ballot_sync(0xffffffffu, surv);
     if (!msurv) continue;
     surv_acc += __popc(msurv);
-    // diameter of s \ {w} for each vertex w of s
-    uint32_t ex[D + 1];
-    ex[0] = pm_up;  // w = v_0
-#pragma unroll
-    for (int j = 1; j <= D; ++j) {
-      uint32_t m = pm_ex[j];
-#pragma unroll
-      for (int i = 1; i <= D; ++i)
-        if (i != j) m = umax(m, a[i]);
-      ex[j] = m;
-    }
-    // Lemma 5.3.6, lane-parallel, at most p.steps cofacet vertices
-    int state = surv ? 0 : 3;  // 0 scanning, 1 apparent, 2 not apparent, 3 idle
+    const uint64_t cidx = cbase + (uint64_t)v0;
+    bool cleared = false;
+    if (B.clr && surv) cleared = bit_test(B.clr, cidx);  // a death of dimension d-1
+    clr_acc += __popc(__ballot_sync(0xffffffffu, cleared));
+    bool active = surv && !cleared;
     int hitv = -1;
-    int v = n - 1;
-    for (int step = 0; step < p.steps; ++step) {
-      const uint32_t mact = __ballot_sync(0xffffffffu, state == 0);
+    // Lemma 5.3.6 condition 1, lane-parallel: the first v with every new edge <= diam(s)
+    for (int j = 0; j < steps; ++j) {
+      const uint32_t mact = __ballot_sync(0xffffffffu, active);
       if (!mact) break;
-      bool up = true;
-      while (up) {  // skip the prefix vertices (warp-uniform)
-        up = false;
-#pragma unroll
-        for (int i = 1; i <= D; ++i) up |= (v == u[i]);
-        if (up) --v;
-      }
+      const int v = n - 1 - j;
       if (v < 0) break;
+      uint32_t m;
+      if (j < 32) {
+        m = __shfl_sync(0xffffffffu, mup0, j);
+      } else {
+        m = 0;
+#pragma unroll
+        for (int i = 1; i <= D; ++i) m = (v == u[i]) ? VR_RINF : umax(m, rank_at(T, u[i], v));
+      }
+      if (!__any_sync(0xffffffffu, active && m <= rs)) continue;  // no lane can hit at v
       scan_acc += __popc(mact);
+      const uint32_t b0 = active ? rank_at(T, v, v0) : VR_RINF;
+      if (active && v != v0 && umax(m, b0) <= rs) {
+        hitv = v;
+        active = false;
+      }
+    }
+    // condition 2 for lanes that found t = s ∪ {hitv}: no facet t \ {w}, w > hitv (the
+    // lex-smaller facets), with diam = diam(s)
+    bool app = false;
+    if (hitv >= 0) {
+      app = true;
       uint32_t b[D + 1];
       uint32_t bup = 0;
 #pragma unroll
       for (int i = 1; i <= D; ++i) {
-        b[i] = rank_at(T, v, u[i]);
+        b[i] = rank_at(T, hitv, u[i]);
         bup = umax(bup, b[i]);
       }
-      const uint32_t b0 = (state == 0) ? rank_at(T, v, v0) : VR_RINF;
-      // t = s ∪ {v} has diam(t) = diam(s) iff every new edge is <= diam(s)
-      if (state == 0 && v != v0 && umax(bup, b0) <= rs) {
-        // condition 2: no facet t \ {w}, w > v (smaller cidx), with diam = diam(s)
-        bool app = true;
-        if (v0 > v && umax(ex[0], bup) == rs) app = false;
+      const uint32_t b0 = rank_at(T, hitv, v0);
+      if (v0 > hitv && umax(pm_up, bup) == rs) app = false;
 #pragma unroll
-        for (int j = 1; j <= D; ++j) {
-          if (u[j] > v) {
-            uint32_t m = umax(ex[j], b0);
+      for (int j = 1; j <= D; ++j) {
+        if (u[j] > hitv) {
+          uint32_t m = umax(pm_ex[j], b0);
 #pragma unroll
-            for (int i = 1; i <= D; ++i)
-              if (i != j) m = umax(m, b[i]);
-            if (m == rs) app = false;
-          }
+          for (int i = 1; i <= D; ++i)
+            if (i != j) m = umax(m, umax(a[i], b[i]));
+          if (m == rs) app = false;
         }
-        state = app ? 1 : 2;
-        hitv = v;
       }
-      --v;
     }
-    const uint32_t mapp = __ballot_sync(0xffffffffu, state == 1);
-    app_acc += __popc(mapp);
-    if (app_pairs) {
-      unsigned long long slot = warp_append(state == 1, &ctr->app_pairs);
-      if (state == 1 && slot < app_cap) {
-        int s[D + 1];
+    app_acc += __popc(__ballot_sync(0xffffffffu, app));
+    if (app && (B.clr_next || B.app_pairs)) {
+      int s[D + 1];
 #pragma unroll
-        for (int i = 0; i < D; ++i) s[i] = u[D - i];
-        s[D] = v0;
-        app_pairs[2 * slot] = cbase + (uint64_t)v0;
-        app_pairs[2 * slot + 1] = cofacet_cidx<D>(T, s, hitv);
+      for (int i = 0; i < D; ++i) s[i] = u[D - i];
+      s[D] = v0;
+      const uint64_t tc = cofacet_cidx<D>(T, s, hitv);
+      if (B.clr_next) bit_set(B.clr_next, tc);
+      if (B.app_pairs) {
+        const unsigned long long slot = atomicAdd(&B.ctr->app_pairs, 1ull);
+        if (slot < B.app_cap) {
+          B.app_pairs[2 * slot] = cidx;
+          B.app_pairs[2 * slot + 1] = tc;
+        }
       }
     }
-    const bool q = surv && state != 1;
-    const unsigned long long slot = warp_append(q, &ctr->queued);
-    if (q && slot < qcap) queue[slot] = ((uint64_t)(p.maxr - rs) << p.cbits) | (cbase + (uint64_t)v0);
+    const uint64_t key = ((uint64_t)(p.maxr - rs) << p.cbits) | cidx;
+    // not apparent and not cleared: a residual column (bitmap mode only — without a
+    // bitmap clearing is decided in phase 2)
+    const bool to_resid = B.clr && hitv >= 0 && !app;
+    const bool to_queue = active || (!B.clr && hitv >= 0 && !app);
+    const unsigned long long rslot = warp_append(to_resid, &B.ctr->residual);
+    if (to_resid && rslot < B.rcap) B.resid[rslot] = key;
+    const unsigned long long qslot = warp_append(to_queue, &B.ctr->queued);
+    if (to_queue && qslot < B.qcap) {
+      int s[D + 1];
+#pragma unroll
+      for (int i = 0; i < D; ++i) s[i] = u[D - i];
+      s[D] = v0;
+      B.qkey[qslot] = key;
+      B.qvert[qslot] = pack_vertices<D>(s);
+    }
   }
 }
 
 template <int D>
-__global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p, uint64_t* __restrict__ queue, uint64_t qcap,
-                                                          DimCounters* __restrict__ ctr, uint64_t* __restrict__ app_pairs,
-                                                          uint64_t app_cap) {
+__global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p, HotBuffers B) {
   constexpr int GRAB = 4;
   const int lane = threadIdx.x & 31;
-  unsigned long long surv_acc = 0, app_acc = 0, scan_acc = 0;
+  unsigned long long surv_acc = 0, app_acc = 0, scan_acc = 0, clr_acc = 0;
   while (true) {
     unsigned long long r0 = 0;
-    if (lane == 0) r0 = atomicAdd(&ctr->row_next, (unsigned long long)GRAB);
+    if (lane == 0) r0 = atomicAdd(&B.ctr->row_next, (unsigned long long)GRAB);
     r0 = __shfl_sync(0xffffffffu, r0, 0) + p.row_begin;
     if (r0 >= p.row_end) break;
     const uint64_t rend = (r0 + GRAB < p.row_end) ? r0 + GRAB : p.row_end;
@@ -195,23 +247,25 @@ __global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p,
           }
         }
       }
-      process_row<D>(T, p, u, queue, qcap, ctr, app_pairs, app_cap, surv_acc, app_acc, scan_acc);
+      process_row<D>(T, p, B, u, surv_acc, app_acc, scan_acc, clr_acc);
     }
   }
   if (lane == 0) {
-    if (surv_acc) atomicAdd(&ctr->survivors, surv_acc);
-    if (app_acc) atomicAdd(&ctr->apparent1, app_acc);
-    if (scan_acc) atomicAdd(&ctr->scanned, scan_acc);
+    if (surv_acc) atomicAdd(&B.ctr->survivors, surv_acc);
+    if (app_acc) atomicAdd(&B.ctr->apparent1, app_acc);
+    if (scan_acc) atomicAdd(&B.ctr->scanned, scan_acc);
+    if (clr_acc) atomicAdd(&B.ctr->cleared, clr_acc);
   }
 }
 
 // ------------------------------------------------------------------ phase 2: resolve
-// First v (descending from n-1) not in S with max_{w in S} R[w][v] <= r, or -1.
+// First v <= start (descending) not in S with max_{w in S} R[w][v] <= r, or -1.
 // Lanes take v = base - lane: each load R[w][v] is a coalesced row segment.
 template <int K>
-__device__ __forceinline__ int coop_scan(const Tables& T, const int (&S)[K], uint32_t r, unsigned long long& scan_acc) {
+__device__ __forceinline__ int coop_scan(const Tables& T, const int (&S)[K], uint32_t r, int start,
+                                         unsigned long long& scan_acc) {
   const int lane = threadIdx.x & 31;
-  for (int base = T.n - 1; base >= 0; base -= 32) {
+  for (int base = start; base >= 0; base -= 32) {
     scan_acc += (unsigned long long)(base + 1 < 32 ? base + 1 : 32);
     const int v = base - lane;
     bool ok = v >= 0;
@@ -230,22 +284,19 @@ __device__ __forceinline__ int coop_scan(const Tables& T, const int (&S)[K], uin
 }
 
 template <int D>
-__global__ void __launch_bounds__(HP_THREADS) k_resolve(Tables T, DimParams p, const uint64_t* __restrict__ queue, uint64_t qn,
-                                                        const uint64_t* __restrict__ deaths, int64_t ndeaths,
-                                                        uint64_t* __restrict__ resid, uint64_t rcap,
-                                                        DimCounters* __restrict__ ctr, uint64_t* __restrict__ app_pairs,
-                                                        uint64_t app_cap) {
+__global__ void __launch_bounds__(HP_THREADS) k_resolve(Tables T, DimParams p, HotBuffers B, uint64_t qn) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t cmask = p.cbits >= 64 ? ~0ull : ((1ull << p.cbits) - 1);
+  const int start = T.n - 1 - p.steps;  // phase 1 examined v = n-1 .. n-steps
   unsigned long long app_acc = 0, clr_acc = 0, scan_acc = 0;
   for (uint64_t e = warp; e < qn; e += nwarps) {
-    const uint64_t key = __ldg(queue + e);
+    const uint64_t key = __ldg(B.qkey + e);
     const uint32_t rs = p.maxr - (uint32_t)(key >> p.cbits);
     const uint64_t cidx = key & cmask;
     int s[D + 1];
-    cns_decode<D>(T, cidx, s);
+    unpack_vertices<D>(B.qvert[e], s);
     uint32_t ex[D + 1];
 #pragma unroll
     for (int j = 0; j <= D; ++j) ex[j] = 0;
@@ -258,71 +309,88 @@ __global__ void __launch_bounds__(HP_THREADS) k_resolve(Tables T, DimParams p, c
         for (int j = 0; j <= D; ++j)
           if (j != a && j != b) ex[j] = umax(ex[j], r);
       }
-    // Lemma 5.3.6 condition 1: the lex-greatest cofacet with diam(t) = diam(s)
-    const int v = coop_scan<D + 1>(T, s, rs, scan_acc);
+    // Lemma 5.3.6 condition 1 (without a bitmap, columns phase 1 already found
+    // non-apparent are queued too and simply re-find their hit from the top)
+    const int v = coop_scan<D + 1>(T, s, rs, B.clr ? start : T.n - 1, scan_acc);
     bool app = false;
     if (v >= 0) {
-      // condition 2: no facet t \ {w}, w > v, with diam = diam(s)
-      app = true;
+      // condition 2: no facet t \ {w}, w > v, with diam = diam(s); lane j checks w = s[j]
+      bool bad = false;
+      if (lane <= D) {
+        const int j = lane;
+        int w = 0;
+        uint32_t m = 0;
 #pragma unroll
-      for (int j = 0; j <= D; ++j) {
-        if (s[j] > v) {
-          uint32_t m = ex[j];
+        for (int q = 0; q <= D; ++q)
+          if (q == j) { w = s[q]; m = ex[q]; }
+        if (w > v) {
 #pragma unroll
           for (int i = 0; i <= D; ++i)
             if (i != j) m = umax(m, rank_at(T, v, s[i]));
-          if (m == rs) app = false;
+          bad = (m == rs);
         }
       }
+      app = !__any_sync(0xffffffffu, bad);
     }
     if (app) {
       ++app_acc;
-      if (app_pairs && lane == 0) {
-        unsigned long long slot = atomicAdd(&ctr->app_pairs, 1ull);
-        if (slot < app_cap) {
-          app_pairs[2 * slot] = cidx;
-          app_pairs[2 * slot + 1] = cofacet_cidx<D>(T, s, v);
+      if (lane == 0 && (B.clr_next || B.app_pairs)) {
+        const uint64_t tc = cofacet_cidx<D>(T, s, v);
+        if (B.clr_next) bit_set(B.clr_next, tc);
+        if (B.app_pairs) {
+          const unsigned long long slot = atomicAdd(&B.ctr->app_pairs, 1ull);
+          if (slot < B.app_cap) {
+            B.app_pairs[2 * slot] = cidx;
+            B.app_pairs[2 * slot + 1] = tc;
+          }
         }
       }
       continue;
     }
-    // clearing (§5.2.3, Lemma 4.2.3): s is cleared iff it is the death of a pair of
-    // dimension d-1 — a residual pair (sorted list) or an apparent pair, recomputed:
-    // s is the apparent cofacet of its youngest facet f (the first facet in Alg 16
-    // order — removing s[0], s[1], ... — with diam(f) = diam(s)) iff the lex-greatest
-    // equal-diameter cofacet of f is s itself.
-    bool cleared = sorted_contains(deaths, ndeaths, cidx);
-    if (D >= 2 && !cleared) {
-      int js = -1;
+    if (!B.clr) {
+      // clearing by recomputation (§5.2.3, Lemma 4.2.3): s is cleared iff it is the death
+      // of a pair of dimension d-1 — a residual pair (sorted list) or an apparent pair:
+      // s is the apparent cofacet of its youngest facet f (the first facet in Alg 16 order
+      // — removing s[0], s[1], ... — with diam(f) = diam(s)) iff the lex-greatest
+      // equal-diameter cofacet of f is s itself.
+      bool cleared = sorted_contains(B.deaths, B.ndeaths, cidx);
+      if (D >= 2 && !cleared) {
+        int js = -1;
 #pragma unroll
-      for (int j = 0; j <= D; ++j)
-        if (js < 0 && ex[j] == rs) js = j;
-      if (js >= 0) {
-        int f[D];
-        int w = 0;
+        for (int j = 0; j <= D; ++j)
+          if (js < 0 && ex[j] == rs) js = j;
+        if (js >= 0) {
+          int f[D];
+          int w = 0;
 #pragma unroll
-        for (int j = 0; j <= D; ++j) {
-          int x = s[j];
-          if (j == js) w = x;
-          else f[j < js ? j : j - 1] = x;
+          for (int j = 0; j <= D; ++j) {
+            const int x = s[j];
+            if (j == js) w = x;
+            else f[j < js ? j : j - 1] = x;
+          }
+          cleared = coop_scan<D>(T, f, rs, T.n - 1, scan_acc) == w;
         }
-        cleared = coop_scan<D>(T, f, rs, scan_acc) == w;
       }
-    }
-    if (cleared) {
-      ++clr_acc;
-      continue;
+      if (cleared) {
+        ++clr_acc;
+        continue;
+      }
     }
     if (lane == 0) {
-      const unsigned long long slot = atomicAdd(&ctr->residual, 1ull);
-      if (slot < rcap) resid[slot] = key;
+      const unsigned long long slot = atomicAdd(&B.ctr->residual, 1ull);
+      if (slot < B.rcap) B.resid[slot] = key;
     }
   }
   if (lane == 0) {
-    if (app_acc) atomicAdd(&ctr->apparent2, app_acc);
-    if (clr_acc) atomicAdd(&ctr->cleared, clr_acc);
-    if (scan_acc) atomicAdd(&ctr->scanned2, scan_acc);
+    if (app_acc) atomicAdd(&B.ctr->apparent2, app_acc);
+    if (clr_acc) atomicAdd(&B.ctr->cleared, clr_acc);
+    if (scan_acc) atomicAdd(&B.ctr->scanned2, scan_acc);
   }
+}
+
+__global__ void k_set_bits(const uint64_t* __restrict__ list, int64_t m, uint32_t* __restrict__ bm) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    bit_set(bm, __ldg(list + i));
 }
 
 // ------------------------------------------------------------------ launchers
@@ -338,59 +406,60 @@ static int sm_count() {
 }
 
 template <int D>
-static void enumerate_d(const DimParams& p, const Tables& T, uint64_t* queue, uint64_t qcap, DimCounters* ctr,
-                        uint64_t* app_pairs, uint64_t app_cap, cudaStream_t st) {
+static void enumerate_d(const DimParams& p, const Tables& T, const HotBuffers& B, cudaStream_t st) {
   const uint64_t rows = p.row_end - p.row_begin;
   const uint64_t warps_needed = (rows + 3) / 4;
   uint64_t blocks = (warps_needed * 32 + HP_THREADS - 1) / HP_THREADS;
   const uint64_t cap = (uint64_t)sm_count() * 8;  // 8 resident CTAs of 256 threads per SM
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  k_enumerate<D><<<(unsigned)blocks, HP_THREADS, 0, st>>>(T, p, queue, qcap, ctr, app_pairs, app_cap);
+  k_enumerate<D><<<(unsigned)blocks, HP_THREADS, 0, st>>>(T, p, B);
 }
 
 template <int D>
-static void resolve_d(const DimParams& p, const Tables& T, const uint64_t* queue, uint64_t qn, const uint64_t* deaths,
-                      int64_t ndeaths, uint64_t* resid, uint64_t rcap, DimCounters* ctr, uint64_t* app_pairs,
-                      uint64_t app_cap, cudaStream_t st) {
+static void resolve_d(const DimParams& p, const Tables& T, const HotBuffers& B, uint64_t qn, cudaStream_t st) {
   uint64_t blocks = (qn * 32 + HP_THREADS - 1) / HP_THREADS;
   const uint64_t cap = (uint64_t)sm_count() * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  k_resolve<D><<<(unsigned)blocks, HP_THREADS, 0, st>>>(T, p, queue, qn, deaths, ndeaths, resid, rcap, ctr, app_pairs,
-                                                         app_cap);
+  k_resolve<D><<<(unsigned)blocks, HP_THREADS, 0, st>>>(T, p, B, qn);
 }
 
-void launch_enumerate(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, uint64_t* queue,
-                      uint64_t qcap, DimCounters* ctr, uint64_t* app_pairs, uint64_t app_cap, cudaStream_t st,
-                      int64_t* launches) {
+void launch_enumerate(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
+                      cudaStream_t st, int64_t* launches) {
   Tables T{rank, binom, (int32_t)p.n, kmax};
   switch (p.d) {
-    case 1: enumerate_d<1>(p, T, queue, qcap, ctr, app_pairs, app_cap, st); break;
-    case 2: enumerate_d<2>(p, T, queue, qcap, ctr, app_pairs, app_cap, st); break;
-    case 3: enumerate_d<3>(p, T, queue, qcap, ctr, app_pairs, app_cap, st); break;
-    case 4: enumerate_d<4>(p, T, queue, qcap, ctr, app_pairs, app_cap, st); break;
-    case 5: enumerate_d<5>(p, T, queue, qcap, ctr, app_pairs, app_cap, st); break;
-    case 6: enumerate_d<6>(p, T, queue, qcap, ctr, app_pairs, app_cap, st); break;
+    case 1: enumerate_d<1>(p, T, B, st); break;
+    case 2: enumerate_d<2>(p, T, B, st); break;
+    case 3: enumerate_d<3>(p, T, B, st); break;
+    case 4: enumerate_d<4>(p, T, B, st); break;
+    case 5: enumerate_d<5>(p, T, B, st); break;
+    case 6: enumerate_d<6>(p, T, B, st); break;
     default: return;
   }
   *launches += 1;
 }
 
-void launch_resolve(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const uint64_t* queue,
-                    uint64_t qn, const uint64_t* deaths, int64_t ndeaths, uint64_t* resid, uint64_t rcap,
-                    DimCounters* ctr, uint64_t* app_pairs, uint64_t app_cap, cudaStream_t st, int64_t* launches) {
+void launch_resolve(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
+                    uint64_t qn, cudaStream_t st, int64_t* launches) {
   if (qn == 0) return;
   Tables T{rank, binom, (int32_t)p.n, kmax};
   switch (p.d) {
-    case 1: resolve_d<1>(p, T, queue, qn, deaths, ndeaths, resid, rcap, ctr, app_pairs, app_cap, st); break;
-    case 2: resolve_d<2>(p, T, queue, qn, deaths, ndeaths, resid, rcap, ctr, app_pairs, app_cap, st); break;
-    case 3: resolve_d<3>(p, T, queue, qn, deaths, ndeaths, resid, rcap, ctr, app_pairs, app_cap, st); break;
-    case 4: resolve_d<4>(p, T, queue, qn, deaths, ndeaths, resid, rcap, ctr, app_pairs, app_cap, st); break;
-    case 5: resolve_d<5>(p, T, queue, qn, deaths, ndeaths, resid, rcap, ctr, app_pairs, app_cap, st); break;
-    case 6: resolve_d<6>(p, T, queue, qn, deaths, ndeaths, resid, rcap, ctr, app_pairs, app_cap, st); break;
+    case 1: resolve_d<1>(p, T, B, qn, st); break;
+    case 2: resolve_d<2>(p, T, B, qn, st); break;
+    case 3: resolve_d<3>(p, T, B, qn, st); break;
+    case 4: resolve_d<4>(p, T, B, qn, st); break;
+    case 5: resolve_d<5>(p, T, B, qn, st); break;
+    case 6: resolve_d<6>(p, T, B, qn, st); break;
     default: return;
   }
+  *launches += 1;
+}
+
+void launch_set_bits(const uint64_t* list, int64_t m, uint32_t* bm, cudaStream_t st, int64_t* launches) {
+  if (m <= 0) return;
+  const int64_t blocks = std::min<int64_t>((m + 255) / 256, (int64_t)sm_count() * 8);
+  k_set_bits<<<(unsigned)blocks, 256, 0, st>>>(list, m, bm);
   *launches += 1;
 }
 

@@ -92,6 +92,8 @@ struct DimRun {
   int sort_bits = 0;
   DevBuf deaths_in;  // sorted death cidx of dimension d-1 (clearing input)
   int64_t ndeaths_in = 0;
+  DevBuf clr;        // clearing bitmap over the d-simplices (empty: recompute mode)
+  size_t clr_words = 0;
 };
 
 }  // namespace
@@ -113,7 +115,7 @@ struct vr_plan {
   const float* d_lt = nullptr;
   uint64_t N = 0;
   int kbits = 1, kmax = 0;
-  DevBuf rank, binom, keys, alt, rowmax, sort_tmp, tout, ctrs, queue, resid, resid_alt, app_pairs, lt_copy;
+  DevBuf rank, binom, keys, alt, rowmax, sort_tmp, tout, ctrs, queue, qvert, resid, resid_alt, app_pairs, lt_copy;
   uint64_t qcap = 0, rcap = 0, app_cap = 0;
   uint32_t maxr = 0;
   uint64_t m = 0;
@@ -134,7 +136,8 @@ struct vr_plan {
 
 namespace {
 
-const int kDefaultSteps = 16;
+const int kDefaultSteps = 32;
+const size_t kMaxBitmapBytes = (size_t)4 << 30;
 
 uint64_t binom_host(uint64_t n, uint64_t k) {
   if (k > n) return 0;
@@ -280,23 +283,43 @@ void run_full(vr_plan& P, vr_result* R) {
 
   // ---------------- dimensions 1..D
   P.dims.clear();
-  P.dims.resize((size_t)D + 1);
+  P.dims.resize((size_t)D + 2);
   const int steps = P.opt.apparent_steps > 0 ? P.opt.apparent_steps : kDefaultSteps;
+  // clearing bitmaps (one bit per d-simplex index) where they fit; else recompute mode
+  CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  for (int d = 1; d <= D; ++d) {
+    const uint64_t cand = binom_host((uint64_t)n, (uint64_t)d + 1);
+    const size_t words = (size_t)((cand + 31) / 32);
+    if (cand && P.m && words * 4 <= kMaxBitmapBytes && words * 4 <= free_b / 16) {
+      P.dims[(size_t)d].clr.ensure(words * 4);
+      P.dims[(size_t)d].clr_words = words;
+    }
+  }
+  auto clr_of = [&](int d) -> uint32_t* {
+    return (d >= 1 && d <= D && P.dims[(size_t)d].clr_words) ? P.dims[(size_t)d].clr.as<uint32_t>() : nullptr;
+  };
+  // deaths of dimension 0 -> clearing input of dimension 1
+  {
+    DimRun& d1 = P.dims[1];
+    d1.deaths_in.ensure(std::max<size_t>(deaths.size(), 1) * 8);
+    d1.ndeaths_in = (int64_t)deaths.size();
+    if (!deaths.empty())
+      CUDA_TRY(cudaMemcpyAsync(d1.deaths_in.p, deaths.data(), deaths.size() * 8, cudaMemcpyHostToDevice, st));
+    if (D >= 1 && clr_of(1)) {
+      CUDA_TRY(cudaMemsetAsync(clr_of(1), 0, d1.clr_words * 4, st));
+      vr::launch_set_bits(d1.deaths_in.as<uint64_t>(), d1.ndeaths_in, clr_of(1), st, &P.launches);
+    }
+  }
   for (int d = 1; d <= D; ++d) {
     DimRun& dr = P.dims[(size_t)d];
     vr_stats stt{};
     const uint64_t cand = binom_host((uint64_t)n, (uint64_t)d + 1);
     stt.candidates = (int64_t)cand;
-    // clearing input: deaths of dimension d-1
-    auto tx = std::chrono::steady_clock::now();
-    dr.ndeaths_in = (int64_t)deaths.size();
-    dr.deaths_in.ensure(std::max<size_t>(deaths.size(), 1) * 8);
-    if (!deaths.empty())
-      CUDA_TRY(cudaMemcpyAsync(dr.deaths_in.p, deaths.data(), deaths.size() * 8, cudaMemcpyHostToDevice, st));
-    double ms_tx = ms_since(tx);
+    double ms_tx = 0;
     if (cand == 0 || P.m == 0) {
       if (R) R->stats[(size_t)d] = stt;
       deaths.clear();
+      if (d < D) P.dims[(size_t)d + 1].ndeaths_in = 0;
       continue;
     }
     const int cbits = bits_for(cand - 1);
@@ -310,13 +333,17 @@ void run_full(vr_plan& P, vr_result* R) {
     p.steps = steps;
     const uint64_t rows = binom_host((uint64_t)n, (uint64_t)d);
     dr.sort_bits = rbits + cbits;
+    // the next dimension's bitmap receives this dimension's apparent cofacets
+    uint32_t* clr_next = clr_of(d + 1);
+    if (clr_next) CUDA_TRY(cudaMemsetAsync(clr_next, 0, P.dims[(size_t)d + 1].clr_words * 4, st));
 
-    // queue capacity: every candidate, bounded by a share of free device memory
+    // queue / residual capacity: every candidate, bounded by a share of free device memory
     CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-    uint64_t qmax = (uint64_t)(free_b / 4 / 8);
+    const uint64_t qmax = std::max<uint64_t>((uint64_t)(free_b / 4 / 40), 1024);
     const uint64_t qwant = std::min<uint64_t>(cand, qmax);
     if (P.qcap < qwant) {
       P.queue.ensure((size_t)qwant * 8);
+      P.qvert.ensure((size_t)qwant * 16);
       P.qcap = qwant;
     }
     uint64_t rows_per_chunk = rows;
@@ -335,13 +362,26 @@ void run_full(vr_plan& P, vr_result* R) {
     uint64_t resid_count = 0;
     for (uint64_t rb = 0; rb < rows; rb += rows_per_chunk) {
       const uint64_t re = std::min(rows, rb + rows_per_chunk);
+      const uint64_t chunk_cand = std::min<uint64_t>(cand, (re - rb) * (uint64_t)n);
+      // residual capacity: what is there plus everything this chunk could add
+      if (P.rcap < resid_count + chunk_cand || !P.resid.p) {
+        const uint64_t ncap = std::max<uint64_t>(resid_count + chunk_cand, 1024);
+        DevBuf nb;
+        nb.ensure((size_t)ncap * 8);
+        if (resid_count) CUDA_TRY(cudaMemcpyAsync(nb.p, P.resid.p, resid_count * 8, cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        std::swap(P.resid.p, nb.p);
+        std::swap(P.resid.bytes, nb.bytes);
+        P.rcap = ncap;
+      }
+      vr::HotBuffers B{P.queue.as<uint64_t>(), P.qvert.as<uint4>(), P.qcap, P.resid.as<uint64_t>(), P.rcap,
+                       clr_of(d), clr_next, dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, ctr, app_ptr, app_cap};
       p.row_begin = rb;
       p.row_end = re;
       CUDA_TRY(cudaMemsetAsync(&ctr->row_next, 0, 8, st));
       CUDA_TRY(cudaMemsetAsync(&ctr->queued, 0, 8, st));
       CUDA_TRY(cudaEventRecord(ev[2], st));
-      vr::launch_enumerate(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, P.queue.as<uint64_t>(), P.qcap,
-                           ctr, app_ptr, app_cap, st, &P.launches);
+      vr::launch_enumerate(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, st, &P.launches);
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaEventRecord(ev[3], st));
       unsigned long long q = 0;
@@ -351,21 +391,8 @@ void run_full(vr_plan& P, vr_result* R) {
       float x = 0;
       cudaEventElapsedTime(&x, ev[2], ev[3]);
       t_enum += x;
-      // residual capacity: what is there plus everything queued
-      if (P.rcap < resid_count + q || !P.resid.p) {
-        const uint64_t ncap = std::max<uint64_t>(std::max<uint64_t>(P.rcap * 2, resid_count + q), 1024);
-        DevBuf nb;
-        nb.ensure((size_t)ncap * 8);
-        if (resid_count) CUDA_TRY(cudaMemcpyAsync(nb.p, P.resid.p, resid_count * 8, cudaMemcpyDeviceToDevice, st));
-        std::swap(P.resid.p, nb.p);
-        std::swap(P.resid.bytes, nb.bytes);
-        CUDA_TRY(cudaStreamSynchronize(st));
-        P.rcap = ncap;
-      }
       CUDA_TRY(cudaEventRecord(ev[4], st));
-      vr::launch_resolve(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, P.queue.as<uint64_t>(), q,
-                         dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, P.resid.as<uint64_t>(), P.rcap, ctr, app_ptr,
-                         app_cap, st, &P.launches);
+      vr::launch_resolve(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, q, st, &P.launches);
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaEventRecord(ev[5], st));
       unsigned long long rc = 0;
@@ -373,6 +400,7 @@ void run_full(vr_plan& P, vr_result* R) {
       CUDA_TRY(cudaStreamSynchronize(st));
       cudaEventElapsedTime(&x, ev[4], ev[5]);
       t_res += x;
+      if (rc > P.rcap) throw VrError(VR_ECAPACITY, "residual list overflow");
       resid_count = rc;
       dr.chunks.push_back(Chunk{rb, re, q});
     }
@@ -389,7 +417,7 @@ void run_full(vr_plan& P, vr_result* R) {
     vr::DimCounters hc{};
     CUDA_TRY(cudaMemcpyAsync(&hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, st));
     std::vector<uint64_t> hkeys((size_t)resid_count);
-    tx = std::chrono::steady_clock::now();
+    auto tx = std::chrono::steady_clock::now();
     CUDA_TRY(cudaStreamSynchronize(st));
     float t_sort = 0;
     cudaEventElapsedTime(&t_sort, ev[6], ev[7]);
@@ -405,6 +433,17 @@ void run_full(vr_plan& P, vr_result* R) {
     vr::ResidualStats rst;
     vr::residual_reduce(M, d, P.maxr, cbits, hkeys.data(), resid_count, P.opt.residual_mode, hp[(size_t)d], deaths, rst);
     stt.ms_residual = ms_since(tr);
+    // deaths of dimension d -> clearing input of dimension d+1
+    if (d < D) {
+      tx = std::chrono::steady_clock::now();
+      DimRun& nx = P.dims[(size_t)d + 1];
+      nx.ndeaths_in = (int64_t)deaths.size();
+      nx.deaths_in.ensure(std::max<size_t>(deaths.size(), 1) * 8);
+      if (!deaths.empty())
+        CUDA_TRY(cudaMemcpyAsync(nx.deaths_in.p, deaths.data(), deaths.size() * 8, cudaMemcpyHostToDevice, st));
+      if (clr_next) vr::launch_set_bits(nx.deaths_in.as<uint64_t>(), nx.ndeaths_in, clr_next, st, &P.launches);
+      ms_tx += ms_since(tx);
+    }
     stt.survivors = (int64_t)hc.survivors;
     stt.apparent = (int64_t)(hc.apparent1 + hc.apparent2);
     stt.cleared = (int64_t)hc.cleared;
@@ -417,11 +456,8 @@ void run_full(vr_plan& P, vr_result* R) {
     P.work_rank_ops += (double)(d + 1) * ((double)cand + (double)hc.scanned);
     P.work_rank_ops2 += (double)(d + 1) * (double)hc.scanned2;
     if (const char* dump = std::getenv("VR_DUMP_RESIDUAL")) dump_residual(dump, M, d, P.maxr, cbits, hkeys);
-    stt.queued = (int64_t)hc.queued;  // last chunk only when chunked
-    if (dr.chunks.size() > 1) {
-      stt.queued = 0;
-      for (auto& c : dr.chunks) stt.queued += (int64_t)c.queued;
-    }
+    stt.queued = 0;
+    for (auto& c : dr.chunks) stt.queued += (int64_t)c.queued;
     stt.ms_enumerate = t_enum;
     stt.ms_resolve = t_res;
     stt.ms_sort = t_sort;
@@ -461,7 +497,8 @@ void run_full(vr_plan& P, vr_result* R) {
 }
 
 // Re-launch the GPU hot path of every dimension with the recorded sizes (no host sync).
-// Each stage is bracketed by CUDA events on the plan's stream (vr_plan_timing).
+// Each stage is bracketed by CUDA events on the plan's stream (vr_plan_timing).  The
+// clearing inputs are the device death lists recorded by the full run.
 void replay(vr_plan& P) {
   cudaStream_t st = P.st;
   int used[4] = {0, 0, 0, 0};
@@ -475,42 +512,56 @@ void replay(vr_plan& P) {
     }
     return v[(size_t)used[stage]++];
   };
+  auto clr_of = [&](int d) -> uint32_t* {
+    return (d >= 1 && d <= P.D && P.dims[(size_t)d].clr_words) ? P.dims[(size_t)d].clr.as<uint32_t>() : nullptr;
+  };
   uint64_t* sorted = nullptr;
   {
     auto& e = ev(0);
     cudaEventRecord(e.first, st);
     vr::launch_tables(P.d_lt, P.n, P.threshold, P.keys.as<uint64_t>(), P.alt.as<uint64_t>(), P.rowmax.as<uint32_t>(),
                       P.sort_tmp.p, P.rank.as<uint32_t>(), P.tout.as<vr::TablesOut>(), &sorted, st, &P.launches);
+    if (P.D >= 1 && clr_of(1)) {
+      cudaMemsetAsync(clr_of(1), 0, P.dims[1].clr_words * 4, st);
+      vr::launch_set_bits(P.dims[1].deaths_in.as<uint64_t>(), P.dims[1].ndeaths_in, clr_of(1), st, &P.launches);
+    }
     cudaEventRecord(e.second, st);
   }
   for (int d = 1; d <= P.D; ++d) {
     DimRun& dr = P.dims[(size_t)d];
     if (dr.chunks.empty()) continue;
     vr::DimCounters* ctr = P.ctrs.as<vr::DimCounters>() + d;
+    uint32_t* clr_next = clr_of(d + 1);
+    auto& e1 = ev(1);
+    cudaEventRecord(e1.first, st);
     cudaMemsetAsync(ctr, 0, sizeof(vr::DimCounters), st);
+    if (clr_next) cudaMemsetAsync(clr_next, 0, P.dims[(size_t)d + 1].clr_words * 4, st);
+    cudaEventRecord(e1.second, st);
     vr::DimParams p = dr.p;
     for (const Chunk& c : dr.chunks) {
+      vr::HotBuffers B{P.queue.as<uint64_t>(), P.qvert.as<uint4>(), P.qcap, P.resid.as<uint64_t>(), P.rcap,
+                       clr_of(d), clr_next, dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, ctr, nullptr, 0};
       p.row_begin = c.row_begin;
       p.row_end = c.row_end;
+      auto& e2 = ev(1);
+      cudaEventRecord(e2.first, st);
       cudaMemsetAsync(&ctr->row_next, 0, 8, st);
       cudaMemsetAsync(&ctr->queued, 0, 8, st);
-      auto& e1 = ev(1);
-      cudaEventRecord(e1.first, st);
-      vr::launch_enumerate(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, P.queue.as<uint64_t>(), P.qcap, ctr,
-                           nullptr, 0, st, &P.launches);
-      cudaEventRecord(e1.second, st);
-      auto& e2 = ev(2);
-      cudaEventRecord(e2.first, st);
-      vr::launch_resolve(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, P.queue.as<uint64_t>(), c.queued,
-                         dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, P.resid.as<uint64_t>(), P.rcap, ctr, nullptr, 0,
-                         st, &P.launches);
+      vr::launch_enumerate(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, st, &P.launches);
       cudaEventRecord(e2.second, st);
+      auto& e3 = ev(2);
+      cudaEventRecord(e3.first, st);
+      vr::launch_resolve(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, c.queued, st, &P.launches);
+      cudaEventRecord(e3.second, st);
     }
-    auto& e3 = ev(3);
-    cudaEventRecord(e3.first, st);
+    auto& e4 = ev(3);
+    cudaEventRecord(e4.first, st);
     vr::radix_sort_u64(P.resid.as<uint64_t>(), P.resid_alt.as<uint64_t>(), dr.residual, 0, dr.sort_bits, P.sort_tmp.p,
                        st, &P.launches);
-    cudaEventRecord(e3.second, st);
+    if (d < P.D && clr_next)
+      vr::launch_set_bits(P.dims[(size_t)d + 1].deaths_in.as<uint64_t>(), P.dims[(size_t)d + 1].ndeaths_in, clr_next,
+                          st, &P.launches);
+    cudaEventRecord(e4.second, st);
   }
   P.used_events[0] = used[0]; P.used_events[1] = used[1]; P.used_events[2] = used[2]; P.used_events[3] = used[3];
 }

@@ -39,12 +39,25 @@ struct DimParams {
 struct DimCounters {   // device counters (unsigned long long each)
   unsigned long long survivors, apparent1, apparent2, cleared, queued, residual, row_next, app_pairs, scanned, scanned2;
 };
-void launch_enumerate(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, uint64_t* queue,
-                      uint64_t qcap, DimCounters* ctr, uint64_t* app_pairs, uint64_t app_cap, cudaStream_t st,
-                      int64_t* launches);
-void launch_resolve(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const uint64_t* queue,
-                    uint64_t qn, const uint64_t* deaths, int64_t ndeaths, uint64_t* resid, uint64_t rcap,
-                    DimCounters* ctr, uint64_t* app_pairs, uint64_t app_cap, cudaStream_t st, int64_t* launches);
+struct HotBuffers {
+  uint64_t* qkey;        // phase-2 queue: column keys
+  uint4* qvert;          // phase-2 queue: packed vertices (16 bits each, s[0] > ... > s[d])
+  uint64_t qcap;
+  uint64_t* resid;       // residual (non-apparent, non-cleared) column keys
+  uint64_t rcap;
+  const uint32_t* clr;   // clearing bitmap over the d-simplices, or nullptr (recompute mode)
+  uint32_t* clr_next;    // bitmap of dimension d+1 receiving apparent cofacets, or nullptr
+  const uint64_t* deaths;// recompute mode: sorted residual deaths of dimension d-1
+  int64_t ndeaths;
+  DimCounters* ctr;
+  uint64_t* app_pairs;   // debug (index-level output): (s, t) per apparent pair, or nullptr
+  uint64_t app_cap;
+};
+void launch_enumerate(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
+                      cudaStream_t st, int64_t* launches);
+void launch_resolve(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
+                    uint64_t qn, cudaStream_t st, int64_t* launches);
+void launch_set_bits(const uint64_t* list, int64_t m, uint32_t* bm, cudaStream_t st, int64_t* launches);
 
 // ---------------------------------------------------------------- host.cpp (off-path)
 struct HostPairs {
