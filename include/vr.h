@@ -156,6 +156,14 @@ int vr_plan_check(vr_plan* plan, int64_t* apparent_total, int64_t* residual_tota
 int vr_plan_timing(vr_plan* plan, double out[9]);
 void vr_plan_free(vr_plan* plan);
 
+/* ----------------------------------------------------------------------------------
+ * Component entry (tests): the library's device radix sort on
+ * caller keys.  keys: HOST pointer to n uint64 values, sorted ascending in place on bits
+ * [begin_bit, end_bit) (LSD, stable; bits outside the range do not take part in the
+ * order), using the current device.  Returns VR_OK or an error code.
+ * ---------------------------------------------------------------------------------- */
+int vr_radix_sort_u64(uint64_t* keys, int64_t n, int32_t begin_bit, int32_t end_bit);
+
 #ifdef __cplusplus
 }
 #endif

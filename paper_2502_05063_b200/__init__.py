@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-__all__ = ["barcodes", "barcodes_device", "Plan", "Barcode", "VRError", "lib_path", "load"]
+__all__ = ["barcodes", "barcodes_device", "radix_sort_u64", "Plan", "Barcode", "VRError", "lib_path", "load"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_HERE, "libvr.so")
@@ -88,6 +88,7 @@ def load() -> ctypes.CDLL:
         "vr_plan_check": (ctypes.c_int, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
         "vr_plan_timing": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double)]),
         "vr_plan_free": (None, [vp]),
+        "vr_radix_sort_u64": (ctypes.c_int, [vp, i64, i32, i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -187,6 +188,13 @@ def _device_ptr_and_stream(t, n, stream):
     else:
         st = getattr(stream, "cuda_stream", stream)
     return ctypes.c_void_p(ptr or None), ctypes.c_void_p(st or None)
+
+
+def radix_sort_u64(keys: np.ndarray, begin_bit: int = 0, end_bit: int = 64) -> np.ndarray:
+    """The library's device LSD radix sort on bits [begin_bit, end_bit) (component test entry)."""
+    a = np.ascontiguousarray(keys, dtype=np.uint64).copy()
+    _check(load().vr_radix_sort_u64(a.ctypes.data if a.size else None, a.size, begin_bit, end_bit))
+    return a
 
 
 class Plan:

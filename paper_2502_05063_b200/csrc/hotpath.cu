@@ -106,7 +106,11 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
     }
     mup0 = m;
   }
-  const int steps = p.steps;
+  const int steps = p.steps < n ? p.steps : n;
+  const uint32_t* __restrict__ rowu[D + 1];
+#pragma unroll
+  for (int i = 1; i <= D; ++i) rowu[i] = T.rank + (size_t)u[i] * (size_t)n;
+  const uint32_t* __restrict__ rowtop = T.rank + (size_t)(n - 1) * (size_t)n;  // row of v = n-1
 
   for (int base = 0; base < v1; base += 32) {
     const int v0 = base + lane;
@@ -115,7 +119,7 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
     uint32_t rs = pm_up;
 #pragma unroll
     for (int i = 1; i <= D; ++i) {
-      a[i] = valid ? rank_at(T, u[i], v0) : VR_RINF;
+      a[i] = valid ? __ldg(rowu[i] + v0) : VR_RINF;
       rs = umax(rs, a[i]);
     }
     const bool surv = valid && rs != VR_RINF;  // diam(s) <= t (Eq 5.3, Alg 17 line 3)
@@ -128,28 +132,34 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
     clr_acc += __popc(__ballot_sync(0xffffffffu, cleared));
     bool active = surv && !cleared;
     int hitv = -1;
-    // Lemma 5.3.6 condition 1, lane-parallel: the first v with every new edge <= diam(s)
-    for (int j = 0; j < steps; ++j) {
-      const uint32_t mact = __ballot_sync(0xffffffffu, active);
-      if (!mact) break;
-      const int v = n - 1 - j;
-      if (v < 0) break;
-      uint32_t m;
-      if (j < 32) {
-        m = __shfl_sync(0xffffffffu, mup0, j);
-      } else {
-        m = 0;
+    int examined = 0;  // cofacet vertices this lane examined
+    // Lemma 5.3.6 condition 1, lane-parallel: the first v with every new edge <= diam(s);
+    // one warp vote per 4 vertices, loads only for lanes whose prefix part allows a hit
+    const uint32_t* __restrict__ pv = rowtop + v0;  // &R[v][v0] for v = n-1-j
+    for (int j = 0; j < steps; j += 4) {
 #pragma unroll
-        for (int i = 1; i <= D; ++i) m = (v == u[i]) ? VR_RINF : umax(m, rank_at(T, u[i], v));
+      for (int q = 0; q < 4; ++q) {
+        const int jj = j + q;
+        const int v = n - 1 - jj;
+        uint32_t m;
+        if (jj < 32) {
+          m = __shfl_sync(0xffffffffu, mup0, jj & 31);
+        } else {
+          m = 0;
+#pragma unroll
+          for (int i = 1; i <= D; ++i) m = (v == u[i]) ? VR_RINF : umax(m, __ldg(rowu[i] + (v < 0 ? 0 : v)));
+        }
+        if (active && jj < steps) {
+          ++examined;
+          if (m <= rs && v != v0 && umax(m, __ldg(pv - (size_t)jj * (size_t)n)) <= rs) {
+            hitv = v;
+            active = false;
+          }
+        }
       }
-      if (!__any_sync(0xffffffffu, active && m <= rs)) continue;  // no lane can hit at v
-      scan_acc += __popc(mact);
-      const uint32_t b0 = active ? rank_at(T, v, v0) : VR_RINF;
-      if (active && v != v0 && umax(m, b0) <= rs) {
-        hitv = v;
-        active = false;
-      }
+      if (!__any_sync(0xffffffffu, active)) break;
     }
+    scan_acc += (unsigned long long)__reduce_add_sync(0xffffffffu, (unsigned)examined);
     // condition 2 for lanes that found t = s ∪ {hitv}: no facet t \ {w}, w > hitv (the
     // lex-smaller facets), with diam = diam(s)
     bool app = false;
@@ -212,7 +222,7 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
 
 template <int D>
 __global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p, HotBuffers B) {
-  constexpr int GRAB = 4;
+  constexpr int GRAB = 16;
   const int lane = threadIdx.x & 31;
   unsigned long long surv_acc = 0, app_acc = 0, scan_acc = 0, clr_acc = 0;
   while (true) {
@@ -408,7 +418,7 @@ static int sm_count() {
 template <int D>
 static void enumerate_d(const DimParams& p, const Tables& T, const HotBuffers& B, cudaStream_t st) {
   const uint64_t rows = p.row_end - p.row_begin;
-  const uint64_t warps_needed = (rows + 3) / 4;
+  const uint64_t warps_needed = (rows + 15) / 16;
   uint64_t blocks = (warps_needed * 32 + HP_THREADS - 1) / HP_THREADS;
   const uint64_t cap = (uint64_t)sm_count() * 8;  // 8 resident CTAs of 256 threads per SM
   if (blocks > cap) blocks = cap;

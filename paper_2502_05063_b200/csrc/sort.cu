@@ -202,6 +202,104 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint64_t* __restr
   }
 }
 
+
+// Tile ranking shared by the kernels below: stable per-warp-segment multisplit of keys_s
+// (cnt valid keys) on digit `shift`, writing the keys in digit order to sorted_s and the
+// tile's digit starts to dstart.  All 256 threads of the block must call it.
+__device__ __forceinline__ void rs_tile_rank(const uint64_t* keys_s, uint64_t* sorted_s, int cnt, int shift,
+                                             uint32_t* whist, uint32_t* dstart, uint32_t* warp_tot, uint32_t* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < RS_WARPS * RS_BINS; i += RS_THREADS) whist[i] = 0;
+  __syncthreads();
+  const int seg0 = w * RS_SEG;
+  for (int i = seg0 + lane; i < seg0 + RS_SEG; i += 32)
+    if (i < cnt) atomicAdd(&whist[w * RS_BINS + ((uint32_t)(keys_s[i] >> shift) & (RS_BINS - 1))], 1u);
+  __syncthreads();
+  {
+    const int b = threadIdx.x;
+    uint32_t run = 0;
+#pragma unroll
+    for (int q = 0; q < RS_WARPS; ++q) {
+      uint32_t t = whist[q * RS_BINS + b];
+      whist[q * RS_BINS + b] = run;
+      run += t;
+    }
+    dstart[b] = block_exclusive_scan_256(run, warp_tot, total);
+  }
+  __syncthreads();
+  for (int i0 = seg0; i0 < seg0 + RS_SEG; i0 += 32) {
+    const int i = i0 + lane;
+    const bool valid = i < cnt;
+    const uint64_t k = valid ? keys_s[i] : 0ull;
+    const uint32_t dg = valid ? ((uint32_t)(k >> shift) & (RS_BINS - 1)) : (RS_BINS + lane);
+    const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+    uint32_t pos = 0;
+    if (valid) pos = dstart[dg] + whist[w * RS_BINS + dg] + __popc(peers & lanemask_lt());
+    __syncwarp();
+    if (valid && (lane == 31 - __clz(peers))) whist[w * RS_BINS + dg] += __popc(peers);
+    if (valid) sorted_s[pos] = k;
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
+// Whole sort of n <= RS_TILE keys in one CTA, every pass in shared memory, one launch.
+__global__ void __launch_bounds__(RS_THREADS) rs_small(uint64_t* __restrict__ keys, int n, int begin_bit, int end_bit) {
+  extern __shared__ __align__(16) unsigned char rs_smem[];
+  uint64_t* A = (uint64_t*)rs_smem;
+  uint64_t* Bk = A + RS_TILE;
+  uint32_t* whist = (uint32_t*)(Bk + RS_TILE);
+  uint32_t* dstart = whist + RS_WARPS * RS_BINS;
+  __shared__ uint32_t warp_tot[SC_THREADS / 32];
+  __shared__ uint32_t total;
+  for (int i = threadIdx.x; i < n; i += RS_THREADS) A[i] = keys[i];
+  __syncthreads();
+  for (int shift = begin_bit; shift < end_bit; shift += 8) {
+    rs_tile_rank(A, Bk, n, shift, whist, dstart, warp_tot, &total);
+    uint64_t* t = A; A = Bk; Bk = t;
+  }
+  for (int i = threadIdx.x; i < n; i += RS_THREADS) keys[i] = A[i];
+}
+
+// Scatter for up to RS_FUSED_TILES tiles: the block computes its own digit offsets from
+// the per-tile histogram (no separate scan launch).
+constexpr uint32_t RS_FUSED_TILES = 256;
+__global__ void __launch_bounds__(RS_THREADS) rs_scatter_fused(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
+                                                               size_t n, int shift, const uint32_t* __restrict__ tile_hist,
+                                                               uint32_t ntiles) {
+  extern __shared__ __align__(16) unsigned char rs_smem[];
+  uint64_t* keys_s = (uint64_t*)rs_smem;
+  uint64_t* sorted_s = keys_s + RS_TILE;
+  uint32_t* whist = (uint32_t*)(sorted_s + RS_TILE);
+  uint32_t* dstart = whist + RS_WARPS * RS_BINS;
+  uint32_t* gofs = dstart + RS_BINS;
+  __shared__ uint32_t warp_tot[SC_THREADS / 32];
+  __shared__ uint32_t total;
+  const size_t base = (size_t)blockIdx.x * RS_TILE;
+  const int cnt = (int)((n - base) < (size_t)RS_TILE ? (n - base) : (size_t)RS_TILE);
+  for (int i = threadIdx.x; i < RS_TILE; i += RS_THREADS) keys_s[i] = i < cnt ? in[base + i] : ~0ull;
+  // global offset of digit b for this tile = sum over digits < b of all tiles
+  //                                          + sum over earlier tiles of digit b
+  {
+    const int b = threadIdx.x;
+    uint32_t tot_b = 0, before = 0;
+    for (uint32_t t = 0; t < ntiles; ++t) {
+      const uint32_t c = tile_hist[(size_t)b * ntiles + t];
+      tot_b += c;
+      if (t < blockIdx.x) before += c;
+    }
+    const uint32_t dig_start = block_exclusive_scan_256(tot_b, warp_tot, &total);
+    gofs[b] = dig_start + before;
+  }
+  __syncthreads();
+  rs_tile_rank(keys_s, sorted_s, cnt, shift, whist, dstart, warp_tot, &total);
+  for (int j = threadIdx.x; j < cnt; j += RS_THREADS) {
+    const uint64_t k = sorted_s[j];
+    const uint32_t dg = (uint32_t)(k >> shift) & (RS_BINS - 1);
+    out[(size_t)gofs[dg] + (size_t)(j - (int)dstart[dg])] = k;
+  }
+}
+
 static size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
 size_t radix_sort_temp_bytes(size_t n) {
@@ -220,7 +318,14 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit,
   const size_t smem = 2 * RS_TILE * sizeof(uint64_t) + (RS_WARPS * RS_BINS + 2 * RS_BINS) * sizeof(uint32_t);
   if (!g_rs_attr_done) {
     cudaFuncSetAttribute(rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(rs_scatter_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(rs_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     g_rs_attr_done = true;
+  }
+  if (n <= (size_t)RS_TILE) {  // one CTA, all passes in shared memory
+    rs_small<<<1, RS_THREADS, smem, st>>>(keys, (int)n, begin_bit, end_bit);
+    if (launches) *launches += 1;
+    return keys;
   }
   const uint32_t ntiles = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
   uint32_t* hist = (uint32_t*)temp;
@@ -229,8 +334,12 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit,
   uint64_t* dst = alt;
   for (int shift = begin_bit; shift < end_bit; shift += 8) {
     rs_hist<<<ntiles, RS_THREADS, 0, st>>>(src, n, shift, hist, ntiles);
-    exclusive_scan_u32(hist, hist, (size_t)RS_BINS * ntiles, scan_tmp, st, launches);
-    rs_scatter<<<ntiles, RS_THREADS, smem, st>>>(src, dst, n, shift, hist, ntiles);
+    if (ntiles <= RS_FUSED_TILES) {
+      rs_scatter_fused<<<ntiles, RS_THREADS, smem, st>>>(src, dst, n, shift, hist, ntiles);
+    } else {
+      exclusive_scan_u32(hist, hist, (size_t)RS_BINS * ntiles, scan_tmp, st, launches);
+      rs_scatter<<<ntiles, RS_THREADS, smem, st>>>(src, dst, n, shift, hist, ntiles);
+    }
     if (launches) *launches += 2;
     uint64_t* t = src; src = dst; dst = t;
   }

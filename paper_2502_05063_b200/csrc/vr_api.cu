@@ -730,4 +730,21 @@ int vr_plan_timing(vr_plan* P, double out[9]) {
 
 void vr_plan_free(vr_plan* P) { delete P; }
 
+int vr_radix_sort_u64(uint64_t* keys, int64_t n, int32_t begin_bit, int32_t end_bit) {
+  return guarded([&] {
+    if (n < 0 || (n > 0 && !keys) || begin_bit < 0 || end_bit > 64 || begin_bit > end_bit)
+      throw VrError(VR_EINVAL, "vr_radix_sort_u64: bad arguments");
+    if (n <= 1) return;
+    DevBuf a, b, t;
+    a.ensure((size_t)n * 8);
+    b.ensure((size_t)n * 8);
+    t.ensure(vr::radix_sort_temp_bytes((size_t)n));
+    CUDA_TRY(cudaMemcpy(a.p, keys, (size_t)n * 8, cudaMemcpyHostToDevice));
+    int64_t launches = 0;
+    uint64_t* r = vr::radix_sort_u64(a.as<uint64_t>(), b.as<uint64_t>(), (size_t)n, begin_bit, end_bit, t.p, 0, &launches);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpy(keys, r, (size_t)n * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
 }  // extern "C"

@@ -218,3 +218,19 @@ def test_betti_circle_and_s3():
     b = vr.barcodes(c2.lower_tri(), c2.n, 3)
     p3 = b.pairs[3][:, 1] - b.pairs[3][:, 0]
     assert len(p3) >= 1 and np.sort(p3)[-1] > 3 * (np.sort(p3)[-2] if len(p3) > 1 else 0)
+
+
+# ------------------------------------------------------------------ a4 alone: the radix sort
+@pytest.mark.parametrize("n", [0, 1, 2, 100, 4096, 4097, 70000, 1_200_000])
+@pytest.mark.parametrize("bits", [(0, 64), (0, 41), (8, 40)])
+def test_radix_sort_matches_numpy(n, bits):
+    rng = np.random.default_rng(n + bits[1])
+    keys = rng.integers(0, 2**63, n, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, n, dtype=np.uint64)
+    if n > 10:
+        keys[: n // 3] = keys[n // 3: 2 * (n // 3)]  # many duplicates
+    got = vr.radix_sort_u64(keys, *bits)
+    b0, b1 = bits
+    mask = np.uint64(((1 << (b1 - b0)) - 1) << b0) if b1 - b0 < 64 else np.uint64(2**64 - 1)
+    sub = keys & mask
+    order = np.argsort(sub, kind="stable")  # LSD radix sort is stable on the sorted bits
+    assert np.array_equal(got, keys[order])
