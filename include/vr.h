@@ -74,7 +74,10 @@ typedef struct {
                             the apparent test before a column moves to the warp-cooperative
                             phase; 0 = library default */
   int32_t device;        /* CUDA device ordinal used by vr_barcodes (host-pointer entry) */
-  int32_t reserved[7];
+  int32_t rows_per_grab; /* tuning: prefix rows a warp takes per atomic grab; 0 = default (4) */
+  int32_t scan_variant;  /* tuning: phase-1 scan loop (0: one warp vote per cofacet vertex,
+                            1: one vote per 4 vertices); results are identical */
+  int32_t reserved[5];
 } vr_options;
 
 /* Per-dimension statistics (Table 5.1 / 5.5 counters, stage times). */

@@ -133,31 +133,54 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
     bool active = surv && !cleared;
     int hitv = -1;
     int examined = 0;  // cofacet vertices this lane examined
-    // Lemma 5.3.6 condition 1, lane-parallel: the first v with every new edge <= diam(s);
-    // one warp vote per 4 vertices, loads only for lanes whose prefix part allows a hit
-    const uint32_t* __restrict__ pv = rowtop + v0;  // &R[v][v0] for v = n-1-j
-    for (int j = 0; j < steps; j += 4) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int jj = j + q;
-        const int v = n - 1 - jj;
+    // Lemma 5.3.6 condition 1, lane-parallel: the first v with every new edge <= diam(s)
+    const uint32_t* __restrict__ pv = rowtop + v0;  // &R[v][v0], v = n-1-j
+    if (p.variant == 0) {
+      // one vote per vertex; vertices no active lane can hit are skipped without loads
+      for (int j = 0; j < steps; ++j, pv -= n) {
+        const uint32_t mact = __ballot_sync(0xffffffffu, active);
+        if (!mact) break;
+        const int v = n - 1 - j;
         uint32_t m;
-        if (jj < 32) {
-          m = __shfl_sync(0xffffffffu, mup0, jj & 31);
+        if (j < 32) {
+          m = __shfl_sync(0xffffffffu, mup0, j);
         } else {
           m = 0;
 #pragma unroll
-          for (int i = 1; i <= D; ++i) m = (v == u[i]) ? VR_RINF : umax(m, __ldg(rowu[i] + (v < 0 ? 0 : v)));
+          for (int i = 1; i <= D; ++i) m = (v == u[i]) ? VR_RINF : umax(m, __ldg(rowu[i] + v));
         }
-        if (active && jj < steps) {
-          ++examined;
-          if (m <= rs && v != v0 && umax(m, __ldg(pv - (size_t)jj * (size_t)n)) <= rs) {
-            hitv = v;
-            active = false;
-          }
+        examined += active;
+        if (!__any_sync(0xffffffffu, active && m <= rs)) continue;
+        if (active && v != v0 && m <= rs && umax(m, __ldg(pv)) <= rs) {
+          hitv = v;
+          active = false;
         }
       }
-      if (!__any_sync(0xffffffffu, active)) break;
+    } else {
+      // one vote per 4 vertices
+      for (int j = 0; j < steps; j += 4) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int jj = j + q;
+          const int v = n - 1 - jj;
+          uint32_t m;
+          if (jj < 32) {
+            m = __shfl_sync(0xffffffffu, mup0, jj & 31);
+          } else {
+            m = 0;
+#pragma unroll
+            for (int i = 1; i <= D; ++i) m = (v == u[i]) ? VR_RINF : umax(m, __ldg(rowu[i] + (v < 0 ? 0 : v)));
+          }
+          if (active && jj < steps) {
+            ++examined;
+            if (m <= rs && v != v0 && umax(m, __ldg(pv - (size_t)jj * (size_t)n)) <= rs) {
+              hitv = v;
+              active = false;
+            }
+          }
+        }
+        if (!__any_sync(0xffffffffu, active)) break;
+      }
     }
     scan_acc += (unsigned long long)__reduce_add_sync(0xffffffffu, (unsigned)examined);
     // condition 2 for lanes that found t = s ∪ {hitv}: no facet t \ {w}, w > hitv (the
@@ -222,7 +245,7 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
 
 template <int D>
 __global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p, HotBuffers B) {
-  constexpr int GRAB = 16;
+  const int GRAB = p.grab;
   const int lane = threadIdx.x & 31;
   unsigned long long surv_acc = 0, app_acc = 0, scan_acc = 0, clr_acc = 0;
   while (true) {
@@ -418,7 +441,7 @@ static int sm_count() {
 template <int D>
 static void enumerate_d(const DimParams& p, const Tables& T, const HotBuffers& B, cudaStream_t st) {
   const uint64_t rows = p.row_end - p.row_begin;
-  const uint64_t warps_needed = (rows + 15) / 16;
+  const uint64_t warps_needed = (rows + (uint64_t)p.grab - 1) / (uint64_t)p.grab;
   uint64_t blocks = (warps_needed * 32 + HP_THREADS - 1) / HP_THREADS;
   const uint64_t cap = (uint64_t)sm_count() * 8;  // 8 resident CTAs of 256 threads per SM
   if (blocks > cap) blocks = cap;

@@ -124,7 +124,7 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t n, void* temp,
 
 // ------------------------------------------------------------------ radix sort
 __global__ void __launch_bounds__(RS_THREADS) rs_hist(const uint64_t* __restrict__ keys, size_t n, int shift,
-                                                      uint32_t* __restrict__ tile_hist, uint32_t ntiles) {
+                                                      uint32_t* __restrict__ tile_hist, uint32_t ntiles, uint32_t dmask) {
   __shared__ uint32_t h[RS_BINS];
   h[threadIdx.x] = 0;
   __syncthreads();
@@ -132,14 +132,14 @@ __global__ void __launch_bounds__(RS_THREADS) rs_hist(const uint64_t* __restrict
 #pragma unroll 4
   for (int i = 0; i < RS_ITEMS; ++i) {
     size_t k = base + (size_t)i * RS_THREADS + threadIdx.x;
-    if (k < n) atomicAdd(&h[(uint32_t)(__ldg(keys + k) >> shift) & (RS_BINS - 1)], 1u);
+    if (k < n) atomicAdd(&h[(uint32_t)(__ldg(keys + k) >> shift) & dmask], 1u);
   }
   __syncthreads();
   tile_hist[(size_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
 
 __global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, size_t n, int shift,
-                                                         const uint32_t* __restrict__ offsets, uint32_t ntiles) {
+                                                         const uint32_t* __restrict__ offsets, uint32_t ntiles, uint32_t dmask) {
   extern __shared__ __align__(16) unsigned char rs_smem[];
   uint64_t* keys_s = (uint64_t*)rs_smem;                 // tile keys, input order
   uint64_t* sorted_s = keys_s + RS_TILE;                 // tile keys, digit order
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint64_t* __restr
   // per-warp digit counts over the warp's contiguous segment
   const int seg0 = w * RS_SEG;
   for (int i = seg0 + lane; i < seg0 + RS_SEG; i += 32)
-    if (i < cnt) atomicAdd(&whist[w * RS_BINS + ((uint32_t)(keys_s[i] >> shift) & (RS_BINS - 1))], 1u);
+    if (i < cnt) atomicAdd(&whist[w * RS_BINS + ((uint32_t)(keys_s[i] >> shift) & dmask)], 1u);
   __syncthreads();
 
   // thread b: exclusive prefix over warps of digit b; tile total of digit b
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint64_t* __restr
     const int i = i0 + lane;
     const bool valid = i < cnt;
     const uint64_t k = keys_s[i];
-    const uint32_t dg = valid ? ((uint32_t)(k >> shift) & (RS_BINS - 1)) : (RS_BINS + lane);
+    const uint32_t dg = valid ? ((uint32_t)(k >> shift) & dmask) : (RS_BINS + lane);
     const uint32_t peers = __match_any_sync(0xffffffffu, dg);
     uint32_t pos = 0;
     if (valid) pos = dstart[dg] + whist[w * RS_BINS + dg] + __popc(peers & lanemask_lt());
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint64_t* __restr
 
   for (int j = threadIdx.x; j < cnt; j += RS_THREADS) {
     const uint64_t k = sorted_s[j];
-    const uint32_t dg = (uint32_t)(k >> shift) & (RS_BINS - 1);
+    const uint32_t dg = (uint32_t)(k >> shift) & dmask;
     out[(size_t)gofs[dg] + (size_t)(j - (int)dstart[dg])] = k;
   }
 }
@@ -206,14 +206,14 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint64_t* __restr
 // Tile ranking shared by the kernels below: stable per-warp-segment multisplit of keys_s
 // (cnt valid keys) on digit `shift`, writing the keys in digit order to sorted_s and the
 // tile's digit starts to dstart.  All 256 threads of the block must call it.
-__device__ __forceinline__ void rs_tile_rank(const uint64_t* keys_s, uint64_t* sorted_s, int cnt, int shift,
+__device__ __forceinline__ void rs_tile_rank(const uint64_t* keys_s, uint64_t* sorted_s, int cnt, int shift, uint32_t dmask,
                                              uint32_t* whist, uint32_t* dstart, uint32_t* warp_tot, uint32_t* total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < RS_WARPS * RS_BINS; i += RS_THREADS) whist[i] = 0;
   __syncthreads();
   const int seg0 = w * RS_SEG;
   for (int i = seg0 + lane; i < seg0 + RS_SEG; i += 32)
-    if (i < cnt) atomicAdd(&whist[w * RS_BINS + ((uint32_t)(keys_s[i] >> shift) & (RS_BINS - 1))], 1u);
+    if (i < cnt) atomicAdd(&whist[w * RS_BINS + ((uint32_t)(keys_s[i] >> shift) & dmask)], 1u);
   __syncthreads();
   {
     const int b = threadIdx.x;
@@ -231,7 +231,7 @@ __device__ __forceinline__ void rs_tile_rank(const uint64_t* keys_s, uint64_t* s
     const int i = i0 + lane;
     const bool valid = i < cnt;
     const uint64_t k = valid ? keys_s[i] : 0ull;
-    const uint32_t dg = valid ? ((uint32_t)(k >> shift) & (RS_BINS - 1)) : (RS_BINS + lane);
+    const uint32_t dg = valid ? ((uint32_t)(k >> shift) & dmask) : (RS_BINS + lane);
     const uint32_t peers = __match_any_sync(0xffffffffu, dg);
     uint32_t pos = 0;
     if (valid) pos = dstart[dg] + whist[w * RS_BINS + dg] + __popc(peers & lanemask_lt());
@@ -255,7 +255,8 @@ __global__ void __launch_bounds__(RS_THREADS) rs_small(uint64_t* __restrict__ ke
   for (int i = threadIdx.x; i < n; i += RS_THREADS) A[i] = keys[i];
   __syncthreads();
   for (int shift = begin_bit; shift < end_bit; shift += 8) {
-    rs_tile_rank(A, Bk, n, shift, whist, dstart, warp_tot, &total);
+    const uint32_t dmask = end_bit - shift >= 8 ? 0xFFu : ((1u << (end_bit - shift)) - 1u);
+    rs_tile_rank(A, Bk, n, shift, dmask, whist, dstart, warp_tot, &total);
     uint64_t* t = A; A = Bk; Bk = t;
   }
   for (int i = threadIdx.x; i < n; i += RS_THREADS) keys[i] = A[i];
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(RS_THREADS) rs_small(uint64_t* __restrict__ ke
 constexpr uint32_t RS_FUSED_TILES = 256;
 __global__ void __launch_bounds__(RS_THREADS) rs_scatter_fused(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
                                                                size_t n, int shift, const uint32_t* __restrict__ tile_hist,
-                                                               uint32_t ntiles) {
+                                                               uint32_t ntiles, uint32_t dmask) {
   extern __shared__ __align__(16) unsigned char rs_smem[];
   uint64_t* keys_s = (uint64_t*)rs_smem;
   uint64_t* sorted_s = keys_s + RS_TILE;
@@ -292,10 +293,10 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter_fused(const uint64_t* _
     gofs[b] = dig_start + before;
   }
   __syncthreads();
-  rs_tile_rank(keys_s, sorted_s, cnt, shift, whist, dstart, warp_tot, &total);
+  rs_tile_rank(keys_s, sorted_s, cnt, shift, dmask, whist, dstart, warp_tot, &total);
   for (int j = threadIdx.x; j < cnt; j += RS_THREADS) {
     const uint64_t k = sorted_s[j];
-    const uint32_t dg = (uint32_t)(k >> shift) & (RS_BINS - 1);
+    const uint32_t dg = (uint32_t)(k >> shift) & dmask;
     out[(size_t)gofs[dg] + (size_t)(j - (int)dstart[dg])] = k;
   }
 }
@@ -333,12 +334,13 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit,
   uint64_t* src = keys;
   uint64_t* dst = alt;
   for (int shift = begin_bit; shift < end_bit; shift += 8) {
-    rs_hist<<<ntiles, RS_THREADS, 0, st>>>(src, n, shift, hist, ntiles);
+    const uint32_t dmask = end_bit - shift >= 8 ? 0xFFu : ((1u << (end_bit - shift)) - 1u);
+    rs_hist<<<ntiles, RS_THREADS, 0, st>>>(src, n, shift, hist, ntiles, dmask);
     if (ntiles <= RS_FUSED_TILES) {
-      rs_scatter_fused<<<ntiles, RS_THREADS, smem, st>>>(src, dst, n, shift, hist, ntiles);
+      rs_scatter_fused<<<ntiles, RS_THREADS, smem, st>>>(src, dst, n, shift, hist, ntiles, dmask);
     } else {
       exclusive_scan_u32(hist, hist, (size_t)RS_BINS * ntiles, scan_tmp, st, launches);
-      rs_scatter<<<ntiles, RS_THREADS, smem, st>>>(src, dst, n, shift, hist, ntiles);
+      rs_scatter<<<ntiles, RS_THREADS, smem, st>>>(src, dst, n, shift, hist, ntiles, dmask);
     }
     if (launches) *launches += 2;
     uint64_t* t = src; src = dst; dst = t;

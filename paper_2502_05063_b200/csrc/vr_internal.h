@@ -34,6 +34,8 @@ struct DimParams {
   uint32_t maxr;       // largest rank <= t
   int cbits;           // bits of cidx of d-simplices
   int steps;           // phase-1 cofacet steps
+  int grab;            // prefix rows per atomic grab in k_enumerate
+  int variant;         // phase-1 scan loop variant (0: vote per vertex, 1: per 4 vertices)
   uint64_t row_begin, row_end;  // prefix rows [row_begin, row_end) of the d-simplices
 };
 struct DimCounters {   // device counters (unsigned long long each)
