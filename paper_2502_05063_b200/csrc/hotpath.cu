@@ -248,16 +248,21 @@ __global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p,
   const int GRAB = p.grab;
   const int lane = threadIdx.x & 31;
   unsigned long long surv_acc = 0, app_acc = 0, scan_acc = 0, clr_acc = 0;
+  // Rows are handed out from the LAST row down: the work of a row grows with its
+  // smallest prefix vertex u_1 (row length), which grows with the row index, so the
+  // small rows form the tail of the schedule.
+  const uint64_t nrows = p.row_end - p.row_begin;
   while (true) {
-    unsigned long long r0 = 0;
-    if (lane == 0) r0 = atomicAdd(&B.ctr->row_next, (unsigned long long)GRAB);
-    r0 = __shfl_sync(0xffffffffu, r0, 0) + p.row_begin;
-    if (r0 >= p.row_end) break;
-    const uint64_t rend = (r0 + GRAB < p.row_end) ? r0 + GRAB : p.row_end;
-    // decode prefix row r0 (colex rank of {u_D > ... > u_1}: r = sum_i C(u_i, i))
+    unsigned long long g0 = 0;
+    if (lane == 0) g0 = atomicAdd(&B.ctr->row_next, (unsigned long long)GRAB);
+    g0 = __shfl_sync(0xffffffffu, g0, 0);
+    if (g0 >= nrows) break;
+    const uint64_t rtop = p.row_end - 1 - g0;  // process rows rtop, rtop-1, ..., rlow
+    const uint64_t cnt = (g0 + GRAB <= nrows) ? (uint64_t)GRAB : nrows - g0;
+    // decode prefix row rtop (colex rank of {u_D > ... > u_1}: r = sum_i C(u_i, i))
     int u[D + 2];
     {
-      uint64_t x = r0;
+      uint64_t x = rtop;
       int hi = T.n;
 #pragma unroll
       for (int i = D; i >= 1; --i) {
@@ -269,16 +274,17 @@ __global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p,
       u[0] = 0;
       u[D + 1] = T.n;
     }
-    for (uint64_t r = r0; r < rend; ++r) {
-      if (r > r0) {  // colex successor of the prefix
-        bool carry = true;
+    for (uint64_t k = 0; k < cnt; ++k) {
+      if (k > 0) {  // colex predecessor of the prefix
+        bool done = false;
+        int top = 0;
 #pragma unroll
         for (int i = 1; i <= D; ++i) {
-          if (carry) {
-            if (i == D || u[i] + 1 < u[i + 1]) { u[i] += 1; carry = false; }
-            else u[i] = i - 1;
-          }
+          if (!done && u[i] > i - 1) { u[i] -= 1; top = i; done = true; }
         }
+#pragma unroll
+        for (int j = D; j >= 1; --j)
+          if (j < top) u[j] = u[top] - (top - j);
       }
       process_row<D>(T, p, B, u, surv_acc, app_acc, scan_acc, clr_acc);
     }

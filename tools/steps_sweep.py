@@ -7,9 +7,9 @@ import paper_2502_05063_b200 as vr
 from datagen import clouds as G
 
 names = [a for a in sys.argv[1:] if not a.startswith("--")]
-steps_list = [16, 32]
-grabs = [1, 4, 16]
-variants = [0, 1]
+steps_list = [32]
+grabs = [1, 2, 4, 8]
+variants = [1, 2]
 for name in names:
     cfg = G.CONFIGS[name]
     lt = torch.from_numpy(cfg.lower_tri()).cuda()
