@@ -74,7 +74,8 @@ typedef struct {
                             the apparent test before a column moves to the warp-cooperative
                             phase; 0 = library default */
   int32_t device;        /* CUDA device ordinal used by vr_barcodes (host-pointer entry) */
-  int32_t rows_per_grab; /* tuning: prefix rows a warp takes per atomic grab; 0 = default (4) */
+  int32_t rows_per_grab; /* tuning: prefix rows a warp takes per atomic grab; 0 = default
+                            (4 for n < 384, else 1) */
   int32_t scan_variant;  /* tuning: phase-1 scan loop, 0 = default (one warp vote per 4 cofacet
                             vertices), 1: one vote per vertex, 2: per 4 vertices; same results */
   int32_t reserved[5];

@@ -331,7 +331,7 @@ void run_full(vr_plan& P, vr_result* R) {
     p.maxr = P.maxr;
     p.cbits = cbits;
     p.steps = steps;
-    p.grab = P.opt.rows_per_grab > 0 ? P.opt.rows_per_grab : 4;
+    p.grab = P.opt.rows_per_grab > 0 ? P.opt.rows_per_grab : (n < 384 ? 4 : 1);
     p.variant = P.opt.scan_variant > 0 ? P.opt.scan_variant - 1 : 1;
     const uint64_t rows = binom_host((uint64_t)n, (uint64_t)d);
     dr.sort_bits = rbits + cbits;
