@@ -78,7 +78,10 @@ typedef struct {
                             (4 for n < 384, else 1) */
   int32_t scan_variant;  /* tuning: phase-1 scan loop, 0 = default (one warp vote per 4 cofacet
                             vertices), 1: one vote per vertex, 2: per 4 vertices; same results */
-  int32_t reserved[5];
+  int32_t sparse_mode;   /* -1/0 = auto (output-sensitive when <= 25% of the edges are under the
+                            threshold, or when the dense index space is too large),
+                            1 = always dense, 2 = always output-sensitive; same results */
+  int32_t reserved[4];
 } vr_options;
 
 /* Per-dimension statistics (Table 5.1 / 5.5 counters, stage times). */

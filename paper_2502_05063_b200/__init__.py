@@ -46,7 +46,7 @@ class _IndexPair(ctypes.Structure):
 class _Options(ctypes.Structure):
     _fields_ = [("include_zero", ctypes.c_int32), ("index_pairs", ctypes.c_int32), ("residual_mode", ctypes.c_int32),
                 ("apparent_steps", ctypes.c_int32), ("device", ctypes.c_int32), ("rows_per_grab", ctypes.c_int32),
-                ("scan_variant", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+                ("scan_variant", ctypes.c_int32), ("sparse_mode", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
 
 
 _STAT_FIELDS = ["candidates", "survivors", "apparent", "cleared", "residual_columns", "emergent", "pairs_all",
@@ -105,11 +105,11 @@ def _check(rc: int):
 
 
 def _options(include_zero=False, index_pairs=False, residual_mode=0, apparent_steps=0, device=0, rows_per_grab=0,
-             scan_variant=0) -> _Options:
+             scan_variant=0, sparse_mode=0) -> _Options:
     o = _Options()
     o.include_zero, o.index_pairs, o.residual_mode = int(include_zero), int(index_pairs), int(residual_mode)
     o.apparent_steps, o.device = int(apparent_steps), int(device)
-    o.rows_per_grab, o.scan_variant = int(rows_per_grab), int(scan_variant)
+    o.rows_per_grab, o.scan_variant, o.sparse_mode = int(rows_per_grab), int(scan_variant), int(sparse_mode)
     return o
 
 

@@ -44,27 +44,6 @@ namespace vr {
 
 constexpr int HP_THREADS = 256;
 
-__device__ __forceinline__ uint32_t umax(uint32_t a, uint32_t b) { return a > b ? a : b; }
-
-__device__ __forceinline__ bool bit_test(const uint32_t* __restrict__ bm, uint64_t i) {
-  return (__ldg(bm + (i >> 5)) >> (i & 31)) & 1u;
-}
-__device__ __forceinline__ void bit_set(uint32_t* bm, uint64_t i) { atomicOr(bm + (i >> 5), 1u << (i & 31)); }
-
-template <int D>
-__device__ __forceinline__ uint4 pack_vertices(const int (&s)[D + 1]) {
-  uint32_t w[4] = {0, 0, 0, 0};
-#pragma unroll
-  for (int i = 0; i <= D; ++i) w[i >> 1] |= (uint32_t)s[i] << ((i & 1) * 16);
-  return make_uint4(w[0], w[1], w[2], w[3]);
-}
-template <int D>
-__device__ __forceinline__ void unpack_vertices(uint4 p, int (&s)[D + 1]) {
-  const uint32_t w[4] = {p.x, p.y, p.z, p.w};
-#pragma unroll
-  for (int i = 0; i <= D; ++i) s[i] = (int)((w[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu);
-}
-
 // ------------------------------------------------------------------ phase 1: enumerate
 template <int D>
 __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p, const HotBuffers& B, const int (&u)[D + 2],

@@ -120,6 +120,12 @@ struct vr_plan {
   uint32_t maxr = 0;
   uint64_t m = 0;
   std::vector<DimRun> dims;  // index d (1..D), dims[0] unused
+  // output-sensitive mode: threshold-graph CSR and per-dimension survivor lists
+  bool sparse = false;
+  DevBuf adj_off, adj, deg, deg_below, scan_tmp2, bound;
+  std::vector<DevBuf> rows;           // rows[d] = packed d-simplex survivors (rows of d+1)
+  std::vector<uint64_t> rows_count;   // survivors written per dimension
+  std::vector<uint64_t> rows_cap;
   int64_t survivors_total = 0;
   int64_t apparent_total = 0, residual_total = 0;
   int64_t launches = 0;
@@ -281,6 +287,33 @@ void run_full(vr_plan& P, vr_result* R) {
     s0.ms_transfer = ms_tx0;
   }
 
+  // ---------------- output-sensitive mode?  (dense enumeration of
+  // C(n, d+1) indices is wasted work when few edges are under the threshold)
+  {
+    const int mode = P.opt.sparse_mode;
+    const uint64_t dense_rows = D >= 1 ? binom_host((uint64_t)n, (uint64_t)D) : 0;
+    bool sp = (P.m * 4 <= P.N) || dense_rows > ((uint64_t)1 << 32);
+    if (mode == 1) sp = false;
+    if (mode == 2) sp = true;
+    P.sparse = sp && D >= 1 && P.m > 0;
+    if (P.sparse) {
+      P.deg.ensure(((size_t)n + 1) * 4);
+      P.deg_below.ensure(((size_t)n + 1) * 4);
+      P.adj_off.ensure(((size_t)n + 1) * 4);
+      P.adj.ensure(std::max<size_t>(2 * (size_t)P.m, 1) * 2);
+      P.scan_tmp2.ensure(vr::scan_temp_bytes((size_t)n + 1));
+      P.bound.ensure(8);
+      CUDA_TRY(cudaMemsetAsync(P.deg.p, 0, ((size_t)n + 1) * 4, st));
+      vr::launch_adjacency(P.rank.as<uint32_t>(), (int)n, P.deg.as<uint32_t>(), P.deg_below.as<uint32_t>(),
+                           P.adj_off.as<uint32_t>(), P.adj.as<uint16_t>(), P.scan_tmp2.p, st, &P.launches);
+      CUDA_TRY(cudaGetLastError());
+      P.rows.clear();
+      P.rows.resize((size_t)D + 2);
+      P.rows_count.assign((size_t)D + 2, 0);
+      P.rows_cap.assign((size_t)D + 2, 0);
+    }
+  }
+
   // ---------------- dimensions 1..D
   P.dims.clear();
   P.dims.resize((size_t)D + 2);
@@ -339,21 +372,46 @@ void run_full(vr_plan& P, vr_result* R) {
     uint32_t* clr_next = clr_of(d + 1);
     if (clr_next) CUDA_TRY(cudaMemsetAsync(clr_next, 0, P.dims[(size_t)d + 1].clr_words * 4, st));
 
+    // sparse mode: the rows are the survivors of dimension d-1 (vertices for d = 1) and
+    // sum over rows of deg_below(u_1) bounds the d-simplices they can produce
+    uint64_t bound = cand;
+    uint64_t nrows_sp = 0;
+    if (P.sparse) {
+      if (d == 1) {
+        nrows_sp = (uint64_t)n;
+        bound = P.m;
+      } else {
+        nrows_sp = P.rows_count[(size_t)d - 1];
+        CUDA_TRY(cudaMemsetAsync(P.bound.p, 0, 8, st));
+        vr::launch_row_bound(P.rows[(size_t)d - 1].as<uint4>(), nrows_sp, d - 1, P.deg_below.as<uint32_t>(),
+                             P.bound.as<unsigned long long>(), st, &P.launches);
+        unsigned long long b = 0;
+        CUDA_TRY(cudaMemcpyAsync(&b, P.bound.p, 8, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        bound = std::min<uint64_t>(cand, b);
+      }
+      if (d < D) {
+        P.rows[(size_t)d].ensure(std::max<uint64_t>(bound, 1) * 16);
+        P.rows_cap[(size_t)d] = std::max<uint64_t>(bound, 1);
+      }
+    }
     // queue / residual capacity: every candidate, bounded by a share of free device memory
     CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
     const uint64_t qmax = std::max<uint64_t>((uint64_t)(free_b / 4 / 40), 1024);
-    const uint64_t qwant = std::min<uint64_t>(cand, qmax);
+    const uint64_t qwant = std::min<uint64_t>(std::max<uint64_t>(bound, 1), qmax);
+    if (P.sparse && bound > qmax) throw VrError(VR_ECAPACITY, "output-sensitive mode: column bound exceeds device memory");
     if (P.qcap < qwant) {
       P.queue.ensure((size_t)qwant * 8);
       P.qvert.ensure((size_t)qwant * 16);
       P.qcap = qwant;
     }
-    uint64_t rows_per_chunk = rows;
-    if (cand > P.qcap) rows_per_chunk = std::max<uint64_t>(1, P.qcap / (uint64_t)n);
+    uint64_t rows_per_chunk = P.sparse ? nrows_sp : rows;
+    const uint64_t rows_total = P.sparse ? nrows_sp : rows;
+    if (!P.sparse && cand > P.qcap) rows_per_chunk = std::max<uint64_t>(1, P.qcap / (uint64_t)n);
     uint64_t app_cap = 0;
     uint64_t* app_ptr = nullptr;
     if (P.opt.index_pairs) {
-      app_cap = cand;
+      app_cap = std::max<uint64_t>(bound, 1);
       P.app_pairs.ensure((size_t)app_cap * 16);
       app_ptr = P.app_pairs.as<uint64_t>();
     }
@@ -362,9 +420,9 @@ void run_full(vr_plan& P, vr_result* R) {
     dr.chunks.clear();
     float t_enum = 0, t_res = 0;
     uint64_t resid_count = 0;
-    for (uint64_t rb = 0; rb < rows; rb += rows_per_chunk) {
-      const uint64_t re = std::min(rows, rb + rows_per_chunk);
-      const uint64_t chunk_cand = std::min<uint64_t>(cand, (re - rb) * (uint64_t)n);
+    for (uint64_t rb = 0; rb < rows_total; rb += rows_per_chunk) {
+      const uint64_t re = std::min(rows_total, rb + rows_per_chunk);
+      const uint64_t chunk_cand = P.sparse ? std::max<uint64_t>(bound, 1) : std::min<uint64_t>(cand, (re - rb) * (uint64_t)n);
       // residual capacity: what is there plus everything this chunk could add
       if (P.rcap < resid_count + chunk_cand || !P.resid.p) {
         const uint64_t ncap = std::max<uint64_t>(resid_count + chunk_cand, 1024);
@@ -378,12 +436,22 @@ void run_full(vr_plan& P, vr_result* R) {
       }
       vr::HotBuffers B{P.queue.as<uint64_t>(), P.qvert.as<uint4>(), P.qcap, P.resid.as<uint64_t>(), P.rcap,
                        clr_of(d), clr_next, dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, ctr, app_ptr, app_cap};
+      vr::SparseRows SR{};
+      if (P.sparse) {
+        SR.adj_off = P.adj_off.as<uint32_t>();
+        SR.adj = P.adj.as<uint16_t>();
+        SR.rows_in = d == 1 ? nullptr : P.rows[(size_t)d - 1].as<uint4>();
+        SR.rows_out = d < D ? P.rows[(size_t)d].as<uint4>() : nullptr;
+        SR.rows_out_cap = d < D ? P.rows_cap[(size_t)d] : 0;
+        SR.rows_out_count = &ctr->rows_out;
+      }
       p.row_begin = rb;
       p.row_end = re;
       CUDA_TRY(cudaMemsetAsync(&ctr->row_next, 0, 8, st));
       CUDA_TRY(cudaMemsetAsync(&ctr->queued, 0, 8, st));
       CUDA_TRY(cudaEventRecord(ev[2], st));
-      vr::launch_enumerate(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, st, &P.launches);
+      if (P.sparse) vr::launch_enumerate_sparse(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, SR, st, &P.launches);
+      else vr::launch_enumerate(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, st, &P.launches);
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaEventRecord(ev[3], st));
       unsigned long long q = 0;
@@ -394,7 +462,8 @@ void run_full(vr_plan& P, vr_result* R) {
       cudaEventElapsedTime(&x, ev[2], ev[3]);
       t_enum += x;
       CUDA_TRY(cudaEventRecord(ev[4], st));
-      vr::launch_resolve(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, q, st, &P.launches);
+      if (P.sparse) vr::launch_resolve_sparse(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, SR, q, st, &P.launches);
+      else vr::launch_resolve(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, q, st, &P.launches);
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaEventRecord(ev[5], st));
       unsigned long long rc = 0;
@@ -405,6 +474,13 @@ void run_full(vr_plan& P, vr_result* R) {
       if (rc > P.rcap) throw VrError(VR_ECAPACITY, "residual list overflow");
       resid_count = rc;
       dr.chunks.push_back(Chunk{rb, re, q});
+    }
+    if (P.sparse && d < D) {
+      unsigned long long ro = 0;
+      CUDA_TRY(cudaMemcpyAsync(&ro, &ctr->rows_out, 8, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      if (ro > P.rows_cap[(size_t)d]) throw VrError(VR_ECAPACITY, "survivor list overflow");
+      P.rows_count[(size_t)d] = ro;
     }
     dr.residual = resid_count;
     // a4: sort the residual columns into coboundary order
@@ -523,6 +599,11 @@ void replay(vr_plan& P) {
     cudaEventRecord(e.first, st);
     vr::launch_tables(P.d_lt, P.n, P.threshold, P.keys.as<uint64_t>(), P.alt.as<uint64_t>(), P.rowmax.as<uint32_t>(),
                       P.sort_tmp.p, P.rank.as<uint32_t>(), P.tout.as<vr::TablesOut>(), &sorted, st, &P.launches);
+    if (P.sparse) {
+      cudaMemsetAsync(P.deg.p, 0, ((size_t)P.n + 1) * 4, st);
+      vr::launch_adjacency(P.rank.as<uint32_t>(), (int)P.n, P.deg.as<uint32_t>(), P.deg_below.as<uint32_t>(),
+                           P.adj_off.as<uint32_t>(), P.adj.as<uint16_t>(), P.scan_tmp2.p, st, &P.launches);
+    }
     if (P.D >= 1 && clr_of(1)) {
       cudaMemsetAsync(clr_of(1), 0, P.dims[1].clr_words * 4, st);
       vr::launch_set_bits(P.dims[1].deaths_in.as<uint64_t>(), P.dims[1].ndeaths_in, clr_of(1), st, &P.launches);
@@ -543,17 +624,28 @@ void replay(vr_plan& P) {
     for (const Chunk& c : dr.chunks) {
       vr::HotBuffers B{P.queue.as<uint64_t>(), P.qvert.as<uint4>(), P.qcap, P.resid.as<uint64_t>(), P.rcap,
                        clr_of(d), clr_next, dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, ctr, nullptr, 0};
+      vr::SparseRows SR{};
+      if (P.sparse) {
+        SR.adj_off = P.adj_off.as<uint32_t>();
+        SR.adj = P.adj.as<uint16_t>();
+        SR.rows_in = d == 1 ? nullptr : P.rows[(size_t)d - 1].as<uint4>();
+        SR.rows_out = d < P.D ? P.rows[(size_t)d].as<uint4>() : nullptr;
+        SR.rows_out_cap = d < P.D ? P.rows_cap[(size_t)d] : 0;
+        SR.rows_out_count = &ctr->rows_out;
+      }
       p.row_begin = c.row_begin;
       p.row_end = c.row_end;
       auto& e2 = ev(1);
       cudaEventRecord(e2.first, st);
       cudaMemsetAsync(&ctr->row_next, 0, 8, st);
       cudaMemsetAsync(&ctr->queued, 0, 8, st);
-      vr::launch_enumerate(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, st, &P.launches);
+      if (P.sparse) vr::launch_enumerate_sparse(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, SR, st, &P.launches);
+      else vr::launch_enumerate(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, st, &P.launches);
       cudaEventRecord(e2.second, st);
       auto& e3 = ev(2);
       cudaEventRecord(e3.first, st);
-      vr::launch_resolve(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, c.queued, st, &P.launches);
+      if (P.sparse) vr::launch_resolve_sparse(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, SR, c.queued, st, &P.launches);
+      else vr::launch_resolve(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, c.queued, st, &P.launches);
       cudaEventRecord(e3.second, st);
     }
     auto& e4 = ev(3);

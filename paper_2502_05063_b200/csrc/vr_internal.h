@@ -39,7 +39,7 @@ struct DimParams {
   uint64_t row_begin, row_end;  // prefix rows [row_begin, row_end) of the d-simplices
 };
 struct DimCounters {   // device counters (unsigned long long each)
-  unsigned long long survivors, apparent1, apparent2, cleared, queued, residual, row_next, app_pairs, scanned, scanned2;
+  unsigned long long survivors, apparent1, apparent2, cleared, queued, residual, row_next, app_pairs, scanned, scanned2, rows_out;
 };
 struct HotBuffers {
   uint64_t* qkey;        // phase-2 queue: column keys
@@ -60,6 +60,24 @@ void launch_enumerate(const DimParams& p, const uint32_t* rank, const uint64_t* 
 void launch_resolve(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
                     uint64_t qn, cudaStream_t st, int64_t* launches);
 void launch_set_bits(const uint64_t* list, int64_t m, uint32_t* bm, cudaStream_t st, int64_t* launches);
+
+// ---------------------------------------------------------------- sparse.cu (output-sensitive mode)
+struct SparseRows {
+  const uint32_t* adj_off;        // CSR offsets of the threshold graph, n+1
+  const uint16_t* adj;            // neighbours, each list descending
+  const uint4* rows_in;           // packed (d-1)-simplex survivors = prefix rows; nullptr for d = 1
+  uint4* rows_out;                // survivors of dimension d (rows of d+1), or nullptr
+  uint64_t rows_out_cap;
+  unsigned long long* rows_out_count;
+};
+void launch_adjacency(const uint32_t* rank, int n, uint32_t* deg, uint32_t* deg_below, uint32_t* off, uint16_t* adj,
+                      void* scan_tmp, cudaStream_t st, int64_t* launches);
+void launch_row_bound(const uint4* rows, uint64_t nrows, int dprev, const uint32_t* deg_below, unsigned long long* out,
+                      cudaStream_t st, int64_t* launches);
+void launch_enumerate_sparse(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
+                             const SparseRows& S, cudaStream_t st, int64_t* launches);
+void launch_resolve_sparse(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
+                           const SparseRows& S, uint64_t qn, cudaStream_t st, int64_t* launches);
 
 // ---------------------------------------------------------------- host.cpp (off-path)
 struct HostPairs {

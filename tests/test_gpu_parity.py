@@ -234,3 +234,55 @@ def test_radix_sort_matches_numpy(n, bits):
     sub = keys & mask
     order = np.argsort(sub, kind="stable")  # LSD radix sort is stable on the sorted bits
     assert np.array_equal(got, keys[order])
+
+
+# ------------------------------------------------------------------ output-sensitive (sparse) mode
+@pytest.mark.parametrize("seed,n,D,kind,thr", CASES[::2])
+def test_sparse_mode_index_level(seed, n, D, kind, thr):
+    if kind == "tied":
+        lt = G.random_tied(n, seed, levels=3)
+    elif kind == "tied2":
+        lt = G.random_tied(n, seed, levels=8)
+    else:
+        lt = G.random_cloud(n, seed)
+    t = math.inf if thr == "inf" else (O.enclosing_radius(lt, n) if thr == "R" else float(np.quantile(lt, 0.6)))
+    full_check(lt, n, D, t, sparse_mode=2)
+
+
+@pytest.mark.parametrize("name,m,D", [("c5_o3_4096", 36, 2), ("c5_o3_4096", 22, 3), ("c3_trefoil1000", 40, 2),
+                                      ("c2_s3_192", 24, 3)])
+@pytest.mark.parametrize("steps", [2, 32])
+def test_sparse_mode_config_subsample(name, m, D, steps):
+    cfg = G.CONFIGS[name]
+    thr = 1.0 if name == "c5_o3_4096" else cfg.threshold  # a sparse threshold graph
+    full_check(cfg.lower_tri(m), m, D, thr, sparse_mode=2, apparent_steps=steps)
+
+
+@pytest.fixture(scope="module")
+def c5_lower_tri():
+    return G.CONFIGS["c5_o3_4096"].lower_tri()
+
+
+def test_config5_dense_equals_sparse_dim2(c5_lower_tri):
+    cfg = G.CONFIGS["c5_o3_4096"]
+    a = vr.barcodes(c5_lower_tri, cfg.n, 2, cfg.threshold, sparse_mode=1)
+    b = vr.barcodes(c5_lower_tri, cfg.n, 2, cfg.threshold, sparse_mode=2)
+    for d in range(3):
+        assert np.array_equal(a.pairs[d], b.pairs[d])
+        for k in ("survivors", "apparent", "cleared", "residual_columns", "pairs_all", "essential"):
+            assert a.stats[d][k] == b.stats[d][k], (d, k)
+
+
+def test_config5_dim3_invariants(c5_lower_tri):
+    cfg = G.CONFIGS["c5_o3_4096"]
+    got = vr.barcodes(c5_lower_tri, cfg.n, 3, cfg.threshold)
+    D = 3
+    assert got.stats[1]["survivors"] == int((c5_lower_tri <= np.float32(cfg.threshold)).sum())
+    P = [got.stats[p]["pairs_all"] for p in range(D + 1)]
+    E = [got.stats[p]["essential"] for p in range(D + 1)]
+    for p in range(1, D + 1):
+        s = got.stats[p]
+        assert s["survivors"] == P[p] + E[p] + P[p - 1]
+        assert s["survivors"] == s["apparent"] + s["cleared"] + s["residual_columns"]
+    # two O(3) components exactly 2.0 apart (> t = 1.4): beta_0 = 2 essential classes
+    assert E[0] == 2
