@@ -111,10 +111,39 @@ struct Ctx {
   }
   // coboundary of the d-simplex s in lex-decreasing order (Alg 14, reading A2), with ranks.
   // The rank matrix is symmetric, so R[v][s_q] is read as the contiguous row R[s_q][.].
+  // With a threshold-graph adjacency only the neighbours of the vertex of s with the
+  // fewest neighbours are visited (a cofacet under the threshold needs v adjacent to all
+  // of s), in the same descending order; the cofacet index is then computed in closed
+  // form: with j vertices of s above v, cidx(s ∪ {v}) = A_j + C(v, d+2-j) + B_j.
   template <class F>
   void cofacets(const int* s, uint64_t cidx, uint32_t rs, F&& emit) const {
     const uint32_t* rows[16];
     for (int q = 0; q <= d; ++q) rows[q] = &M.rank[(size_t)s[q] * (size_t)M.n];
+    if (!M.adj_off.empty()) {
+      uint64_t A[17], B[17];
+      A[0] = 0;
+      for (int j = 0; j <= d; ++j) A[j + 1] = A[j] + M.C(s[j], d + 2 - j);
+      B[d + 1] = 0;
+      for (int j = d; j >= 0; --j) B[j] = B[j + 1] + M.C(s[j], d + 1 - j);
+      int anchor = s[0];
+      uint32_t best = ~0u;
+      for (int q = 0; q <= d; ++q) {
+        const uint32_t dg = M.adj_off[(size_t)s[q] + 1] - M.adj_off[(size_t)s[q]];
+        if (dg < best) { best = dg; anchor = s[q]; }
+      }
+      const uint16_t* L = M.adj.data() + M.adj_off[(size_t)anchor];
+      int j = 0;  // vertices of s above v
+      for (uint32_t k = 0; k < best; ++k) {
+        const int v = L[k];
+        while (j <= d && s[j] > v) ++j;
+        if (j <= d && s[j] == v) continue;
+        uint32_t r = rs;
+        for (int q = 0; q <= d; ++q) r = std::max(r, rows[q][v]);
+        if (r == VR_RINF_H) continue;
+        if (!emit(Entry{r, A[j] + M.C(v, d + 2 - j) + B[j]})) return;
+      }
+      return;
+    }
     uint64_t below = cidx, above = 0;
     int k = d + 1, j = 0;
     for (int64_t v = M.n - 1; v >= 0; --v) {
@@ -134,6 +163,22 @@ struct Ctx {
   int64_t first_equal_cofacet_vertex(const int* S, int K, uint32_t r) const {
     const uint32_t* rows[16];
     for (int q = 0; q < K; ++q) rows[q] = &M.rank[(size_t)S[q] * (size_t)M.n];
+    if (!M.adj_off.empty()) {
+      int anchor = S[0];
+      uint32_t best = ~0u;
+      for (int q = 0; q < K; ++q) {
+        const uint32_t dg = M.adj_off[(size_t)S[q] + 1] - M.adj_off[(size_t)S[q]];
+        if (dg < best) { best = dg; anchor = S[q]; }
+      }
+      const uint16_t* L = M.adj.data() + M.adj_off[(size_t)anchor];
+      for (uint32_t k = 0; k < best; ++k) {
+        const int v = L[k];
+        bool ok = true;
+        for (int q = 0; q < K && ok; ++q) ok = (v != S[q]) && rows[q][v] <= r;
+        if (ok) return v;
+      }
+      return -1;
+    }
     for (int64_t v = M.n - 1; v >= 0; --v) {
       bool ok = true;
       for (int q = 0; q < K && ok; ++q) ok = (v != S[q]) && rows[q][v] <= r;

@@ -314,6 +314,16 @@ void run_full(vr_plan& P, vr_result* R) {
     }
   }
 
+  if (P.sparse) {  // the host residual walks the same threshold-graph adjacency
+    auto ta = std::chrono::steady_clock::now();
+    M.adj_off.resize((size_t)n + 1);
+    CUDA_TRY(cudaMemcpyAsync(M.adj_off.data(), P.adj_off.p, ((size_t)n + 1) * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    M.adj.resize((size_t)M.adj_off[(size_t)n]);
+    if (!M.adj.empty()) CUDA_TRY(cudaMemcpy(M.adj.data(), P.adj.p, M.adj.size() * 2, cudaMemcpyDeviceToHost));
+    if (R) R->stats[0].ms_transfer += ms_since(ta);
+  }
+
   // ---------------- dimensions 1..D
   P.dims.clear();
   P.dims.resize((size_t)D + 2);

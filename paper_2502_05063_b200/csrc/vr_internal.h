@@ -93,6 +93,9 @@ struct HostMatrix {
   std::vector<uint32_t> rank;   // n*n
   std::vector<uint64_t> binom;  // (kmax+1)*(n+1)
   int kmax = 0;
+  // optional threshold-graph adjacency (output-sensitive mode): neighbours descending
+  std::vector<uint32_t> adj_off;  // n+1, empty = dense scans over all vertices
+  std::vector<uint16_t> adj;
   uint64_t C(int64_t v, int k) const { return binom[(size_t)k * (size_t)(n + 1) + (size_t)v]; }
   uint32_t R(int64_t i, int64_t j) const { return rank[(size_t)i * (size_t)n + (size_t)j]; }
 };
