@@ -16,7 +16,7 @@ HEADERS = ["vr_common.cuh", "vr_internal.h"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC,-O3",
+    "-Xcompiler", "-fPIC,-O3,-pthread",
     "-shared",
     "--expt-relaxed-constexpr",
 ]

@@ -22,6 +22,8 @@
 //                     only zeros to the left of f (Def 5.3.4), so no column left of f can
 //                     ever have its pivot there.
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <functional>
 #include <chrono>
 #include <cstdio>
@@ -462,6 +464,195 @@ void residual_reduce_t(const HostMatrix& M, int d, uint32_t maxr, int cbits, con
   std::sort(deaths_sorted.begin(), deaths_sorted.end());
 }
 
+// ------------------------------------------------------------------ parallel (speculative)
+// Reduction-matrix mode on T threads with IN-ORDER COMMIT.  Threads take columns in
+// coboundary order and reduce them concurrently against the pivots committed so far
+// (every addition of an earlier column with the same pivot is a step the standard
+// algorithm, Alg 11, could take).  A column may only claim its final pivot when every
+// earlier column has committed: it waits for its turn, re-checks the pivot against the
+// now complete table of earlier pivots, keeps reducing if needed, then commits.  The
+// committed pivots are therefore exactly the sequential algorithm's.
+struct ConcPivotMap {  // insert-only, one writer at a time (the committing column)
+  std::vector<std::atomic<uint64_t>> k;
+  std::vector<int64_t> v;
+  size_t mask;
+  explicit ConcPivotMap(size_t cap) {
+    size_t c = 16;
+    while (c < cap * 2) c <<= 1;
+    k = std::vector<std::atomic<uint64_t>>(c);
+    for (auto& x : k) x.store(~0ull, std::memory_order_relaxed);
+    v.assign(c, -1);
+    mask = c - 1;
+  }
+  bool get(uint64_t key, int64_t& out) const {
+    for (size_t i = U64Map::h(key) & mask;; i = (i + 1) & mask) {
+      const uint64_t x = k[i].load(std::memory_order_acquire);
+      if (x == key) { out = v[i]; return true; }
+      if (x == ~0ull) return false;
+    }
+  }
+  void put(uint64_t key, int64_t val) {
+    for (size_t i = U64Map::h(key) & mask;; i = (i + 1) & mask) {
+      if (k[i].load(std::memory_order_relaxed) == ~0ull) {
+        v[i] = val;
+        k[i].store(key, std::memory_order_release);
+        return;
+      }
+    }
+  }
+};
+
+template <class K>
+void residual_reduce_par(const HostMatrix& M, int d, uint32_t maxr, int cbits, const uint64_t* keys, uint64_t nkeys, int cb,
+                         int nthreads, HostPairs& out, std::vector<uint64_t>& deaths_sorted, ResidualStats& stats) {
+  const uint64_t cmask = cbits >= 64 ? ~0ull : ((1ull << cbits) - 1);
+  struct ColOut {
+    uint32_t death_r = 0;
+    uint64_t death_cidx = UINT64_MAX;  // UINT64_MAX: essential
+    bool emergent = false;
+    int64_t adds = 0, cobs = 0;
+  };
+  std::vector<ColOut> res((size_t)nkeys);
+  std::vector<std::vector<uint64_t>> vcols((size_t)nkeys);
+  ConcPivotMap pivots((size_t)nkeys + 16);
+  std::atomic<uint64_t> next_commit{0}, next_col{0};
+
+  auto worker = [&]() {
+    Ctx cx(M, d);
+    U64Map app_memo(1024);
+    RadixHeap<K> W(maxr, cb);
+    std::vector<uint64_t> work_v;
+    int s[16], f[16];
+    auto apparent_of = [&](const Entry& e) -> int64_t {
+      int64_t a;
+      if (app_memo.get(e.cidx, a)) return a;
+      a = cx.apparent_partner(e.cidx, e.r);
+      app_memo.put(e.cidx, a);
+      return a;
+    };
+    auto wait_turn = [&](uint64_t j) {
+      int spins = 0;
+      while (next_commit.load(std::memory_order_acquire) != j) {
+        if (++spins > 64) std::this_thread::yield();
+      }
+    };
+    for (;;) {
+      const uint64_t j = next_col.fetch_add(1, std::memory_order_relaxed);
+      if (j >= nkeys) break;
+      ColOut& R = res[(size_t)j];
+      const uint64_t key = keys[j];
+      const uint32_t rs = maxr - (uint32_t)(key >> cbits);
+      const uint64_t sc = key & cmask;
+      cx.decode(sc, d + 1, s);
+      W.clear();
+      work_v.clear();
+      work_v.push_back(key);
+      auto push_coboundary = [&](uint64_t cidx, uint32_t r) {
+        ++R.cobs;
+        cx.decode(cidx, d + 1, f);
+        cx.cofacets(f, cidx, r, [&](const Entry& e) { W.push(e.r, e.cidx); return true; });
+      };
+      // initial coboundary with the emergent check (§5.2.11), speculative
+      bool check = true, emergent = false;
+      Entry first{0, 0};
+      cx.cofacets(s, sc, rs, [&](const Entry& e) {
+        if (check && e.r == rs) {
+          int64_t col;
+          if (!pivots.get(e.cidx, col) && apparent_of(e) < 0) { first = e; emergent = true; return false; }
+          check = false;
+        }
+        W.push(e.r, e.cidx);
+        return true;
+      });
+      if (emergent) {
+        wait_turn(j);
+        int64_t col;
+        if (!pivots.get(first.cidx, col)) {
+          R.emergent = true;
+          R.death_r = first.r;
+          R.death_cidx = first.cidx;
+          vcols[(size_t)j].assign(1, key);
+          pivots.put(first.cidx, (int64_t)j);
+          next_commit.store(j + 1, std::memory_order_release);
+          continue;
+        }
+        // an earlier column took that row meanwhile: reduce normally (we hold the turn)
+        W.clear();
+        cx.cofacets(s, sc, rs, [&](const Entry& e) { W.push(e.r, e.cidx); return true; });
+      }
+      Entry pe{0, 0};
+      bool have = W.pivot(pe.r, pe.cidx);
+      bool my_turn = emergent;
+      for (;;) {
+        while (have) {
+          int64_t col;
+          if (pivots.get(pe.cidx, col)) {
+            for (const uint64_t vk : vcols[(size_t)col]) {
+              push_coboundary(vk & cmask, maxr - (uint32_t)(vk >> cbits));
+              work_v.push_back(vk);
+            }
+          } else {
+            const int64_t a = apparent_of(pe);
+            if (a < 0) break;
+            int fv[16];
+            cx.decode((uint64_t)a, d + 1, fv);
+            const uint32_t fr = cx.diam_rank(fv);
+            push_coboundary((uint64_t)a, fr);
+            work_v.push_back(((uint64_t)(maxr - fr) << cbits) | (uint64_t)a);
+          }
+          ++R.adds;
+          have = W.pivot(pe.r, pe.cidx);
+        }
+        if (my_turn) break;
+        wait_turn(j);  // every earlier column has committed: the pivot table is final for us
+        my_turn = true;
+        int64_t col;
+        if (have && pivots.get(pe.cidx, col)) continue;
+        if (have && apparent_of(pe) >= 0) continue;
+        break;
+      }
+      if (have) {
+        R.death_r = pe.r;
+        R.death_cidx = pe.cidx;
+        auto& V = vcols[(size_t)j];
+        V.clear();
+        V.push_back(key);
+        if (work_v.size() > 1) {
+          std::sort(work_v.begin() + 1, work_v.end());
+          for (size_t i = 1; i < work_v.size();) {
+            size_t q = i;
+            while (q < work_v.size() && work_v[q] == work_v[i]) ++q;
+            if (((q - i) & 1) && work_v[i] != key) V.push_back(work_v[i]);
+            i = q;
+          }
+        }
+        pivots.put(pe.cidx, (int64_t)j);
+      }
+      next_commit.store(j + 1, std::memory_order_release);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nthreads; ++t) pool.emplace_back(worker);
+  for (auto& th : pool) th.join();
+
+  deaths_sorted.clear();
+  for (uint64_t j = 0; j < nkeys; ++j) {
+    const ColOut& R = res[(size_t)j];
+    const uint32_t rs = maxr - (uint32_t)(keys[j] >> cbits);
+    const uint64_t sc = keys[j] & cmask;
+    stats.additions += R.adds;
+    stats.coboundaries += R.cobs;
+    stats.emergent += R.emergent;
+    if (R.death_cidx != UINT64_MAX) {
+      out.push(M.value[rs], M.value[R.death_r], sc, R.death_cidx);
+      deaths_sorted.push_back(R.death_cidx);
+    } else {
+      out.push(M.value[rs], INFINITY, sc, UINT64_MAX);
+    }
+  }
+  std::sort(deaths_sorted.begin(), deaths_sorted.end());
+}
+
 }  // namespace
 
 void residual_reduce(const HostMatrix& M, int d, uint32_t maxr, int cbits, const uint64_t* keys, uint64_t nkeys, int mode,
@@ -473,6 +664,13 @@ void residual_reduce(const HostMatrix& M, int d, uint32_t maxr, int cbits, const
   int rb = 1;
   while (rb < 32 && (maxr >> rb) != 0) ++rb;
   using u128 = unsigned __int128;
+  int nthreads = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
+  if (const char* e = std::getenv("VR_RESIDUAL_THREADS")) nthreads = std::max(1, std::atoi(e));
+  if (mode == 0 && nthreads > 1 && nkeys >= 64) {
+    if (rb + cb <= 64) residual_reduce_par<uint64_t>(M, d, maxr, cbits, keys, nkeys, cb, nthreads, out, deaths_sorted, st);
+    else residual_reduce_par<u128>(M, d, maxr, cbits, keys, nkeys, cb, nthreads, out, deaths_sorted, st);
+    return;
+  }
   if (rb + cb <= 64) {
     if (mode == 0) {
       RadixHeap<uint64_t> W(maxr, cb);

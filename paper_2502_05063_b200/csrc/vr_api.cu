@@ -191,8 +191,20 @@ void dump_residual(const char* dir, const vr::HostMatrix& M, int d, uint32_t max
   }
 }
 
+struct SectionTimer {
+  bool on = std::getenv("VR_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[vr] %-28s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 // ------------------------------------------------------------------ the run
 void run_full(vr_plan& P, vr_result* R) {
+  SectionTimer ST;
   const int64_t n = P.n;
   const int D = P.D;
   cudaStream_t st = P.st;
@@ -205,6 +217,7 @@ void run_full(vr_plan& P, vr_result* R) {
   for (int k = 0; k <= P.kmax; ++k)
     for (int64_t v = 0; v <= n; ++v) hb[(size_t)k * (size_t)(n + 1) + (size_t)v] = binom_host((uint64_t)v, (uint64_t)k);
 
+  ST.mark("binomials");
   // ---------------- device memory for the tables
   size_t free_b = 0, total_b = 0;
   CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
@@ -227,6 +240,7 @@ void run_full(vr_plan& P, vr_result* R) {
     ~EvGuard() { for (int i = 0; i < 8; ++i) cudaEventDestroy(e[i]); }
   } evg{ev};
 
+  ST.mark("allocate tables");
   // ---------------- a0
   uint64_t* sorted = nullptr;
   CUDA_TRY(cudaEventRecord(ev[0], st));
@@ -237,6 +251,7 @@ void run_full(vr_plan& P, vr_result* R) {
   CUDA_TRY(cudaMemcpyAsync(&to, P.tout.p, sizeof to, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaEventRecord(ev[1], st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  ST.mark("tables (device)");
   if (to.err) throw VrError(VR_EINPUT, "dist_lower_tri holds a negative or NaN distance");
   float tms = 0;
   cudaEventElapsedTime(&tms, ev[0], ev[1]);
@@ -273,6 +288,7 @@ void run_full(vr_plan& P, vr_result* R) {
     CUDA_TRY(cudaMemcpy(M.rank.data(), P.rank.p, M.rank.size() * 4, cudaMemcpyDeviceToHost));
   }
   const double ms_tx0 = ms_since(tx0);
+  ST.mark("D2H edges + rank matrix");
 
   // ---------------- dimension 0
   auto t0 = std::chrono::steady_clock::now();
@@ -287,6 +303,7 @@ void run_full(vr_plan& P, vr_result* R) {
     s0.ms_transfer = ms_tx0;
   }
 
+  ST.mark("dim 0");
   // ---------------- output-sensitive mode?  (dense enumeration of
   // C(n, d+1) indices is wasted work when few edges are under the threshold)
   {
@@ -324,6 +341,7 @@ void run_full(vr_plan& P, vr_result* R) {
     if (R) R->stats[0].ms_transfer += ms_since(ta);
   }
 
+  ST.mark("adjacency");
   // ---------------- dimensions 1..D
   P.dims.clear();
   P.dims.resize((size_t)D + 2);
@@ -353,9 +371,11 @@ void run_full(vr_plan& P, vr_result* R) {
       vr::launch_set_bits(d1.deaths_in.as<uint64_t>(), d1.ndeaths_in, clr_of(1), st, &P.launches);
     }
   }
+  ST.mark("bitmaps");
   for (int d = 1; d <= D; ++d) {
     DimRun& dr = P.dims[(size_t)d];
     vr_stats stt{};
+    ST.mark("dim start");
     const uint64_t cand = binom_host((uint64_t)n, (uint64_t)d + 1);
     stt.candidates = (int64_t)cand;
     double ms_tx = 0;
@@ -405,6 +425,7 @@ void run_full(vr_plan& P, vr_result* R) {
         P.rows_cap[(size_t)d] = std::max<uint64_t>(bound, 1);
       }
     }
+    ST.mark("  row bound");
     // queue / residual capacity: every candidate, bounded by a share of free device memory
     CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
     const uint64_t qmax = std::max<uint64_t>((uint64_t)(free_b / 4 / 40), 1024);
@@ -425,6 +446,7 @@ void run_full(vr_plan& P, vr_result* R) {
       P.app_pairs.ensure((size_t)app_cap * 16);
       app_ptr = P.app_pairs.as<uint64_t>();
     }
+    ST.mark("  allocate queue");
     vr::DimCounters* ctr = P.ctrs.as<vr::DimCounters>() + d;
     CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(vr::DimCounters), st));
     dr.chunks.clear();
@@ -493,6 +515,7 @@ void run_full(vr_plan& P, vr_result* R) {
       P.rows_count[(size_t)d] = ro;
     }
     dr.residual = resid_count;
+    ST.mark("  enumerate + resolve");
     // a4: sort the residual columns into coboundary order
     P.resid_alt.ensure(std::max<uint64_t>(resid_count, 1) * 8);
     size_t stmp = vr::radix_sort_temp_bytes(std::max<uint64_t>(resid_count, 1));
@@ -516,11 +539,13 @@ void run_full(vr_plan& P, vr_result* R) {
       app_h.resize((size_t)std::min<uint64_t>(hc.app_pairs, app_cap) * 2);
       CUDA_TRY(cudaMemcpy(app_h.data(), app_ptr, app_h.size() * 8, cudaMemcpyDeviceToHost));
     }
+    ST.mark("  sort + D2H");
     // off path: residual reduction on the host
     auto tr = std::chrono::steady_clock::now();
     vr::ResidualStats rst;
     vr::residual_reduce(M, d, P.maxr, cbits, hkeys.data(), resid_count, P.opt.residual_mode, hp[(size_t)d], deaths, rst);
     stt.ms_residual = ms_since(tr);
+    ST.mark("  residual (host)");
     // deaths of dimension d -> clearing input of dimension d+1
     if (d < D) {
       tx = std::chrono::steady_clock::now();
@@ -560,6 +585,7 @@ void run_full(vr_plan& P, vr_result* R) {
     }
   }
 
+  ST.mark("dims done");
   // ---------------- result
   if (R) {
     for (int d = 0; d <= D; ++d) {
@@ -714,7 +740,8 @@ int vr_barcodes_device(const float* d_lt, int64_t n, int32_t max_dim, float thre
 
 int vr_barcodes(const float* lt, int64_t n, int32_t max_dim, float threshold, const vr_options* opt, vr_result** out) {
   if (out) *out = nullptr;
-  return guarded([&] {
+  SectionTimer ST;
+  int rc = guarded([&] {
     if (!out) throw VrError(VR_EINVAL, "out is NULL");
     check_args(lt, n, max_dim, threshold);
     vr_options o = default_options(opt);
@@ -722,19 +749,24 @@ int vr_barcodes(const float* lt, int64_t n, int32_t max_dim, float threshold, co
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw VrError(VR_EDEVICE, "no CUDA device");
     if (o.device < 0 || o.device >= ndev) throw VrError(VR_EINVAL, "options.device out of range");
     CUDA_TRY(cudaSetDevice(o.device));
-    vr_plan P;
-    P.n = n; P.D = max_dim; P.threshold = threshold; P.opt = o;
-    CUDA_TRY(cudaStreamCreateWithFlags(&P.st, cudaStreamNonBlocking));
-    struct SG { cudaStream_t s; ~SG() { cudaStreamDestroy(s); } } sg{P.st};
+    std::unique_ptr<vr_plan> P(new vr_plan());
+    P->n = n; P->D = max_dim; P->threshold = threshold; P->opt = o;
+    CUDA_TRY(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking));
+    struct SG { cudaStream_t s; ~SG() { cudaStreamDestroy(s); } } sg{P->st};
     const size_t bytes = (size_t)n * (size_t)(n - 1) / 2 * sizeof(float);
-    P.lt_copy.ensure(std::max<size_t>(bytes, 4));
-    if (bytes) CUDA_TRY(cudaMemcpyAsync(P.lt_copy.p, lt, bytes, cudaMemcpyHostToDevice, P.st));
-    P.d_lt = P.lt_copy.as<float>();
+    P->lt_copy.ensure(std::max<size_t>(bytes, 4));
+    if (bytes) CUDA_TRY(cudaMemcpyAsync(P->lt_copy.p, lt, bytes, cudaMemcpyHostToDevice, P->st));
+    P->d_lt = P->lt_copy.as<float>();
+    ST.mark("H2D input");
     std::unique_ptr<vr_result> R(new vr_result());
-    run_full(P, R.get());
-    CUDA_TRY(cudaStreamSynchronize(P.st));
+    run_full(*P, R.get());
+    CUDA_TRY(cudaStreamSynchronize(P->st));
+    ST.mark("run_full");
+    P.reset();
+    ST.mark("release device buffers");
     *out = R.release();
   });
+  return rc;
 }
 
 int32_t vr_max_dim(const vr_result* r) { return r ? r->max_dim : -1; }
