@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sample", type=int, default=None, help="oracle sample size (points)")
+    ap.add_argument("--no-target", action="store_true", help="skip the north-star target run (config 5, max_dim 2)")
     return ap.parse_args()
 
 
@@ -279,6 +280,21 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    if not args.no_target:
+        # BASELINE.json north_star target: "the dim-2 n=4096 workload under 1 s on one B200"
+        # (reading A22: config 5's o3-shaped cloud at max_dim = 2, t = 1.4), end to end
+        # through the public host-pointer call
+        c5 = G.CONFIGS["c5_o3_4096"]
+        lt5 = c5.lower_tri()
+        vr.barcodes(lt5, c5.n, 2, c5.threshold)  # warm
+        walls = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            b5 = vr.barcodes(lt5, c5.n, 2, c5.threshold)
+            walls.append(time.perf_counter() - t0)
+        line["target_c5_maxdim2"] = {"wall_s": statistics.median(walls), "target_s": 1.0,
+                                     "survivors": sum(b5.stats[d]["survivors"] for d in (1, 2)),
+                                     "bars": [len(p) for p in b5.pairs]}
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(cfg, D, args.sample or default_sample(cfg, D))
