@@ -164,6 +164,47 @@ int vr_plan_timing(vr_plan* plan, double out[9]);
 void vr_plan_free(vr_plan* plan);
 
 /* ----------------------------------------------------------------------------------
+ * Distributed stepping (the a7 exchange).  One process per GPU.  Each
+ * rank runs its shard of every dimension's hot path; the caller performs the two
+ * exchanges of each dimension with its own collectives (paper_2502_05063_b200/dist.py
+ * uses torch.distributed / NCCL):
+ *   1. the next dimension's clearing bitmap: copy out (vr_dist_bitmap direction 0), SUM
+ *      all-reduce over the ranks — every death bit is set by exactly one rank, so the sum
+ *      is the bitwise OR — and copy back in (direction 1);
+ *   2. the residual columns: copy the locally sorted keys out (vr_dist_copy_keys),
+ *      all-gather, merge by key (coboundary order is the key order) and hand the merged
+ *      host array to vr_dist_dim_finish, which every rank runs identically.
+ * Shards: dense prefix rows are interleaved over the ranks (row r belongs to rank
+ * r mod world, taken from the last row down); in the output-sensitive mode dimension 1
+ * interleaves the vertices and dimension d >= 2 extends each rank's own survivors of
+ * d-1, which partitions the d-simplices (each has exactly one prefix (d-1)-simplex).
+ * Device pointers are on the current device; `stream` as in vr_barcodes_device.
+ * ---------------------------------------------------------------------------------- */
+int vr_dist_begin(const float* d_dist_lower_tri, int64_t n, int32_t max_dim, float threshold, const vr_options* opt,
+                  void* stream, int32_t rank, int32_t world, vr_plan** plan);
+/* runs dimension d locally; *nkeys = local residual columns; *next_bitmap_words = size of
+ * the dimension-(d+1) clearing bitmap in uint32 words (0 = recompute mode, no exchange) */
+int vr_dist_dim_local(vr_plan* plan, int32_t d, int64_t* nkeys, int64_t* next_bitmap_words);
+int vr_dist_copy_keys(vr_plan* plan, int32_t d, uint64_t* dst_device);
+int vr_dist_bitmap(vr_plan* plan, int32_t d, uint32_t* buf_device, int32_t direction /* 0 out, 1 in */);
+/* local counters of dimension d: survivors, apparent, cleared, queued, scanned, residual */
+int vr_dist_counters(vr_plan* plan, int32_t d, int64_t out[6]);
+int vr_dist_dim_finish(vr_plan* plan, int32_t d, const uint64_t* merged_keys_host, int64_t nkeys);
+/* assembles the barcode (every rank holds the same pairs); free the plan with vr_plan_free */
+int vr_dist_end(vr_plan* plan, vr_result** out);
+
+/* ----------------------------------------------------------------------------------
+ * Component entry (tests, no GPU needed): the library's host residual reduction of
+ * dimension d (Alg 12 / §5.2.9-5.2.11) on caller-provided columns.  rank: host n x n rank
+ * matrix (see vr_common.cuh), values[r] = the distance with rank r, keys: the
+ * non-apparent, non-cleared columns ((maxr - rank) << cbits | cidx) sorted ascending.
+ * Writes one entry per column (death = +inf, death_cidx = UINT64_MAX for essential).
+ * ---------------------------------------------------------------------------------- */
+int vr_host_residual(const uint32_t* rank, const float* values, int64_t nvalues, int64_t n, int32_t d, uint32_t maxr,
+                     int32_t cbits, const uint64_t* keys, int64_t nkeys, int32_t mode, float* birth, float* death,
+                     uint64_t* birth_cidx, uint64_t* death_cidx, int64_t* emergent);
+
+/* ----------------------------------------------------------------------------------
  * Component entry (tests): the library's device radix sort on
  * caller keys.  keys: HOST pointer to n uint64 values, sorted ascending in place on bits
  * [begin_bit, end_bit) (LSD, stable; bits outside the range do not take part in the

@@ -90,6 +90,15 @@ def load() -> ctypes.CDLL:
         "vr_plan_timing": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double)]),
         "vr_plan_free": (None, [vp]),
         "vr_radix_sort_u64": (ctypes.c_int, [vp, i64, i32, i32]),
+        "vr_dist_begin": (ctypes.c_int, [vp, i64, i32, f32, vp, vp, i32, i32, ctypes.POINTER(vp)]),
+        "vr_dist_dim_local": (ctypes.c_int, [vp, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+        "vr_dist_copy_keys": (ctypes.c_int, [vp, i32, vp]),
+        "vr_dist_bitmap": (ctypes.c_int, [vp, i32, vp, i32]),
+        "vr_dist_counters": (ctypes.c_int, [vp, i32, ctypes.POINTER(i64)]),
+        "vr_dist_dim_finish": (ctypes.c_int, [vp, i32, vp, i64]),
+        "vr_dist_end": (ctypes.c_int, [vp, ctypes.POINTER(vp)]),
+        "vr_host_residual": (ctypes.c_int, [vp, vp, i64, i64, i32, ctypes.c_uint32, i32, vp, i64, i32, vp, vp, vp, vp,
+                                            ctypes.POINTER(i64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -198,6 +207,23 @@ def radix_sort_u64(keys: np.ndarray, begin_bit: int = 0, end_bit: int = 64) -> n
     a = np.ascontiguousarray(keys, dtype=np.uint64).copy()
     _check(load().vr_radix_sort_u64(a.ctypes.data if a.size else None, a.size, begin_bit, end_bit))
     return a
+
+
+def host_residual(rank: np.ndarray, values: np.ndarray, n: int, d: int, maxr: int, cbits: int, keys: np.ndarray,
+                  mode: int = 0):
+    """The library's host residual reduction (component entry; no GPU needed).  Returns
+    (birth, death, birth_cidx, death_cidx, emergent) per column."""
+    lib = load()
+    R = np.ascontiguousarray(rank, dtype=np.uint32)
+    V = np.ascontiguousarray(values, dtype=np.float32)
+    K = np.ascontiguousarray(keys, dtype=np.uint64)
+    m = K.size
+    b = np.zeros(max(m, 1), np.float32); de = np.zeros(max(m, 1), np.float32)
+    bc = np.zeros(max(m, 1), np.uint64); dc = np.zeros(max(m, 1), np.uint64)
+    em = ctypes.c_int64(0)
+    _check(lib.vr_host_residual(R.ctypes.data, V.ctypes.data, V.size, n, d, maxr, cbits, K.ctypes.data if m else None, m,
+                                mode, b.ctypes.data, de.ctypes.data, bc.ctypes.data, dc.ctypes.data, ctypes.byref(em)))
+    return b[:m], de[:m], bc[:m], dc[:m], int(em.value)
 
 
 class Plan:

@@ -230,13 +230,16 @@ __global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p,
   // Rows are handed out from the LAST row down: the work of a row grows with its
   // smallest prefix vertex u_1 (row length), which grows with the row index, so the
   // small rows form the tail of the schedule.
-  const uint64_t nrows = p.row_end - p.row_begin;
+  const uint64_t W = (uint64_t)p.shard_world;
+  const uint64_t all = p.row_end - p.row_begin;
+  const uint64_t nrows = all > (uint64_t)p.shard_rank ? (all - (uint64_t)p.shard_rank + W - 1) / W : 0;  // this shard's rows
   while (true) {
     unsigned long long g0 = 0;
     if (lane == 0) g0 = atomicAdd(&B.ctr->row_next, (unsigned long long)GRAB);
     g0 = __shfl_sync(0xffffffffu, g0, 0);
     if (g0 >= nrows) break;
-    const uint64_t rtop = p.row_end - 1 - g0;  // process rows rtop, rtop-1, ..., rlow
+    // process rows rtop, rtop-1, ... (GRAB is 1 when sharded)
+    const uint64_t rtop = p.row_end - 1 - (g0 * W + (uint64_t)p.shard_rank);
     const uint64_t cnt = (g0 + GRAB <= nrows) ? (uint64_t)GRAB : nrows - g0;
     // decode prefix row rtop (colex rank of {u_D > ... > u_1}: r = sum_i C(u_i, i))
     int u[D + 2];

@@ -227,13 +227,15 @@ template <int D>
 __global__ void __launch_bounds__(SP_THREADS) k_enum_sparse(Tables T, DimParams p, HotBuffers B, SparseRows S) {
   const int lane = threadIdx.x & 31;
   unsigned long long surv_acc = 0, app_acc = 0, scan_acc = 0, clr_acc = 0;
-  const uint64_t nrows = p.row_end - p.row_begin;
+  const uint64_t W = (uint64_t)p.shard_world;
+  const uint64_t all = p.row_end - p.row_begin;
+  const uint64_t nrows = all > (uint64_t)p.shard_rank ? (all - (uint64_t)p.shard_rank + W - 1) / W : 0;  // this shard's rows
   while (true) {
     unsigned long long g = 0;
     if (lane == 0) g = atomicAdd(&B.ctr->row_next, 1ull);
     g = __shfl_sync(0xffffffffu, g, 0);
     if (g >= nrows) break;
-    const uint64_t r = p.row_begin + g;
+    const uint64_t r = p.row_begin + g * W + (uint64_t)p.shard_rank;
     int u[D + 2];
     if (S.rows_in == nullptr) {  // dimension 1: the rows are the vertices
       u[1] = (int)r;

@@ -94,6 +94,7 @@ struct DimRun {
   int64_t ndeaths_in = 0;
   DevBuf clr;        // clearing bitmap over the d-simplices (empty: recompute mode)
   size_t clr_words = 0;
+  bool active = false;
 };
 
 }  // namespace
@@ -107,6 +108,14 @@ struct vr_result {
 };
 
 struct vr_plan {
+  std::unique_ptr<vr_result> R{new vr_result()};
+  vr::HostMatrix M;                  // host copies for the off-path steps
+  std::vector<vr::HostPairs> hp;     // pairs per dimension
+  std::vector<uint64_t> deaths;      // deaths of the last finished dimension
+  int rbits = 1;
+  cudaEvent_t ev[8] = {};
+  uint64_t* local_sorted = nullptr;  // this rank's sorted residual keys of the last dimension run
+  int32_t rank_id = 0, world = 1;    // shard of the rows (distributed driver)
   int64_t n = 0;
   int32_t D = 0;
   float threshold = 0.0f;
@@ -137,6 +146,23 @@ struct vr_plan {
   ~vr_plan() {
     for (auto& v : stage_ev)
       for (auto& e : v) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  uint32_t* clr_of(int d) {
+    return (d >= 1 && d <= D && dims[(size_t)d].clr_words) ? dims[(size_t)d].clr.as<uint32_t>() : nullptr;
+  }
+  vr::SparseRows sparse_rows(int d, vr::DimCounters* ctr) {
+    vr::SparseRows SR{};
+    if (sparse) {
+      SR.adj_off = adj_off.as<uint32_t>();
+      SR.adj = adj.as<uint16_t>();
+      SR.rows_in = d == 1 ? nullptr : rows[(size_t)d - 1].as<uint4>();
+      SR.rows_out = d < D ? rows[(size_t)d].as<uint4>() : nullptr;
+      SR.rows_out_cap = d < D ? rows_cap[(size_t)d] : 0;
+      SR.rows_out_count = &ctr->rows_out;
+    }
+    return SR;
   }
 };
 
@@ -202,9 +228,20 @@ struct SectionTimer {
   }
 };
 
-// ------------------------------------------------------------------ the run
-void run_full(vr_plan& P, vr_result* R) {
+// ------------------------------------------------------------------ the run, in stages
+// stage_setup        binomials, a0 tables, host copies, dimension 0, sparse adjacency,
+//                    clearing bitmaps, dimension-1 clearing input
+// stage_dim_local    this rank's shard of dimension d on the device (enumerate, apparent,
+//                    clearing, compaction, local radix sort); leaves the sorted residual
+//                    keys on the device
+// stage_dim_finish   the host residual reduction of dimension d on the (merged) residual
+//                    columns; deaths -> clearing input of d+1
+// stage_result       barcode assembly
+// A single-GPU run calls them in sequence; the distributed driver (paper_2502_05063_b200/
+// dist.py) interleaves the two exchanges of SURVEY.md §8(e) between local and finish.
+void stage_setup(vr_plan& P) {
   SectionTimer ST;
+  vr_result* R = P.R.get();
   const int64_t n = P.n;
   const int D = P.D;
   cudaStream_t st = P.st;
@@ -232,47 +269,41 @@ void run_full(vr_plan& P, vr_result* R) {
   P.ctrs.ensure(sizeof(vr::DimCounters) * (size_t)(D + 1));
   P.sort_tmp.ensure(vr::radix_sort_temp_bytes(std::max<size_t>(P.N, 1)));
   CUDA_TRY(cudaMemcpyAsync(P.binom.p, hb.data(), hb.size() * 8, cudaMemcpyHostToDevice, st));
-
-  cudaEvent_t ev[8];
-  for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
-  struct EvGuard {
-    cudaEvent_t* e;
-    ~EvGuard() { for (int i = 0; i < 8; ++i) cudaEventDestroy(e[i]); }
-  } evg{ev};
+  for (auto& e : P.ev)
+    if (!e) CUDA_TRY(cudaEventCreate(&e));
 
   ST.mark("allocate tables");
   // ---------------- a0
   uint64_t* sorted = nullptr;
-  CUDA_TRY(cudaEventRecord(ev[0], st));
+  CUDA_TRY(cudaEventRecord(P.ev[0], st));
   vr::launch_tables(P.d_lt, n, P.threshold, P.keys.as<uint64_t>(), P.alt.as<uint64_t>(), P.rowmax.as<uint32_t>(),
                     P.sort_tmp.p, P.rank.as<uint32_t>(), P.tout.as<vr::TablesOut>(), &sorted, st, &P.launches);
   CUDA_TRY(cudaGetLastError());
   vr::TablesOut to{};
   CUDA_TRY(cudaMemcpyAsync(&to, P.tout.p, sizeof to, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaEventRecord(ev[1], st));
+  CUDA_TRY(cudaEventRecord(P.ev[1], st));
   CUDA_TRY(cudaStreamSynchronize(st));
   ST.mark("tables (device)");
   if (to.err) throw VrError(VR_EINPUT, "dist_lower_tri holds a negative or NaN distance");
   float tms = 0;
-  cudaEventElapsedTime(&tms, ev[0], ev[1]);
+  cudaEventElapsedTime(&tms, P.ev[0], P.ev[1]);
   float tused;
   std::memcpy(&tused, &to.tbits, 4);
   P.m = to.m_le_t;
   P.maxr = P.m ? (uint32_t)(P.m - 1) : 0;
-  const int rbits = bits_for(P.maxr);
+  P.rbits = bits_for(P.maxr);
 
-  if (R) {
-    R->max_dim = D;
-    R->tused = tused;
-    R->pairs.assign((size_t)D + 1, {});
-    R->ipairs.assign((size_t)D + 1, {});
-    R->stats.assign((size_t)D + 1, vr_stats{});
-  }
-  std::vector<vr::HostPairs> hp((size_t)D + 1);
+  R->max_dim = D;
+  R->tused = tused;
+  R->pairs.assign((size_t)D + 1, {});
+  R->ipairs.assign((size_t)D + 1, {});
+  R->stats.assign((size_t)D + 1, vr_stats{});
+  P.hp.assign((size_t)D + 1, {});
 
   // ---------------- host copies for the off-path steps (sorted edges, rank matrix)
   auto tx0 = std::chrono::steady_clock::now();
-  vr::HostMatrix M;
+  vr::HostMatrix& M = P.M;
+  M = vr::HostMatrix();
   M.n = n;
   M.kmax = P.kmax;
   M.binom = hb;
@@ -290,11 +321,11 @@ void run_full(vr_plan& P, vr_result* R) {
   const double ms_tx0 = ms_since(tx0);
   ST.mark("D2H edges + rank matrix");
 
-  // ---------------- dimension 0
+  // ---------------- dimension 0 (replicated on every rank: cheap, §5.2.5)
   auto t0 = std::chrono::steady_clock::now();
-  std::vector<uint64_t> deaths;
-  vr::dim0_union_find(n, h_edges.data(), P.m, P.kbits, hp[0], deaths);
-  if (R) {
+  P.deaths.clear();
+  vr::dim0_union_find(n, h_edges.data(), P.m, P.kbits, P.hp[0], P.deaths);
+  {
     vr_stats& s0 = R->stats[0];
     s0.candidates = n;
     s0.survivors = n;
@@ -328,25 +359,21 @@ void run_full(vr_plan& P, vr_result* R) {
       P.rows.resize((size_t)D + 2);
       P.rows_count.assign((size_t)D + 2, 0);
       P.rows_cap.assign((size_t)D + 2, 0);
+      // the host residual walks the same threshold-graph adjacency
+      auto ta = std::chrono::steady_clock::now();
+      M.adj_off.resize((size_t)n + 1);
+      CUDA_TRY(cudaMemcpyAsync(M.adj_off.data(), P.adj_off.p, ((size_t)n + 1) * 4, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      M.adj.resize((size_t)M.adj_off[(size_t)n]);
+      if (!M.adj.empty()) CUDA_TRY(cudaMemcpy(M.adj.data(), P.adj.p, M.adj.size() * 2, cudaMemcpyDeviceToHost));
+      R->stats[0].ms_transfer += ms_since(ta);
     }
   }
-
-  if (P.sparse) {  // the host residual walks the same threshold-graph adjacency
-    auto ta = std::chrono::steady_clock::now();
-    M.adj_off.resize((size_t)n + 1);
-    CUDA_TRY(cudaMemcpyAsync(M.adj_off.data(), P.adj_off.p, ((size_t)n + 1) * 4, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    M.adj.resize((size_t)M.adj_off[(size_t)n]);
-    if (!M.adj.empty()) CUDA_TRY(cudaMemcpy(M.adj.data(), P.adj.p, M.adj.size() * 2, cudaMemcpyDeviceToHost));
-    if (R) R->stats[0].ms_transfer += ms_since(ta);
-  }
-
   ST.mark("adjacency");
-  // ---------------- dimensions 1..D
+
+  // ---------------- clearing bitmaps (one bit per d-simplex index) where they fit
   P.dims.clear();
   P.dims.resize((size_t)D + 2);
-  const int steps = P.opt.apparent_steps > 0 ? P.opt.apparent_steps : kDefaultSteps;
-  // clearing bitmaps (one bit per d-simplex index) where they fit; else recompute mode
   CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
   for (int d = 1; d <= D; ++d) {
     const uint64_t cand = binom_host((uint64_t)n, (uint64_t)d + 1);
@@ -356,258 +383,284 @@ void run_full(vr_plan& P, vr_result* R) {
       P.dims[(size_t)d].clr_words = words;
     }
   }
-  auto clr_of = [&](int d) -> uint32_t* {
-    return (d >= 1 && d <= D && P.dims[(size_t)d].clr_words) ? P.dims[(size_t)d].clr.as<uint32_t>() : nullptr;
-  };
   // deaths of dimension 0 -> clearing input of dimension 1
   {
     DimRun& d1 = P.dims[1];
-    d1.deaths_in.ensure(std::max<size_t>(deaths.size(), 1) * 8);
-    d1.ndeaths_in = (int64_t)deaths.size();
-    if (!deaths.empty())
-      CUDA_TRY(cudaMemcpyAsync(d1.deaths_in.p, deaths.data(), deaths.size() * 8, cudaMemcpyHostToDevice, st));
-    if (D >= 1 && clr_of(1)) {
-      CUDA_TRY(cudaMemsetAsync(clr_of(1), 0, d1.clr_words * 4, st));
-      vr::launch_set_bits(d1.deaths_in.as<uint64_t>(), d1.ndeaths_in, clr_of(1), st, &P.launches);
+    d1.deaths_in.ensure(std::max<size_t>(P.deaths.size(), 1) * 8);
+    d1.ndeaths_in = (int64_t)P.deaths.size();
+    if (!P.deaths.empty())
+      CUDA_TRY(cudaMemcpyAsync(d1.deaths_in.p, P.deaths.data(), P.deaths.size() * 8, cudaMemcpyHostToDevice, st));
+    if (D >= 1 && P.clr_of(1)) {
+      CUDA_TRY(cudaMemsetAsync(P.clr_of(1), 0, d1.clr_words * 4, st));
+      vr::launch_set_bits(d1.deaths_in.as<uint64_t>(), d1.ndeaths_in, P.clr_of(1), st, &P.launches);
     }
   }
   ST.mark("bitmaps");
-  for (int d = 1; d <= D; ++d) {
-    DimRun& dr = P.dims[(size_t)d];
-    vr_stats stt{};
-    ST.mark("dim start");
-    const uint64_t cand = binom_host((uint64_t)n, (uint64_t)d + 1);
-    stt.candidates = (int64_t)cand;
-    double ms_tx = 0;
-    if (cand == 0 || P.m == 0) {
-      if (R) R->stats[(size_t)d] = stt;
-      deaths.clear();
-      if (d < D) P.dims[(size_t)d + 1].ndeaths_in = 0;
-      continue;
-    }
-    const int cbits = bits_for(cand - 1);
-    if (rbits + cbits > 64)
-      throw VrError(VR_ECAPACITY, "column key (rank bits + cidx bits) does not fit 64 bits");
-    vr::DimParams& p = dr.p;
-    p.d = d;
-    p.n = n;
-    p.maxr = P.maxr;
-    p.cbits = cbits;
-    p.steps = steps;
-    p.grab = P.opt.rows_per_grab > 0 ? P.opt.rows_per_grab : (n < 384 ? 4 : 1);
-    p.variant = P.opt.scan_variant > 0 ? P.opt.scan_variant - 1 : 1;
-    const uint64_t rows = binom_host((uint64_t)n, (uint64_t)d);
-    dr.sort_bits = rbits + cbits;
-    // the next dimension's bitmap receives this dimension's apparent cofacets
-    uint32_t* clr_next = clr_of(d + 1);
-    if (clr_next) CUDA_TRY(cudaMemsetAsync(clr_next, 0, P.dims[(size_t)d + 1].clr_words * 4, st));
+}
 
-    // sparse mode: the rows are the survivors of dimension d-1 (vertices for d = 1) and
-    // sum over rows of deg_below(u_1) bounds the d-simplices they can produce
-    uint64_t bound = cand;
-    uint64_t nrows_sp = 0;
-    if (P.sparse) {
-      if (d == 1) {
-        nrows_sp = (uint64_t)n;
-        bound = P.m;
-      } else {
-        nrows_sp = P.rows_count[(size_t)d - 1];
-        CUDA_TRY(cudaMemsetAsync(P.bound.p, 0, 8, st));
-        vr::launch_row_bound(P.rows[(size_t)d - 1].as<uint4>(), nrows_sp, d - 1, P.deg_below.as<uint32_t>(),
-                             P.bound.as<unsigned long long>(), st, &P.launches);
-        unsigned long long b = 0;
-        CUDA_TRY(cudaMemcpyAsync(&b, P.bound.p, 8, cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaStreamSynchronize(st));
-        bound = std::min<uint64_t>(cand, b);
-      }
-      if (d < D) {
-        P.rows[(size_t)d].ensure(std::max<uint64_t>(bound, 1) * 16);
-        P.rows_cap[(size_t)d] = std::max<uint64_t>(bound, 1);
-      }
-    }
-    ST.mark("  row bound");
-    // queue / residual capacity: every candidate, bounded by a share of free device memory
-    CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-    const uint64_t qmax = std::max<uint64_t>((uint64_t)(free_b / 4 / 40), 1024);
-    const uint64_t qwant = std::min<uint64_t>(std::max<uint64_t>(bound, 1), qmax);
-    if (P.sparse && bound > qmax) throw VrError(VR_ECAPACITY, "output-sensitive mode: column bound exceeds device memory");
-    if (P.qcap < qwant) {
-      P.queue.ensure((size_t)qwant * 8);
-      P.qvert.ensure((size_t)qwant * 16);
-      P.qcap = qwant;
-    }
-    uint64_t rows_per_chunk = P.sparse ? nrows_sp : rows;
-    const uint64_t rows_total = P.sparse ? nrows_sp : rows;
-    if (!P.sparse && cand > P.qcap) rows_per_chunk = std::max<uint64_t>(1, P.qcap / (uint64_t)n);
-    uint64_t app_cap = 0;
-    uint64_t* app_ptr = nullptr;
-    if (P.opt.index_pairs) {
-      app_cap = std::max<uint64_t>(bound, 1);
-      P.app_pairs.ensure((size_t)app_cap * 16);
-      app_ptr = P.app_pairs.as<uint64_t>();
-    }
-    ST.mark("  allocate queue");
-    vr::DimCounters* ctr = P.ctrs.as<vr::DimCounters>() + d;
-    CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(vr::DimCounters), st));
-    dr.chunks.clear();
-    float t_enum = 0, t_res = 0;
-    uint64_t resid_count = 0;
-    for (uint64_t rb = 0; rb < rows_total; rb += rows_per_chunk) {
-      const uint64_t re = std::min(rows_total, rb + rows_per_chunk);
-      const uint64_t chunk_cand = P.sparse ? std::max<uint64_t>(bound, 1) : std::min<uint64_t>(cand, (re - rb) * (uint64_t)n);
-      // residual capacity: what is there plus everything this chunk could add
-      if (P.rcap < resid_count + chunk_cand || !P.resid.p) {
-        const uint64_t ncap = std::max<uint64_t>(resid_count + chunk_cand, 1024);
-        DevBuf nb;
-        nb.ensure((size_t)ncap * 8);
-        if (resid_count) CUDA_TRY(cudaMemcpyAsync(nb.p, P.resid.p, resid_count * 8, cudaMemcpyDeviceToDevice, st));
-        CUDA_TRY(cudaStreamSynchronize(st));
-        std::swap(P.resid.p, nb.p);
-        std::swap(P.resid.bytes, nb.bytes);
-        P.rcap = ncap;
-      }
-      vr::HotBuffers B{P.queue.as<uint64_t>(), P.qvert.as<uint4>(), P.qcap, P.resid.as<uint64_t>(), P.rcap,
-                       clr_of(d), clr_next, dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, ctr, app_ptr, app_cap};
-      vr::SparseRows SR{};
-      if (P.sparse) {
-        SR.adj_off = P.adj_off.as<uint32_t>();
-        SR.adj = P.adj.as<uint16_t>();
-        SR.rows_in = d == 1 ? nullptr : P.rows[(size_t)d - 1].as<uint4>();
-        SR.rows_out = d < D ? P.rows[(size_t)d].as<uint4>() : nullptr;
-        SR.rows_out_cap = d < D ? P.rows_cap[(size_t)d] : 0;
-        SR.rows_out_count = &ctr->rows_out;
-      }
-      p.row_begin = rb;
-      p.row_end = re;
-      CUDA_TRY(cudaMemsetAsync(&ctr->row_next, 0, 8, st));
-      CUDA_TRY(cudaMemsetAsync(&ctr->queued, 0, 8, st));
-      CUDA_TRY(cudaEventRecord(ev[2], st));
-      if (P.sparse) vr::launch_enumerate_sparse(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, SR, st, &P.launches);
-      else vr::launch_enumerate(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, st, &P.launches);
-      CUDA_TRY(cudaGetLastError());
-      CUDA_TRY(cudaEventRecord(ev[3], st));
-      unsigned long long q = 0;
-      CUDA_TRY(cudaMemcpyAsync(&q, &ctr->queued, 8, cudaMemcpyDeviceToHost, st));
+// Runs this rank's shard of dimension d; returns the number of local residual columns,
+// sorted on the device at P.local_sorted.
+uint64_t stage_dim_local(vr_plan& P, int d) {
+  SectionTimer ST;
+  vr_result* R = P.R.get();
+  const int64_t n = P.n;
+  const int D = P.D;
+  cudaStream_t st = P.st;
+  DimRun& dr = P.dims[(size_t)d];
+  vr_stats& stt = R->stats[(size_t)d];
+  stt = vr_stats{};
+  P.local_sorted = nullptr;
+  const uint64_t cand = binom_host((uint64_t)n, (uint64_t)d + 1);
+  stt.candidates = (int64_t)cand;
+  dr.chunks.clear();
+  dr.residual = 0;
+  dr.active = !(cand == 0 || P.m == 0);
+  if (!dr.active) return 0;
+  const int cbits = bits_for(cand - 1);
+  if (P.rbits + cbits > 64) throw VrError(VR_ECAPACITY, "column key (rank bits + cidx bits) does not fit 64 bits");
+  const int steps = P.opt.apparent_steps > 0 ? P.opt.apparent_steps : kDefaultSteps;
+  vr::DimParams& p = dr.p;
+  p.d = d;
+  p.n = n;
+  p.maxr = P.maxr;
+  p.cbits = cbits;
+  p.steps = steps;
+  p.grab = P.world > 1 ? 1 : (P.opt.rows_per_grab > 0 ? P.opt.rows_per_grab : (n < 384 ? 4 : 1));
+  p.variant = P.opt.scan_variant > 0 ? P.opt.scan_variant - 1 : 1;
+  // shards: dense rows (and the vertex rows of sparse dimension 1) are interleaved over
+  // the ranks; sparse rows of d >= 2 are this rank's own survivors of d-1, which already
+  // partition the d-simplices (each has exactly one prefix (d-1)-simplex)
+  const bool interleave = P.world > 1 && (!P.sparse || d == 1);
+  p.shard_rank = interleave ? P.rank_id : 0;
+  p.shard_world = interleave ? P.world : 1;
+  const uint64_t rows = binom_host((uint64_t)n, (uint64_t)d);
+  dr.sort_bits = P.rbits + cbits;
+  // the next dimension's bitmap receives this dimension's apparent cofacets
+  uint32_t* clr_next = P.clr_of(d + 1);
+  if (clr_next) CUDA_TRY(cudaMemsetAsync(clr_next, 0, P.dims[(size_t)d + 1].clr_words * 4, st));
+
+  // sparse mode: the rows are the survivors of dimension d-1 (vertices for d = 1) and
+  // sum over rows of deg_below(u_1) bounds the d-simplices they can produce
+  uint64_t bound = cand;
+  uint64_t nrows_sp = 0;
+  if (P.sparse) {
+    if (d == 1) {
+      nrows_sp = (uint64_t)n;
+      bound = P.m;
+    } else {
+      nrows_sp = P.rows_count[(size_t)d - 1];
+      CUDA_TRY(cudaMemsetAsync(P.bound.p, 0, 8, st));
+      vr::launch_row_bound(P.rows[(size_t)d - 1].as<uint4>(), nrows_sp, d - 1, P.deg_below.as<uint32_t>(),
+                           P.bound.as<unsigned long long>(), st, &P.launches);
+      unsigned long long b = 0;
+      CUDA_TRY(cudaMemcpyAsync(&b, P.bound.p, 8, cudaMemcpyDeviceToHost, st));
       CUDA_TRY(cudaStreamSynchronize(st));
-      if (q > P.qcap) throw VrError(VR_ECAPACITY, "apparent-phase queue overflow");
-      float x = 0;
-      cudaEventElapsedTime(&x, ev[2], ev[3]);
-      t_enum += x;
-      CUDA_TRY(cudaEventRecord(ev[4], st));
-      if (P.sparse) vr::launch_resolve_sparse(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, SR, q, st, &P.launches);
-      else vr::launch_resolve(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, q, st, &P.launches);
-      CUDA_TRY(cudaGetLastError());
-      CUDA_TRY(cudaEventRecord(ev[5], st));
-      unsigned long long rc = 0;
-      CUDA_TRY(cudaMemcpyAsync(&rc, &ctr->residual, 8, cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaStreamSynchronize(st));
-      cudaEventElapsedTime(&x, ev[4], ev[5]);
-      t_res += x;
-      if (rc > P.rcap) throw VrError(VR_ECAPACITY, "residual list overflow");
-      resid_count = rc;
-      dr.chunks.push_back(Chunk{rb, re, q});
+      bound = std::min<uint64_t>(cand, b);
     }
-    if (P.sparse && d < D) {
-      unsigned long long ro = 0;
-      CUDA_TRY(cudaMemcpyAsync(&ro, &ctr->rows_out, 8, cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaStreamSynchronize(st));
-      if (ro > P.rows_cap[(size_t)d]) throw VrError(VR_ECAPACITY, "survivor list overflow");
-      P.rows_count[(size_t)d] = ro;
-    }
-    dr.residual = resid_count;
-    ST.mark("  enumerate + resolve");
-    // a4: sort the residual columns into coboundary order
-    P.resid_alt.ensure(std::max<uint64_t>(resid_count, 1) * 8);
-    size_t stmp = vr::radix_sort_temp_bytes(std::max<uint64_t>(resid_count, 1));
-    if (P.sort_tmp.bytes < stmp) P.sort_tmp.ensure(stmp);
-    CUDA_TRY(cudaEventRecord(ev[6], st));
-    uint64_t* rsorted = vr::radix_sort_u64(P.resid.as<uint64_t>(), P.resid_alt.as<uint64_t>(), resid_count, 0,
-                                           dr.sort_bits, P.sort_tmp.p, st, &P.launches);
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaEventRecord(ev[7], st));
-    vr::DimCounters hc{};
-    CUDA_TRY(cudaMemcpyAsync(&hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, st));
-    std::vector<uint64_t> hkeys((size_t)resid_count);
-    auto tx = std::chrono::steady_clock::now();
-    CUDA_TRY(cudaStreamSynchronize(st));
-    float t_sort = 0;
-    cudaEventElapsedTime(&t_sort, ev[6], ev[7]);
-    if (resid_count) CUDA_TRY(cudaMemcpy(hkeys.data(), rsorted, resid_count * 8, cudaMemcpyDeviceToHost));
-    ms_tx += ms_since(tx);
-    std::vector<uint64_t> app_h;
-    if (P.opt.index_pairs && hc.app_pairs) {
-      app_h.resize((size_t)std::min<uint64_t>(hc.app_pairs, app_cap) * 2);
-      CUDA_TRY(cudaMemcpy(app_h.data(), app_ptr, app_h.size() * 8, cudaMemcpyDeviceToHost));
-    }
-    ST.mark("  sort + D2H");
-    // off path: residual reduction on the host
-    auto tr = std::chrono::steady_clock::now();
-    vr::ResidualStats rst;
-    vr::residual_reduce(M, d, P.maxr, cbits, hkeys.data(), resid_count, P.opt.residual_mode, hp[(size_t)d], deaths, rst);
-    stt.ms_residual = ms_since(tr);
-    ST.mark("  residual (host)");
-    // deaths of dimension d -> clearing input of dimension d+1
     if (d < D) {
-      tx = std::chrono::steady_clock::now();
-      DimRun& nx = P.dims[(size_t)d + 1];
-      nx.ndeaths_in = (int64_t)deaths.size();
-      nx.deaths_in.ensure(std::max<size_t>(deaths.size(), 1) * 8);
-      if (!deaths.empty())
-        CUDA_TRY(cudaMemcpyAsync(nx.deaths_in.p, deaths.data(), deaths.size() * 8, cudaMemcpyHostToDevice, st));
-      if (clr_next) vr::launch_set_bits(nx.deaths_in.as<uint64_t>(), nx.ndeaths_in, clr_next, st, &P.launches);
-      ms_tx += ms_since(tx);
-    }
-    stt.survivors = (int64_t)hc.survivors;
-    stt.apparent = (int64_t)(hc.apparent1 + hc.apparent2);
-    stt.cleared = (int64_t)hc.cleared;
-    stt.residual_columns = (int64_t)resid_count;
-    stt.emergent = rst.emergent;
-    stt.scanned = (int64_t)(hc.scanned + hc.scanned2);
-    P.work_candidates += (double)cand;
-    P.work_scanned += (double)hc.scanned;
-    P.work_scanned2 += (double)hc.scanned2;
-    P.work_rank_ops += (double)(d + 1) * ((double)cand + (double)hc.scanned);
-    P.work_rank_ops2 += (double)(d + 1) * (double)hc.scanned2;
-    if (const char* dump = std::getenv("VR_DUMP_RESIDUAL")) dump_residual(dump, M, d, P.maxr, cbits, hkeys);
-    stt.queued = 0;
-    for (auto& c : dr.chunks) stt.queued += (int64_t)c.queued;
-    stt.ms_enumerate = t_enum;
-    stt.ms_resolve = t_res;
-    stt.ms_sort = t_sort;
-    stt.ms_transfer = ms_tx;
-    P.survivors_total += stt.survivors;
-    P.apparent_total += stt.apparent;
-    P.residual_total += (int64_t)resid_count;
-    if (R) {
-      R->stats[(size_t)d] = stt;
-      if (P.opt.index_pairs)
-        for (size_t i = 0; i + 1 < app_h.size(); i += 2) R->ipairs[(size_t)d].push_back(vr_index_pair{app_h[i], app_h[i + 1]});
+      P.rows[(size_t)d].ensure(std::max<uint64_t>(bound, 1) * 16);
+      P.rows_cap[(size_t)d] = std::max<uint64_t>(bound, 1);
     }
   }
+  ST.mark("  row bound");
+  // queue / residual capacity: every candidate, bounded by a share of free device memory
+  size_t free_b = 0, total_b = 0;
+  CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  const uint64_t qmax = std::max<uint64_t>((uint64_t)(free_b / 4 / 40), 1024);
+  const uint64_t qwant = std::min<uint64_t>(std::max<uint64_t>(bound, 1), qmax);
+  if (P.sparse && bound > qmax) throw VrError(VR_ECAPACITY, "output-sensitive mode: column bound exceeds device memory");
+  if (P.qcap < qwant) {
+    P.queue.ensure((size_t)qwant * 8);
+    P.qvert.ensure((size_t)qwant * 16);
+    P.qcap = qwant;
+  }
+  uint64_t rows_per_chunk = P.sparse ? nrows_sp : rows;
+  const uint64_t rows_total = P.sparse ? nrows_sp : rows;
+  if (!P.sparse && cand > P.qcap) rows_per_chunk = std::max<uint64_t>(1, P.qcap / (uint64_t)n);
+  uint64_t app_cap = 0;
+  uint64_t* app_ptr = nullptr;
+  if (P.opt.index_pairs) {
+    app_cap = std::max<uint64_t>(bound, 1);
+    P.app_pairs.ensure((size_t)app_cap * 16);
+    app_ptr = P.app_pairs.as<uint64_t>();
+  }
+  ST.mark("  allocate queue");
+  vr::DimCounters* ctr = P.ctrs.as<vr::DimCounters>() + d;
+  CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(vr::DimCounters), st));
+  float t_enum = 0, t_res = 0;
+  uint64_t resid_count = 0;
+  for (uint64_t rb = 0; rb < rows_total; rb += rows_per_chunk) {
+    const uint64_t re = std::min(rows_total, rb + rows_per_chunk);
+    const uint64_t chunk_cand = P.sparse ? std::max<uint64_t>(bound, 1) : std::min<uint64_t>(cand, (re - rb) * (uint64_t)n);
+    // residual capacity: what is there plus everything this chunk could add
+    if (P.rcap < resid_count + chunk_cand || !P.resid.p) {
+      const uint64_t ncap = std::max<uint64_t>(resid_count + chunk_cand, 1024);
+      DevBuf nb;
+      nb.ensure((size_t)ncap * 8);
+      if (resid_count) CUDA_TRY(cudaMemcpyAsync(nb.p, P.resid.p, resid_count * 8, cudaMemcpyDeviceToDevice, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      std::swap(P.resid.p, nb.p);
+      std::swap(P.resid.bytes, nb.bytes);
+      P.rcap = ncap;
+    }
+    vr::HotBuffers B{P.queue.as<uint64_t>(), P.qvert.as<uint4>(), P.qcap, P.resid.as<uint64_t>(), P.rcap,
+                     P.clr_of(d), clr_next, dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, ctr, app_ptr, app_cap};
+    vr::SparseRows SR = P.sparse_rows(d, ctr);
+    p.row_begin = rb;
+    p.row_end = re;
+    CUDA_TRY(cudaMemsetAsync(&ctr->row_next, 0, 8, st));
+    CUDA_TRY(cudaMemsetAsync(&ctr->queued, 0, 8, st));
+    CUDA_TRY(cudaEventRecord(P.ev[2], st));
+    if (P.sparse) vr::launch_enumerate_sparse(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, SR, st, &P.launches);
+    else vr::launch_enumerate(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, st, &P.launches);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(P.ev[3], st));
+    unsigned long long q = 0;
+    CUDA_TRY(cudaMemcpyAsync(&q, &ctr->queued, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (q > P.qcap) throw VrError(VR_ECAPACITY, "apparent-phase queue overflow");
+    float x = 0;
+    cudaEventElapsedTime(&x, P.ev[2], P.ev[3]);
+    t_enum += x;
+    CUDA_TRY(cudaEventRecord(P.ev[4], st));
+    if (P.sparse) vr::launch_resolve_sparse(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, SR, q, st, &P.launches);
+    else vr::launch_resolve(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, q, st, &P.launches);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(P.ev[5], st));
+    unsigned long long rc = 0;
+    CUDA_TRY(cudaMemcpyAsync(&rc, &ctr->residual, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    cudaEventElapsedTime(&x, P.ev[4], P.ev[5]);
+    t_res += x;
+    if (rc > P.rcap) throw VrError(VR_ECAPACITY, "residual list overflow");
+    resid_count = rc;
+    dr.chunks.push_back(Chunk{rb, re, q});
+  }
+  if (P.sparse && d < D) {
+    unsigned long long ro = 0;
+    CUDA_TRY(cudaMemcpyAsync(&ro, &ctr->rows_out, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (ro > P.rows_cap[(size_t)d]) throw VrError(VR_ECAPACITY, "survivor list overflow");
+    P.rows_count[(size_t)d] = ro;
+  }
+  dr.residual = resid_count;
+  ST.mark("  enumerate + resolve");
+  // a4: sort the residual columns into coboundary order
+  P.resid_alt.ensure(std::max<uint64_t>(resid_count, 1) * 8);
+  size_t stmp = vr::radix_sort_temp_bytes(std::max<uint64_t>(resid_count, 1));
+  if (P.sort_tmp.bytes < stmp) P.sort_tmp.ensure(stmp);
+  CUDA_TRY(cudaEventRecord(P.ev[6], st));
+  P.local_sorted = vr::radix_sort_u64(P.resid.as<uint64_t>(), P.resid_alt.as<uint64_t>(), resid_count, 0, dr.sort_bits,
+                                      P.sort_tmp.p, st, &P.launches);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(P.ev[7], st));
+  vr::DimCounters hc{};
+  CUDA_TRY(cudaMemcpyAsync(&hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  float t_sort = 0;
+  cudaEventElapsedTime(&t_sort, P.ev[6], P.ev[7]);
+  if (P.opt.index_pairs && hc.app_pairs) {
+    std::vector<uint64_t> app_h((size_t)std::min<uint64_t>(hc.app_pairs, app_cap) * 2);
+    CUDA_TRY(cudaMemcpy(app_h.data(), app_ptr, app_h.size() * 8, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i + 1 < app_h.size(); i += 2) R->ipairs[(size_t)d].push_back(vr_index_pair{app_h[i], app_h[i + 1]});
+  }
+  ST.mark("  sort");
+  stt.survivors = (int64_t)hc.survivors;
+  stt.apparent = (int64_t)(hc.apparent1 + hc.apparent2);
+  stt.cleared = (int64_t)hc.cleared;
+  stt.scanned = (int64_t)(hc.scanned + hc.scanned2);
+  stt.queued = 0;
+  for (auto& c : dr.chunks) stt.queued += (int64_t)c.queued;
+  stt.ms_enumerate = t_enum;
+  stt.ms_resolve = t_res;
+  stt.ms_sort = t_sort;
+  P.work_candidates += (double)cand;
+  P.work_scanned += (double)hc.scanned;
+  P.work_scanned2 += (double)hc.scanned2;
+  P.work_rank_ops += (double)(d + 1) * ((double)cand + (double)hc.scanned);
+  P.work_rank_ops2 += (double)(d + 1) * (double)hc.scanned2;
+  P.survivors_total += stt.survivors;
+  P.apparent_total += stt.apparent;
+  return resid_count;
+}
 
-  ST.mark("dims done");
-  // ---------------- result
-  if (R) {
-    for (int d = 0; d <= D; ++d) {
-      const vr::HostPairs& h = hp[(size_t)d];
-      vr_stats& s = R->stats[(size_t)d];
-      auto& out = R->pairs[(size_t)d];
-      for (size_t i = 0; i < h.birth.size(); ++i) {
-        const bool ess = std::isinf(h.death[i]);
-        if (ess) ++s.essential;
-        else {
-          ++s.pairs_all;
-          if (h.birth[i] < h.death[i]) ++s.pairs_positive;
-        }
-        if (ess || h.birth[i] < h.death[i] || P.opt.include_zero) out.push_back(vr_pair{h.birth[i], h.death[i]});
-        if (P.opt.index_pairs) R->ipairs[(size_t)d].push_back(vr_index_pair{h.birth_cidx[i], h.death_cidx[i]});
-      }
-      if (d >= 1) s.pairs_all += s.apparent;  // apparent pairs: zero-length, counted only
-      std::sort(out.begin(), out.end(), [](const vr_pair& a, const vr_pair& b) {
-        return a.birth < b.birth || (a.birth == b.birth && a.death < b.death);
-      });
+// Host residual of dimension d on the sorted residual columns (all ranks' columns when
+// distributed); deaths -> the clearing input of dimension d+1.
+void stage_dim_finish(vr_plan& P, int d, const uint64_t* keys, uint64_t nkeys) {
+  SectionTimer ST;
+  vr_result* R = P.R.get();
+  const int D = P.D;
+  cudaStream_t st = P.st;
+  DimRun& dr = P.dims[(size_t)d];
+  vr_stats& stt = R->stats[(size_t)d];
+  if (!dr.active) {
+    P.deaths.clear();
+    if (d < D) {
+      P.dims[(size_t)d + 1].ndeaths_in = 0;
     }
+    return;
   }
+  auto tr = std::chrono::steady_clock::now();
+  vr::ResidualStats rst;
+  vr::residual_reduce(P.M, d, P.maxr, dr.p.cbits, keys, nkeys, P.opt.residual_mode, P.hp[(size_t)d], P.deaths, rst);
+  stt.ms_residual = ms_since(tr);
+  ST.mark("  residual (host)");
+  if (const char* dump = std::getenv("VR_DUMP_RESIDUAL")) {
+    std::vector<uint64_t> kv(keys, keys + nkeys);
+    dump_residual(dump, P.M, d, P.maxr, dr.p.cbits, kv);
+  }
+  // deaths of dimension d -> clearing input of dimension d+1
+  if (d < D) {
+    auto tx = std::chrono::steady_clock::now();
+    DimRun& nx = P.dims[(size_t)d + 1];
+    nx.ndeaths_in = (int64_t)P.deaths.size();
+    nx.deaths_in.ensure(std::max<size_t>(P.deaths.size(), 1) * 8);
+    if (!P.deaths.empty())
+      CUDA_TRY(cudaMemcpyAsync(nx.deaths_in.p, P.deaths.data(), P.deaths.size() * 8, cudaMemcpyHostToDevice, st));
+    if (P.clr_of(d + 1)) vr::launch_set_bits(nx.deaths_in.as<uint64_t>(), nx.ndeaths_in, P.clr_of(d + 1), st, &P.launches);
+    stt.ms_transfer += ms_since(tx);
+  }
+  stt.residual_columns = (int64_t)nkeys;
+  stt.emergent = rst.emergent;
+  P.residual_total += (int64_t)nkeys;
+}
+
+void stage_result(vr_plan& P) {
+  vr_result* R = P.R.get();
+  for (int d = 0; d <= P.D; ++d) {
+    const vr::HostPairs& h = P.hp[(size_t)d];
+    vr_stats& s = R->stats[(size_t)d];
+    auto& out = R->pairs[(size_t)d];
+    out.clear();
+    s.essential = s.pairs_all = s.pairs_positive = 0;
+    for (size_t i = 0; i < h.birth.size(); ++i) {
+      const bool ess = std::isinf(h.death[i]);
+      if (ess) ++s.essential;
+      else {
+        ++s.pairs_all;
+        if (h.birth[i] < h.death[i]) ++s.pairs_positive;
+      }
+      if (ess || h.birth[i] < h.death[i] || P.opt.include_zero) out.push_back(vr_pair{h.birth[i], h.death[i]});
+      if (P.opt.index_pairs) R->ipairs[(size_t)d].push_back(vr_index_pair{h.birth_cidx[i], h.death_cidx[i]});
+    }
+    if (d >= 1) s.pairs_all += s.apparent;  // apparent pairs: zero-length, counted only
+    std::sort(out.begin(), out.end(), [](const vr_pair& a, const vr_pair& b) {
+      return a.birth < b.birth || (a.birth == b.birth && a.death < b.death);
+    });
+  }
+}
+
+void run_full(vr_plan& P) {
+  stage_setup(P);
+  for (int d = 1; d <= P.D; ++d) {
+    const uint64_t nk = stage_dim_local(P, d);
+    std::vector<uint64_t> hkeys((size_t)nk);
+    auto tx = std::chrono::steady_clock::now();
+    if (nk) CUDA_TRY(cudaMemcpy(hkeys.data(), P.local_sorted, nk * 8, cudaMemcpyDeviceToHost));
+    P.R->stats[(size_t)d].ms_transfer += ms_since(tx);
+    stage_dim_finish(P, d, hkeys.data(), nk);
+  }
+  stage_result(P);
 }
 
 // Re-launch the GPU hot path of every dimension with the recorded sizes (no host sync).
@@ -626,9 +679,7 @@ void replay(vr_plan& P) {
     }
     return v[(size_t)used[stage]++];
   };
-  auto clr_of = [&](int d) -> uint32_t* {
-    return (d >= 1 && d <= P.D && P.dims[(size_t)d].clr_words) ? P.dims[(size_t)d].clr.as<uint32_t>() : nullptr;
-  };
+  auto clr_of = [&](int d) -> uint32_t* { return P.clr_of(d); };
   uint64_t* sorted = nullptr;
   {
     auto& e = ev(0);
@@ -660,15 +711,7 @@ void replay(vr_plan& P) {
     for (const Chunk& c : dr.chunks) {
       vr::HotBuffers B{P.queue.as<uint64_t>(), P.qvert.as<uint4>(), P.qcap, P.resid.as<uint64_t>(), P.rcap,
                        clr_of(d), clr_next, dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, ctr, nullptr, 0};
-      vr::SparseRows SR{};
-      if (P.sparse) {
-        SR.adj_off = P.adj_off.as<uint32_t>();
-        SR.adj = P.adj.as<uint16_t>();
-        SR.rows_in = d == 1 ? nullptr : P.rows[(size_t)d - 1].as<uint4>();
-        SR.rows_out = d < P.D ? P.rows[(size_t)d].as<uint4>() : nullptr;
-        SR.rows_out_cap = d < P.D ? P.rows_cap[(size_t)d] : 0;
-        SR.rows_out_count = &ctr->rows_out;
-      }
+      vr::SparseRows SR = P.sparse_rows(d, ctr);
       p.row_begin = c.row_begin;
       p.row_end = c.row_end;
       auto& e2 = ev(1);
@@ -732,9 +775,8 @@ int vr_barcodes_device(const float* d_lt, int64_t n, int32_t max_dim, float thre
     vr_plan P;
     P.n = n; P.D = max_dim; P.threshold = threshold; P.opt = default_options(opt);
     P.st = (cudaStream_t)stream; P.d_lt = d_lt;
-    std::unique_ptr<vr_result> R(new vr_result());
-    run_full(P, R.get());
-    *out = R.release();
+    run_full(P);
+    *out = P.R.release();
   });
 }
 
@@ -758,10 +800,10 @@ int vr_barcodes(const float* lt, int64_t n, int32_t max_dim, float threshold, co
     if (bytes) CUDA_TRY(cudaMemcpyAsync(P->lt_copy.p, lt, bytes, cudaMemcpyHostToDevice, P->st));
     P->d_lt = P->lt_copy.as<float>();
     ST.mark("H2D input");
-    std::unique_ptr<vr_result> R(new vr_result());
-    run_full(*P, R.get());
+    run_full(*P);
     CUDA_TRY(cudaStreamSynchronize(P->st));
     ST.mark("run_full");
+    std::unique_ptr<vr_result> R(std::move(P->R));
     P.reset();
     ST.mark("release device buffers");
     *out = R.release();
@@ -805,10 +847,11 @@ int vr_plan_create(const float* d_lt, int64_t n, int32_t max_dim, float threshol
     P->n = n; P->D = max_dim; P->threshold = threshold; P->opt = default_options(opt);
     P->opt.index_pairs = 0;
     P->st = (cudaStream_t)stream; P->d_lt = d_lt;
-    std::unique_ptr<vr_result> R(new vr_result());
-    run_full(*P, R.get());
+    run_full(*P);
     CUDA_TRY(cudaStreamSynchronize(P->st));
     P->launches = 0;
+    std::unique_ptr<vr_result> R(std::move(P->R));
+    P->R.reset(new vr_result(*R));
     *plan = P.release();
     if (out) *out = R.release();
   });
@@ -880,6 +923,111 @@ int vr_radix_sort_u64(uint64_t* keys, int64_t n, int32_t begin_bit, int32_t end_
     uint64_t* r = vr::radix_sort_u64(a.as<uint64_t>(), b.as<uint64_t>(), (size_t)n, begin_bit, end_bit, t.p, 0, &launches);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpy(keys, r, (size_t)n * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+// ---------------------------------------------------------------- distributed stepping
+int vr_dist_begin(const float* d_lt, int64_t n, int32_t max_dim, float threshold, const vr_options* opt, void* stream,
+                  int32_t rank, int32_t world, vr_plan** plan) {
+  if (plan) *plan = nullptr;
+  return guarded([&] {
+    if (!plan) throw VrError(VR_EINVAL, "plan is NULL");
+    if (world < 1 || rank < 0 || rank >= world) throw VrError(VR_EINVAL, "bad rank / world");
+    check_args(d_lt, n, max_dim, threshold);
+    std::unique_ptr<vr_plan> P(new vr_plan());
+    P->n = n; P->D = max_dim; P->threshold = threshold; P->opt = default_options(opt);
+    P->opt.index_pairs = 0;
+    P->st = (cudaStream_t)stream; P->d_lt = d_lt;
+    P->rank_id = rank;
+    P->world = world;
+    stage_setup(*P);
+    *plan = P.release();
+  });
+}
+
+int vr_dist_dim_local(vr_plan* P, int32_t d, int64_t* nkeys, int64_t* next_bitmap_words) {
+  return guarded([&] {
+    if (!P || d < 1 || d > P->D) throw VrError(VR_EINVAL, "bad plan / dimension");
+    const uint64_t nk = stage_dim_local(*P, d);
+    if (nkeys) *nkeys = (int64_t)nk;
+    if (next_bitmap_words) *next_bitmap_words = P->clr_of(d + 1) ? (int64_t)P->dims[(size_t)d + 1].clr_words : 0;
+  });
+}
+
+int vr_dist_copy_keys(vr_plan* P, int32_t d, uint64_t* dst) {
+  return guarded([&] {
+    if (!P || d < 1 || d > P->D) throw VrError(VR_EINVAL, "bad plan / dimension");
+    const uint64_t nk = P->dims[(size_t)d].residual;
+    if (nk && P->local_sorted)
+      CUDA_TRY(cudaMemcpyAsync(dst, P->local_sorted, nk * 8, cudaMemcpyDeviceToDevice, P->st));
+    CUDA_TRY(cudaStreamSynchronize(P->st));
+  });
+}
+
+int vr_dist_bitmap(vr_plan* P, int32_t d, uint32_t* buf, int32_t direction) {
+  return guarded([&] {
+    if (!P || d < 1) throw VrError(VR_EINVAL, "bad plan / dimension");
+    uint32_t* bm = P->clr_of(d);
+    if (!bm) return;
+    const size_t bytes = P->dims[(size_t)d].clr_words * 4;
+    if (direction == 0) CUDA_TRY(cudaMemcpyAsync(buf, bm, bytes, cudaMemcpyDeviceToDevice, P->st));
+    else CUDA_TRY(cudaMemcpyAsync(bm, buf, bytes, cudaMemcpyDeviceToDevice, P->st));
+    CUDA_TRY(cudaStreamSynchronize(P->st));
+  });
+}
+
+int vr_dist_counters(vr_plan* P, int32_t d, int64_t out[6]) {
+  return guarded([&] {
+    if (!P || d < 1 || d > P->D || !out) throw VrError(VR_EINVAL, "bad arguments");
+    const vr_stats& s = P->R->stats[(size_t)d];
+    out[0] = s.survivors; out[1] = s.apparent; out[2] = s.cleared; out[3] = s.queued; out[4] = s.scanned;
+    out[5] = (int64_t)P->dims[(size_t)d].residual;
+  });
+}
+
+int vr_dist_dim_finish(vr_plan* P, int32_t d, const uint64_t* keys, int64_t nkeys) {
+  return guarded([&] {
+    if (!P || d < 1 || d > P->D || nkeys < 0 || (nkeys && !keys)) throw VrError(VR_EINVAL, "bad arguments");
+    stage_dim_finish(*P, d, keys, (uint64_t)nkeys);
+  });
+}
+
+int vr_dist_end(vr_plan* P, vr_result** out) {
+  if (out) *out = nullptr;
+  return guarded([&] {
+    if (!P || !out) throw VrError(VR_EINVAL, "bad arguments");
+    stage_result(*P);
+    CUDA_TRY(cudaStreamSynchronize(P->st));
+    *out = new vr_result(*P->R);
+  });
+}
+
+// ---------------------------------------------------------------- host-only residual
+int vr_host_residual(const uint32_t* rank, const float* values, int64_t nvalues, int64_t n, int32_t d, uint32_t maxr,
+                     int32_t cbits, const uint64_t* keys, int64_t nkeys, int32_t mode, float* birth, float* death,
+                     uint64_t* birth_cidx, uint64_t* death_cidx, int64_t* emergent) {
+  return guarded([&] {
+    if (!rank || !values || n < 2 || d < 1 || d > VR_MAX_DIM || nkeys < 0 || (nkeys && !keys))
+      throw VrError(VR_EINVAL, "vr_host_residual: bad arguments");
+    vr::HostMatrix M;
+    M.n = n;
+    M.kmax = d + 2;
+    M.rank.assign(rank, rank + (size_t)n * (size_t)n);
+    M.value.assign(values, values + nvalues);
+    M.binom.resize((size_t)(M.kmax + 1) * (size_t)(n + 1));
+    for (int k = 0; k <= M.kmax; ++k)
+      for (int64_t v = 0; v <= n; ++v) M.binom[(size_t)k * (size_t)(n + 1) + (size_t)v] = binom_host((uint64_t)v, (uint64_t)k);
+    vr::HostPairs hp;
+    std::vector<uint64_t> deaths;
+    vr::ResidualStats st;
+    vr::residual_reduce(M, d, maxr, cbits, keys, (uint64_t)nkeys, mode, hp, deaths, st);
+    for (size_t i = 0; i < hp.birth.size(); ++i) {
+      birth[i] = hp.birth[i];
+      death[i] = hp.death[i];
+      birth_cidx[i] = hp.birth_cidx[i];
+      death_cidx[i] = hp.death_cidx[i];
+    }
+    if (emergent) *emergent = st.emergent;
   });
 }
 

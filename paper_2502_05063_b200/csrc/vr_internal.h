@@ -36,6 +36,8 @@ struct DimParams {
   int steps;           // phase-1 cofacet steps
   int grab;            // prefix rows per atomic grab in k_enumerate
   int variant;         // phase-1 scan loop variant (0: vote per vertex, 1: per 4 vertices)
+  int shard_rank = 0;  // interleaved row shard: rows r with (row_end-1-r) % shard_world == shard_rank
+  int shard_world = 1;
   uint64_t row_begin, row_end;  // prefix rows [row_begin, row_end) of the d-simplices
 };
 struct DimCounters {   // device counters (unsigned long long each)

@@ -8,6 +8,7 @@ included) is unique for the §5.1.4 refinement and must match too (SURVEY.md §8
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -286,3 +287,71 @@ def test_config5_dim3_invariants(c5_lower_tri):
         assert s["survivors"] == s["apparent"] + s["cleared"] + s["residual_columns"]
     # two O(3) components exactly 2.0 apart (> t = 1.4): beta_0 = 2 essential classes
     assert E[0] == 2
+
+
+# ------------------------------------------------------------------ multi-GPU shards, emulated in one process
+def _emulated_ranks(lt, n, D, world, **opts):
+    """Runs `world` shards of the real device stage one after another on this GPU and
+    performs the two exchanges in-process (sum of bitmaps, merge of keys)."""
+    torch = pytest.importorskip("torch")
+    from paper_2502_05063_b200.dist import LibBackend, merge_sorted_keys
+    t = torch.from_numpy(np.ascontiguousarray(lt)).cuda()
+    bes = [LibBackend(t, n, D, math.inf, r, world, **opts) for r in range(world)]
+    try:
+        tot = {}
+        for d in range(1, D + 1):
+            outs = [be.dim_local(d) for be in bes]
+            words = outs[0][1]
+            if words:
+                s = sum(be.bitmap_out(d + 1, words).to(torch.int64) for be in bes)
+                s = (s & 0xFFFFFFFF).to(torch.int64)
+                s = torch.where(s >= 2**31, s - 2**32, s).to(torch.int32)
+                for be in bes:
+                    be.bitmap_in(d + 1, s.clone())
+            parts = [be.local_keys(d, nk).cpu().numpy().view(np.uint64) for be, (nk, _) in zip(bes, outs)]
+            merged = merge_sorted_keys(parts)
+            for be in bes:
+                be.dim_finish(d, merged)
+            tot[d] = np.sum([be.counters(d) for be in bes], axis=0)
+        return [be.end() for be in bes], tot
+    finally:
+        for be in bes:
+            be.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("sparse", [1, 2])
+@pytest.mark.parametrize("name,m,D", [("c2_s3_192", 60, 3), ("c3_trefoil1000", 150, 2)])
+def test_emulated_shards_match_single_gpu(world, sparse, name, m, D):
+    cfg = G.CONFIGS[name]
+    lt = cfg.lower_tri(m)
+    ref = vr.barcodes(lt, m, D, sparse_mode=sparse)
+    bcs, tot = _emulated_ranks(lt, m, D, world, sparse_mode=sparse)
+    for bc in bcs:
+        for d in range(D + 1):
+            assert np.array_equal(bc.pairs[d], ref.pairs[d]), d
+    for d in range(1, D + 1):
+        assert tot[d][0] == ref.stats[d]["survivors"]
+        assert tot[d][1] == ref.stats[d]["apparent"]
+        assert tot[d][2] == ref.stats[d]["cleared"]
+        assert tot[d][5] == ref.stats[d]["residual_columns"]
+
+
+def test_sharded_single_rank_process_group():
+    torch = pytest.importorskip("torch")
+    import socket
+    import torch.distributed as tdist
+    from paper_2502_05063_b200.dist import barcodes_sharded
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    tdist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        cfg = G.CONFIGS["c4a_sierpinski512"]
+        lt = cfg.lower_tri(120)
+        ref = vr.barcodes(lt, 120, 2)
+        got = barcodes_sharded(torch.from_numpy(lt).cuda(), 120, 2)
+        for d in range(3):
+            assert np.array_equal(got.pairs[d], ref.pairs[d])
+            assert got.stats[d]["pairs_all"] == ref.stats[d]["pairs_all"]
+    finally:
+        tdist.destroy_process_group()
