@@ -14,8 +14,10 @@ Metric (BASELINE.json `metric`): "VR barcode wall-time (s) and hot-path simplice
             seconds per barcode ("wall_s").
 Default workload: BASELINE.json configs[1] (n=192 points on S^3, max_dim=3, t = R).
 
-Multi-GPU (torchrun): every rank runs its own replica of the workload on its GPU (weak
-scaling); value = all ranks' survivors / max-over-ranks time.  --impl reference times the
+Multi-GPU (torchrun): the workload is sharded over the ranks (strong scaling): every rank
+runs its shard of each dimension's hot path, with the two exchanges of SURVEY.md §8(e)
+per dimension (clearing-bitmap SUM all-reduce, all-gather of the sorted residual keys) over
+NCCL; value = the workload's survivors / max-over-ranks step time.  --impl reference times the
 CPU oracle (explicit boundary matrix + Alg 2) on a bounded sample of the same workload.
 """
 from __future__ import annotations
@@ -53,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sample", type=int, default=None, help="oracle sample size (points)")
     ap.add_argument("--no-target", action="store_true", help="skip the north-star target run (config 5, max_dim 2)")
+    ap.add_argument("--sharded", action="store_true", help="use the sharded (multi-GPU) path even at N=1")
     return ap.parse_args()
 
 
@@ -178,16 +181,26 @@ def run_ours(args, rank, world, local_rank):
     n = cfg.n
     dev_lt = torch.from_numpy(lt_host).cuda()
     stream = torch.cuda.current_stream()
-    plan = vr.Plan(dev_lt, n, D, cfg.threshold, stream=stream)
-    survivors = plan.survivors
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    if world == 1 and not args.sharded:
+        plan = vr.Plan(dev_lt, n, D, cfg.threshold, stream=stream)
+        survivors = plan.survivors
+        step_fn = plan.replay
+        a_ref = (sum(plan.result.stats[d]["apparent"] for d in range(1, D + 1)),
+                 sum(plan.result.stats[d]["residual_columns"] for d in range(1, D + 1)))
+    else:
+        # shards of every dimension's hot path + the two exchanges per dimension (NCCL)
+        from paper_2502_05063_b200.dist import ShardedHotPath
+        plan = ShardedHotPath(dev_lt, n, D, cfg.threshold)
+        survivors = plan.survivors_total
+        step_fn = plan.step
+        a_ref = None
 
     for _ in range(args.warmup):
-        plan.replay()
+        step_fn()
     torch.cuda.synchronize()
-    a_ref = (sum(plan.result.stats[d]["apparent"] for d in range(1, D + 1)),
-             sum(plan.result.stats[d]["residual_columns"] for d in range(1, D + 1)))
-    assert plan.check() == a_ref, "replay did not reproduce the apparent/residual counts"
+    if a_ref is not None:
+        assert plan.check() == a_ref, "replay did not reproduce the apparent/residual counts"
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -200,30 +213,41 @@ def run_ours(args, rank, world, local_rank):
         for i in range(args.steps):
             flush.zero_()
             starts[i].record(stream)
-            launches += plan.replay()
+            launches += step_fn()
             ends[i].record(stream)
-            tm = plan.timing()  # synchronizes; reads this step's stage events
-            for k in stage:
-                stage[k] += tm[k]
+            if a_ref is not None:
+                tm = plan.timing()  # synchronizes; reads this step's stage events
+                for k in stage:
+                    stage[k] += tm[k]
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = sum(step_ms)
-    assert plan.check() == a_ref
+    if a_ref is not None:
+        assert plan.check() == a_ref
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms_max = float(t.item())
     ms_per_step = total_ms_max / args.steps
-    value = survivors * world / (ms_per_step / 1000.0)
+    value = survivors / (ms_per_step / 1000.0)  # survivors of the whole (sharded) workload
 
-    # ---- e2e: the public host-pointer call, H2D and D2H inside the timed region
+    # ---- e2e: the public call, H2D of the input and D2H of the barcode in the timed region
     e2e_times, pairs_bytes = [], 0
-    vr.barcodes(lt_host, n, D, cfg.threshold)  # warm
+
+    def e2e_call():
+        if a_ref is not None:
+            return vr.barcodes(lt_host, n, D, cfg.threshold)
+        from paper_2502_05063_b200.dist import barcodes_sharded
+        return barcodes_sharded(torch.from_numpy(lt_host).cuda(), n, D, cfg.threshold)
+
+    e2e_call()  # warm
     for _ in range(args.e2e_steps):
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        bc = vr.barcodes(lt_host, n, D, cfg.threshold)
+        bc = e2e_call()
         e2e_times.append(time.perf_counter() - t0)
         pairs_bytes = sum(p.nbytes for p in bc.pairs)
     e2e_s = statistics.median(e2e_times)
@@ -235,7 +259,10 @@ def run_ours(args, rank, world, local_rank):
 
     if rank != 0:
         return
-    tm = plan.timing()
+    if a_ref is None:  # per-stage device times are reported by the single-GPU replay only
+        tm = {"rank_ops_enumerate": 0.0, "rank_ops_resolve": 0.0}
+    else:
+        tm = plan.timing()
     per = {k: stage[k] / args.steps for k in stage}
     # roofline of the dominant kernel: k_enumerate is ALU-bound —
     # algorithmic work = rank comparisons of the method, sum_d (d+1)*(candidates_d + scanned_d);
@@ -265,11 +292,12 @@ def run_ours(args, rank, world, local_rank):
                            "work = rank comparisons (d+1 per candidate and per scanned cofacet vertex)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "u32", "data": "synthetic",
-        "config": config_obj(cfg, D, {"survivors": survivors, "parallelism": f"replica x{world}"}),
+        "config": config_obj(cfg, D, {"survivors": survivors,
+                                      "parallelism": "single GPU" if a_ref is not None else f"row shards x{world}"}),
         "wall_s": e2e_s,
-        "e2e": {"value": survivors * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(lt_host.nbytes),
+        "e2e": {"value": survivors / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(lt_host.nbytes),
                 "d2h_bytes_per_step": int(pairs_bytes), "wall_s_per_barcode": e2e_s},
         "stages_ms": per,
         "residual_ms": sum(st[d]["ms_residual"] for d in range(1, D + 1)),
@@ -280,7 +308,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
-    if not args.no_target:
+    if not args.no_target and world == 1:
         # BASELINE.json north_star target: "the dim-2 n=4096 workload under 1 s on one B200"
         # (reading A22: config 5's o3-shaped cloud at max_dim = 2, t = 1.4), end to end
         # through the public host-pointer call
@@ -311,13 +339,15 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        dist.init_process_group("nccl", rank=rank, world_size=world)
     run_ours(args, rank, world, local_rank)
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch.distributed as dist
         dist.destroy_process_group()
 

@@ -192,6 +192,15 @@ int vr_dist_counters(vr_plan* plan, int32_t d, int64_t out[6]);
 int vr_dist_dim_finish(vr_plan* plan, int32_t d, const uint64_t* merged_keys_host, int64_t nkeys);
 /* assembles the barcode (every rank holds the same pairs); free the plan with vr_plan_free */
 int vr_dist_end(vr_plan* plan, vr_result** out);
+/* device-only replay of a finished distributed plan (benchmarking, asynchronous on the
+ * plan's stream): tables; dimension d's local kernels + local sort; the residual-death
+ * bits of dimension d into the bitmap of d+1 (call after exchange A of dimension d).
+ * vr_dist_bitmap directions 2/3 and vr_dist_copy_keys_async are the asynchronous copies. */
+int vr_dist_replay_tables(vr_plan* plan);
+int vr_dist_replay_dim(vr_plan* plan, int32_t d);
+int vr_dist_replay_deaths(vr_plan* plan, int32_t d);
+int vr_dist_copy_keys_async(vr_plan* plan, int32_t d, uint64_t* dst_device);
+int64_t vr_plan_launches(const vr_plan* plan); /* kernels launched through this plan so far */
 
 /* ----------------------------------------------------------------------------------
  * Component entry (tests, no GPU needed): the library's host residual reduction of

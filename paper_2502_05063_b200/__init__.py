@@ -97,6 +97,11 @@ def load() -> ctypes.CDLL:
         "vr_dist_counters": (ctypes.c_int, [vp, i32, ctypes.POINTER(i64)]),
         "vr_dist_dim_finish": (ctypes.c_int, [vp, i32, vp, i64]),
         "vr_dist_end": (ctypes.c_int, [vp, ctypes.POINTER(vp)]),
+        "vr_dist_replay_tables": (ctypes.c_int, [vp]),
+        "vr_dist_replay_dim": (ctypes.c_int, [vp, i32]),
+        "vr_dist_replay_deaths": (ctypes.c_int, [vp, i32]),
+        "vr_dist_copy_keys_async": (ctypes.c_int, [vp, i32, vp]),
+        "vr_plan_launches": (i64, [vp]),
         "vr_host_residual": (ctypes.c_int, [vp, vp, i64, i64, i32, ctypes.c_uint32, i32, vp, i64, i32, vp, vp, vp, vp,
                                             ctypes.POINTER(i64)]),
     }

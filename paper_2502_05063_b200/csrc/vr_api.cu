@@ -970,9 +970,18 @@ int vr_dist_bitmap(vr_plan* P, int32_t d, uint32_t* buf, int32_t direction) {
     uint32_t* bm = P->clr_of(d);
     if (!bm) return;
     const size_t bytes = P->dims[(size_t)d].clr_words * 4;
-    if (direction == 0) CUDA_TRY(cudaMemcpyAsync(buf, bm, bytes, cudaMemcpyDeviceToDevice, P->st));
+    // direction 0/1: copy out/in and synchronize; 2/3: the same, asynchronous on the stream
+    if (direction == 0 || direction == 2) CUDA_TRY(cudaMemcpyAsync(buf, bm, bytes, cudaMemcpyDeviceToDevice, P->st));
     else CUDA_TRY(cudaMemcpyAsync(bm, buf, bytes, cudaMemcpyDeviceToDevice, P->st));
-    CUDA_TRY(cudaStreamSynchronize(P->st));
+    if (direction < 2) CUDA_TRY(cudaStreamSynchronize(P->st));
+  });
+}
+
+int vr_dist_copy_keys_async(vr_plan* P, int32_t d, uint64_t* dst) {
+  return guarded([&] {
+    if (!P || d < 1 || d > P->D) throw VrError(VR_EINVAL, "bad plan / dimension");
+    const uint64_t nk = P->dims[(size_t)d].residual;
+    if (nk && P->local_sorted) CUDA_TRY(cudaMemcpyAsync(dst, P->local_sorted, nk * 8, cudaMemcpyDeviceToDevice, P->st));
   });
 }
 
@@ -1001,6 +1010,71 @@ int vr_dist_end(vr_plan* P, vr_result** out) {
     *out = new vr_result(*P->R);
   });
 }
+
+// replay pieces of a distributed plan (after one full distributed run): tables, one
+// dimension's local kernels (bitmap of d+1 zeroed, then this rank's apparent cofacets),
+// and the residual-death bits of dimension d into the bitmap of d+1 (after exchange A)
+int vr_dist_replay_tables(vr_plan* P) {
+  return guarded([&] {
+    if (!P) throw VrError(VR_EINVAL, "plan is NULL");
+    uint64_t* sorted = nullptr;
+    vr::launch_tables(P->d_lt, P->n, P->threshold, P->keys.as<uint64_t>(), P->alt.as<uint64_t>(),
+                      P->rowmax.as<uint32_t>(), P->sort_tmp.p, P->rank.as<uint32_t>(), P->tout.as<vr::TablesOut>(),
+                      &sorted, P->st, &P->launches);
+    if (P->sparse) {
+      cudaMemsetAsync(P->deg.p, 0, ((size_t)P->n + 1) * 4, P->st);
+      vr::launch_adjacency(P->rank.as<uint32_t>(), (int)P->n, P->deg.as<uint32_t>(), P->deg_below.as<uint32_t>(),
+                           P->adj_off.as<uint32_t>(), P->adj.as<uint16_t>(), P->scan_tmp2.p, P->st, &P->launches);
+    }
+    if (P->D >= 1 && P->clr_of(1)) {
+      cudaMemsetAsync(P->clr_of(1), 0, P->dims[1].clr_words * 4, P->st);
+      vr::launch_set_bits(P->dims[1].deaths_in.as<uint64_t>(), P->dims[1].ndeaths_in, P->clr_of(1), P->st, &P->launches);
+    }
+    CUDA_TRY(cudaGetLastError());
+  });
+}
+
+int vr_dist_replay_dim(vr_plan* P, int32_t d) {
+  return guarded([&] {
+    if (!P || d < 1 || d > P->D) throw VrError(VR_EINVAL, "bad plan / dimension");
+    DimRun& dr = P->dims[(size_t)d];
+    if (dr.chunks.empty()) return;
+    cudaStream_t st = P->st;
+    vr::DimCounters* ctr = P->ctrs.as<vr::DimCounters>() + d;
+    uint32_t* clr_next = P->clr_of(d + 1);
+    cudaMemsetAsync(ctr, 0, sizeof(vr::DimCounters), st);
+    if (clr_next) cudaMemsetAsync(clr_next, 0, P->dims[(size_t)d + 1].clr_words * 4, st);
+    vr::DimParams p = dr.p;
+    for (const Chunk& c : dr.chunks) {
+      vr::HotBuffers B{P->queue.as<uint64_t>(), P->qvert.as<uint4>(), P->qcap, P->resid.as<uint64_t>(), P->rcap,
+                       P->clr_of(d), clr_next, dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, ctr, nullptr, 0};
+      vr::SparseRows SR = P->sparse_rows(d, ctr);
+      p.row_begin = c.row_begin;
+      p.row_end = c.row_end;
+      cudaMemsetAsync(&ctr->row_next, 0, 8, st);
+      cudaMemsetAsync(&ctr->queued, 0, 8, st);
+      if (P->sparse) vr::launch_enumerate_sparse(p, P->rank.as<uint32_t>(), P->binom.as<uint64_t>(), P->kmax, B, SR, st, &P->launches);
+      else vr::launch_enumerate(p, P->rank.as<uint32_t>(), P->binom.as<uint64_t>(), P->kmax, B, st, &P->launches);
+      if (P->sparse) vr::launch_resolve_sparse(p, P->rank.as<uint32_t>(), P->binom.as<uint64_t>(), P->kmax, B, SR, c.queued, st, &P->launches);
+      else vr::launch_resolve(p, P->rank.as<uint32_t>(), P->binom.as<uint64_t>(), P->kmax, B, c.queued, st, &P->launches);
+    }
+    P->local_sorted = vr::radix_sort_u64(P->resid.as<uint64_t>(), P->resid_alt.as<uint64_t>(), dr.residual, 0, dr.sort_bits,
+                                         P->sort_tmp.p, st, &P->launches);
+    CUDA_TRY(cudaGetLastError());
+  });
+}
+
+int vr_dist_replay_deaths(vr_plan* P, int32_t d) {
+  return guarded([&] {
+    if (!P || d < 1 || d > P->D) throw VrError(VR_EINVAL, "bad plan / dimension");
+    if (d < P->D && P->clr_of(d + 1))
+      vr::launch_set_bits(P->dims[(size_t)d + 1].deaths_in.as<uint64_t>(), P->dims[(size_t)d + 1].ndeaths_in,
+                          P->clr_of(d + 1), P->st, &P->launches);
+    CUDA_TRY(cudaGetLastError());
+  });
+}
+
+int64_t vr_plan_launches(const vr_plan* P) { return P ? P->launches : 0; }
 
 // ---------------------------------------------------------------- host-only residual
 int vr_host_residual(const uint32_t* rank, const float* values, int64_t nvalues, int64_t n, int32_t d, uint32_t maxr,

@@ -128,6 +128,7 @@ def orchestrate(backend, max_dim: int, group=None):
         backend.dim_finish(d, merged)
         lc = backend.counters(d)
         local[d] = dict(zip(names, lc))
+        local[d]["next_bitmap_words"] = words
         c = torch.tensor(lc, dtype=torch.int64, device=backend.device)
         dist.all_reduce(c, op=dist.ReduceOp.SUM, group=group)
         totals[d] = dict(zip(names, [int(x) for x in c.cpu().tolist()]))
@@ -142,6 +143,60 @@ def globalize_stats(bc: Barcode, totals: dict, local: dict) -> Barcode:
         for k in ("survivors", "apparent", "cleared", "queued", "scanned"):
             bc.stats[d][k] = t[k]
     return bc
+
+
+class ShardedHotPath:
+    """Benchmark harness for N ranks: one full distributed run, then `step()` replays
+    this rank's shard of the GPU hot path of every dimension with the two exchanges
+    (bitmap SUM all-reduce, all-gather of the sorted residual keys) — device work and
+    NCCL collectives only, asynchronous on the current stream."""
+
+    def __init__(self, d_dist_lower_tri, n, max_dim, threshold=math.inf, group=None, **opts):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.group = torch, dist, group
+        self.D = max_dim
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        self.be = LibBackend(d_dist_lower_tri, n, max_dim, threshold, rank, world, **opts)
+        self.result, self.totals, self.local = orchestrate(self.be, max_dim, group)
+        self.result = globalize_stats(self.result, self.totals, self.local)
+        self.survivors_total = sum(t["survivors"] for t in self.totals.values())
+        lib, h = self.be.lib, self.be.h
+        self.lib, self.h = lib, h
+        # fixed buffers for the exchanges (sizes of the first run are deterministic)
+        self.words, self.bm, self.keys, self.gathered = {}, {}, {}, {}
+        for d in range(1, max_dim + 1):
+            nk = self.local[d]["residual_local"]
+            nmax = torch.tensor([nk], dtype=torch.int64, device=self.be.device)
+            dist.all_reduce(nmax, op=dist.ReduceOp.MAX, group=group)
+            m = max(int(nmax.item()), 1)
+            self.keys[d] = torch.zeros(m, dtype=torch.int64, device=self.be.device)
+            self.gathered[d] = [torch.zeros(m, dtype=torch.int64, device=self.be.device) for _ in range(world)]
+        for d in range(1, max_dim + 1):
+            w = self.local[d]["next_bitmap_words"]  # bitmap of d+1; 0 = recompute mode
+            if w:
+                self.words[d] = w
+                self.bm[d] = torch.zeros(w, dtype=torch.int32, device=self.be.device)
+
+    def step(self) -> int:
+        """One hot-path pass over every dimension; returns the kernels launched."""
+        lib, h, dist, g = self.lib, self.h, self.dist, self.group
+        before = lib.vr_plan_launches(h)
+        _check(lib.vr_dist_replay_tables(h))
+        for d in range(1, self.D + 1):
+            _check(lib.vr_dist_replay_dim(h, d))
+            if d in self.bm:  # exchange A
+                _check(lib.vr_dist_bitmap(h, d + 1, ctypes.c_void_p(self.bm[d].data_ptr()), 2))
+                dist.all_reduce(self.bm[d], op=dist.ReduceOp.SUM, group=g)
+                _check(lib.vr_dist_bitmap(h, d + 1, ctypes.c_void_p(self.bm[d].data_ptr()), 3))
+            # exchange B
+            _check(lib.vr_dist_copy_keys_async(h, d, ctypes.c_void_p(self.keys[d].data_ptr())))
+            dist.all_gather(self.gathered[d], self.keys[d], group=g)
+            _check(lib.vr_dist_replay_deaths(h, d))
+        return int(lib.vr_plan_launches(h) - before)
+
+    def close(self):
+        self.be.close()
 
 
 def barcodes_sharded(d_dist_lower_tri, n: int, max_dim: int, threshold: float = math.inf, group=None, **opts):
