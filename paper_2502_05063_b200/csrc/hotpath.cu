@@ -53,6 +53,9 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
   const int n = T.n;
   const int v1 = u[1];
   if (v1 == 0) return;  // no v_0 < v_1
+  const uint32_t* __restrict__ rowu[D + 1];
+#pragma unroll
+  for (int i = 1; i <= D; ++i) rowu[i] = T.rank + (size_t)u[i] * (size_t)n;
   // prefix pair maxima: pm_up over all prefix pairs, pm_ex[j] over pairs avoiding u[j]
   uint32_t pm_up = 0;
   uint32_t pm_ex[D + 1];
@@ -62,7 +65,7 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
   for (int a = 1; a <= D; ++a)
 #pragma unroll
     for (int b = a + 1; b <= D; ++b) {
-      const uint32_t r = rank_at(T, u[a], u[b]);
+      const uint32_t r = __ldg(rowu[a] + u[b]);
       pm_up = umax(pm_up, r);
 #pragma unroll
       for (int j = 1; j <= D; ++j)
@@ -81,14 +84,12 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
     if (v >= 0) {
       m = 0;
 #pragma unroll
-      for (int i = 1; i <= D; ++i) m = (v == u[i]) ? VR_RINF : umax(m, rank_at(T, u[i], v));
+      for (int i = 1; i <= D; ++i) m = (v == u[i]) ? VR_RINF : umax(m, __ldg(rowu[i] + v));
     }
     mup0 = m;
   }
   const int steps = p.steps < n ? p.steps : n;
-  const uint32_t* __restrict__ rowu[D + 1];
-#pragma unroll
-  for (int i = 1; i <= D; ++i) rowu[i] = T.rank + (size_t)u[i] * (size_t)n;
+  const int steps4 = steps & ~3;  // whole groups of 4; the rest (n < steps) one by one
   const uint32_t* __restrict__ rowtop = T.rank + (size_t)(n - 1) * (size_t)n;  // row of v = n-1
 
   for (int base = 0; base < v1; base += 32) {
@@ -136,8 +137,10 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
         }
       }
     } else {
-      // one vote per 4 vertices
-      for (int j = 0; j < steps; j += 4) {
+      // one vote per 4 vertices; loads only for lanes whose prefix part allows a hit
+      const size_t nn = (size_t)n;
+      int j = 0;
+      for (; j < steps4; j += 4, pv -= 4 * nn) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int jj = j + q;
@@ -148,18 +151,34 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
           } else {
             m = 0;
 #pragma unroll
-            for (int i = 1; i <= D; ++i) m = (v == u[i]) ? VR_RINF : umax(m, __ldg(rowu[i] + (v < 0 ? 0 : v)));
+            for (int i = 1; i <= D; ++i) m = (v == u[i]) ? VR_RINF : umax(m, __ldg(rowu[i] + v));
           }
-          if (active && jj < steps) {
-            ++examined;
-            if (m <= rs && v != v0 && umax(m, __ldg(pv - (size_t)jj * (size_t)n)) <= rs) {
-              hitv = v;
-              active = false;
-            }
+          if (active && m <= rs && v != v0 && umax(m, __ldg(pv - (size_t)q * nn)) <= rs) {
+            hitv = v;
+            active = false;
           }
         }
         if (!__any_sync(0xffffffffu, active)) break;
       }
+      if (j >= steps4) {  // remainder (only when n < steps and n % 4 != 0)
+        for (; j < steps; ++j, pv -= nn) {
+          const int v = n - 1 - j;
+          uint32_t m;
+          if (j < 32) {
+            m = __shfl_sync(0xffffffffu, mup0, j & 31);
+          } else {
+            m = 0;
+#pragma unroll
+            for (int i = 1; i <= D; ++i) m = (v == u[i]) ? VR_RINF : umax(m, __ldg(rowu[i] + v));
+          }
+          if (active && m <= rs && v != v0 && umax(m, __ldg(pv)) <= rs) {
+            hitv = v;
+            active = false;
+          }
+        }
+      }
+      // vertices this lane examined: up to its hit, or the whole budget
+      examined = hitv >= 0 ? n - hitv : (active ? steps : 0);
     }
     scan_acc += (unsigned long long)__reduce_add_sync(0xffffffffu, (unsigned)examined);
     // condition 2 for lanes that found t = s ∪ {hitv}: no facet t \ {w}, w > hitv (the
@@ -171,10 +190,10 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
       uint32_t bup = 0;
 #pragma unroll
       for (int i = 1; i <= D; ++i) {
-        b[i] = rank_at(T, hitv, u[i]);
+        b[i] = __ldg(rowu[i] + hitv);
         bup = umax(bup, b[i]);
       }
-      const uint32_t b0 = rank_at(T, hitv, v0);
+      const uint32_t b0 = __ldg(rowtop - (size_t)(n - 1 - hitv) * (size_t)n + v0);
       if (v0 > hitv && umax(pm_up, bup) == rs) app = false;
 #pragma unroll
       for (int j = 1; j <= D; ++j) {
