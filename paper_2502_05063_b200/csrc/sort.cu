@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 
 #include "vr_common.cuh"
 #include "vr_internal.h"
@@ -301,6 +302,59 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter_fused(const uint64_t* _
   }
 }
 
+
+// Every pass in ONE cooperative launch (one CTA per tile, all co-resident): per-tile
+// histogram -> grid sync -> offsets + stable scatter -> grid sync, per 8-bit digit.
+__global__ void __launch_bounds__(RS_THREADS) rs_coop(uint64_t* __restrict__ a, uint64_t* __restrict__ b, size_t n,
+                                                     int begin_bit, int end_bit, uint32_t* __restrict__ tile_hist,
+                                                     uint32_t ntiles) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char rs_smem[];
+  uint64_t* keys_s = (uint64_t*)rs_smem;
+  uint64_t* sorted_s = keys_s + RS_TILE;
+  uint32_t* whist = (uint32_t*)(sorted_s + RS_TILE);
+  uint32_t* dstart = whist + RS_WARPS * RS_BINS;
+  uint32_t* gofs = dstart + RS_BINS;
+  __shared__ uint32_t warp_tot[SC_THREADS / 32];
+  __shared__ uint32_t total;
+  __shared__ uint32_t h[RS_BINS];
+  const size_t base = (size_t)blockIdx.x * RS_TILE;
+  const int cnt = (int)((n - base) < (size_t)RS_TILE ? (n - base) : (size_t)RS_TILE);
+  uint64_t* src = a;
+  uint64_t* dst = b;
+  for (int shift = begin_bit; shift < end_bit; shift += 8) {
+    const uint32_t dmask = end_bit - shift >= 8 ? 0xFFu : ((1u << (end_bit - shift)) - 1u);
+    for (int i = threadIdx.x; i < RS_TILE; i += RS_THREADS) keys_s[i] = i < cnt ? src[base + i] : ~0ull;
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += RS_THREADS) atomicAdd(&h[(uint32_t)(keys_s[i] >> shift) & dmask], 1u);
+    __syncthreads();
+    tile_hist[(size_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+    grid.sync();
+    {
+      const int bb = threadIdx.x;
+      uint32_t tot_b = 0, before = 0;
+      for (uint32_t t = 0; t < ntiles; ++t) {
+        const uint32_t c = tile_hist[(size_t)bb * ntiles + t];
+        tot_b += c;
+        if (t < blockIdx.x) before += c;
+      }
+      const uint32_t dig_start = block_exclusive_scan_256(tot_b, warp_tot, &total);
+      gofs[bb] = dig_start + before;
+    }
+    __syncthreads();
+    rs_tile_rank(keys_s, sorted_s, cnt, shift, dmask, whist, dstart, warp_tot, &total);
+    for (int j = threadIdx.x; j < cnt; j += RS_THREADS) {
+      const uint64_t k = sorted_s[j];
+      const uint32_t dg = (uint32_t)(k >> shift) & dmask;
+      dst[(size_t)gofs[dg] + (size_t)(j - (int)dstart[dg])] = k;
+    }
+    grid.sync();  // the next pass reads dst, and tile_hist is rewritten
+    uint64_t* t = src; src = dst; dst = t;
+  }
+}
+
 static size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
 size_t radix_sort_temp_bytes(size_t n) {
@@ -330,6 +384,23 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit,
   }
   const uint32_t ntiles = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
   uint32_t* hist = (uint32_t*)temp;
+  static int coop_cap = -1;
+  if (coop_cap < 0) {
+    int dev = 0, sms = 0, per = 0, coop = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaFuncSetAttribute(rs_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rs_coop, RS_THREADS, smem);
+    coop_cap = coop ? sms * per : 0;
+  }
+  if ((int)ntiles <= coop_cap) {  // every pass in one cooperative launch
+    const int passes = (end_bit - begin_bit + 7) / 8;
+    void* args[] = {(void*)&keys, (void*)&alt, (void*)&n, (void*)&begin_bit, (void*)&end_bit, (void*)&hist, (void*)&ntiles};
+    cudaLaunchCooperativeKernel((void*)rs_coop, dim3(ntiles), dim3(RS_THREADS), args, smem, st);
+    if (launches) *launches += 1;
+    return (passes & 1) ? alt : keys;
+  }
   void* scan_tmp = (char*)temp + align256((size_t)RS_BINS * ntiles * sizeof(uint32_t));
   uint64_t* src = keys;
   uint64_t* dst = alt;
