@@ -49,6 +49,9 @@ def _load():
                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         lib.oracle_reduce_columns.restype = ctypes.c_int
         lib.oracle_reduce_columns.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_apparent_one.restype = ctypes.c_int
+        lib.oracle_apparent_one.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float, ctypes.c_void_p,
+                                            ctypes.c_void_p]
         lib.oracle_enclosing_radius.restype = ctypes.c_float
         lib.oracle_enclosing_radius.argtypes = [ctypes.c_void_p, ctypes.c_int64]
         _lib = lib
@@ -123,6 +126,18 @@ def apparent(lower_tri: np.ndarray, n: int, d: int, threshold: float = float("in
     if m:
         lib.oracle_apparent(lt.ctypes.data, n, d, ctypes.c_float(threshold), c.ctypes.data, f.ctypes.data, p.ctypes.data)
     return c, f.astype(bool), p
+
+
+def apparent_one(lower_tri: np.ndarray, n: int, vertices, threshold: float = float("inf")):
+    """Def 5.3.4 for one simplex by brute force: (is_apparent, partner_cidx or None);
+    None if the simplex is over the threshold."""
+    lt = np.ascontiguousarray(lower_tri, dtype=np.float32)
+    v = np.ascontiguousarray(vertices, dtype=np.int32)
+    p = ctypes.c_uint64(0)
+    r = _load().oracle_apparent_one(lt.ctypes.data, n, v.size - 1, ctypes.c_float(threshold), v.ctypes.data, ctypes.byref(p))
+    if r < 0:
+        return None
+    return bool(r), (int(p.value) if r else None)
 
 
 def reduce_columns(columns: list[list[int]]) -> list[int]:

@@ -429,6 +429,75 @@ int64_t oracle_apparent(const float *lt, int64_t n, int d, float threshold, uint
   return m;
 }
 
+/* Def 5.3.4 for ONE d-simplex given by its vertices (any order), by brute force over its
+ * explicit cofacets and their facets — usable at full problem sizes on sampled simplices.
+ * Returns 1 and the partner's cidx if (s, t) is apparent, 0 if not, -1 if s is not in the
+ * complex (diam > t). */
+int oracle_apparent_one(const float *lt, int64_t n, int d, float threshold, const int *verts, uint64_t *partner) {
+  if (d < 0 || d + 2 > OR_MAXV) return -1;
+  uint64_t **C = binom_table(n, d + 2);
+  simplex s;
+  memset(&s, 0, sizeof s);
+  s.dim = d;
+  for (int p = 0; p <= d; ++p) s.v[p] = verts[p];
+  for (int a = 0; a <= d; ++a) /* sort decreasing */
+    for (int b = a + 1; b <= d; ++b)
+      if (s.v[b] > s.v[a]) { int t = s.v[a]; s.v[a] = s.v[b]; s.v[b] = t; }
+  float ds = 0.0f;
+  for (int a = 0; a <= d; ++a)
+    for (int b = a + 1; b <= d; ++b) { float x = dist_lt(lt, s.v[a], s.v[b]); if (x > ds) ds = x; }
+  if (!(ds <= threshold)) { binom_free(C, n); return -1; }
+  s.diam = ds;
+  s.cidx = cidx_of(C, s.v, d);
+  int have = 0;
+  simplex best;
+  memset(&best, 0, sizeof best);
+  for (int64_t v = 0; v < n; v++) {
+    int inside = 0;
+    for (int p = 0; p <= d; ++p) inside |= (s.v[p] == v);
+    if (inside) continue;
+    simplex t;
+    memset(&t, 0, sizeof t);
+    t.dim = d + 1;
+    int q = 0, placed = 0;
+    for (int p = 0; p <= d; ++p) {
+      if (!placed && v > s.v[p]) { t.v[q++] = (int)v; placed = 1; }
+      t.v[q++] = s.v[p];
+    }
+    if (!placed) t.v[q++] = (int)v;
+    float dm = 0.0f;
+    for (int a = 0; a <= d + 1; a++)
+      for (int b = a + 1; b <= d + 1; b++) { float x = dist_lt(lt, t.v[a], t.v[b]); if (x > dm) dm = x; }
+    if (!(dm <= threshold)) continue;
+    t.diam = dm;
+    t.cidx = cidx_of(C, t.v, d + 1);
+    if (!have || filtration_cmp(&t, &best) < 0) { best = t; have = 1; } /* oldest cofacet */
+  }
+  int res = 0;
+  if (have) {
+    simplex young;
+    memset(&young, 0, sizeof young);
+    int hy = 0;
+    for (int drop = 0; drop <= d + 1; drop++) {
+      simplex f;
+      memset(&f, 0, sizeof f);
+      f.dim = d;
+      int q = 0;
+      for (int p = 0; p <= d + 1; p++)
+        if (p != drop) f.v[q++] = best.v[p];
+      float dm = 0.0f;
+      for (int a = 0; a <= d; a++)
+        for (int b = a + 1; b <= d; b++) { float x = dist_lt(lt, f.v[a], f.v[b]); if (x > dm) dm = x; }
+      f.diam = dm;
+      f.cidx = cidx_of(C, f.v, d);
+      if (!hy || filtration_cmp(&f, &young) > 0) { young = f; hy = 1; } /* youngest facet */
+    }
+    if (young.cidx == s.cidx) { res = 1; if (partner) *partner = best.cidx; }
+  }
+  binom_free(C, n);
+  return res;
+}
+
 /* ---------------------------------------------------------------- Alg 2 alone */
 /* Explicit matrix in CSC (col_ptr[ncols+1], rows[] ascending per column).  Writes the
  * final low of every column (NONE = -1 for a zero column).  Used for the Fig 4.1 pin. */

@@ -382,3 +382,42 @@ def test_sharded_hot_path_replay_single_rank():
         hp.close()
     finally:
         tdist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ full sizes: sampled outputs vs the oracle
+def _decode(c, k, n):
+    out, hi = [], n
+    for q in range(k):
+        kk = k - q
+        lo, h = kk - 1, hi - 1
+        while lo < h:
+            mid = (lo + h + 1) // 2
+            if math.comb(mid, kk) <= c:
+                lo = mid
+            else:
+                h = mid - 1
+        out.append(lo)
+        c -= math.comb(lo, kk)
+        hi = lo
+    return out
+
+
+@pytest.mark.parametrize("name,D,thr,sparse", [("c2_s3_192", 3, None, 0), ("c4a_sierpinski512", 2, None, 0),
+                                                ("c5_o3_4096", 2, 1.4, 0)])
+def test_full_size_sampled_apparent_pairs(name, D, thr, sparse):
+    cfg = G.CONFIGS[name]
+    lt = cfg.lower_tri()
+    got = vr.barcodes(lt, cfg.n, D, cfg.threshold, index_pairs=True, sparse_mode=sparse)
+    t = got.threshold
+    rng = np.random.default_rng(7)
+    for d in range(1, D + 1):
+        ip = got.index_pairs[d]
+        napp = got.stats[d]["apparent"]
+        app, rest = ip[:napp], ip[napp:]
+        assert len(rest) == got.stats[d]["residual_columns"]
+        for k in rng.choice(napp, size=min(400, napp), replace=False):
+            s, tt = int(app[k, 0]), int(app[k, 1])
+            assert O.apparent_one(lt, cfg.n, _decode(s, d + 1, cfg.n), t) == (True, tt), (d, s)
+        for k in rng.choice(len(rest), size=min(200, len(rest)), replace=False):
+            s = int(rest[k, 0])
+            assert O.apparent_one(lt, cfg.n, _decode(s, d + 1, cfg.n), t) == (False, None), (d, s)

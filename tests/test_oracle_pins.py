@@ -346,3 +346,25 @@ def test_sphere_s2_betti():
     h2 = b.positive(2)
     assert len(h2) == 1 and h2[0, 1] - h2[0, 0] > 0.5
     assert b.num_essential(1) == 0 and b.num_essential(2) == 0 and b.num_essential(0) == 1
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_apparent_one_matches_set_definition(seed):
+    # the per-simplex brute force (used on sampled full-size outputs) agrees with the
+    # pinned set-based Def 5.3.4 on every simplex of small inputs
+    n = 8
+    lt = G.random_tied(n, seed, levels=3) if seed % 2 else G.random_cloud(n, seed)
+    t = [math.inf, float(np.quantile(lt, 0.7))][seed % 2]
+    for d in (1, 2):
+        c, f, p = O.apparent(lt, n, d, t)
+        for ci, fl, pi in zip(c.tolist(), f.tolist(), p.tolist()):
+            vs, x, hi = [], ci, n
+            for q in range(d + 1):
+                kk = d + 1 - q
+                v = kk - 1
+                while v + 1 < hi and math.comb(v + 1, kk) <= x:
+                    v += 1
+                vs.append(v)
+                x -= math.comb(v, kk)
+                hi = v
+            assert O.apparent_one(lt, n, vs, t) == (fl, pi if fl else None)
