@@ -76,8 +76,9 @@ typedef struct {
   int32_t device;        /* CUDA device ordinal used by vr_barcodes (host-pointer entry) */
   int32_t rows_per_grab; /* tuning: prefix rows a warp takes per atomic grab; 0 = default
                             (4 for n < 384, else 1) */
-  int32_t scan_variant;  /* tuning: phase-1 scan loop, 0 = default (one warp vote per 4 cofacet
-                            vertices), 1: one vote per vertex, 2: per 4 vertices; same results */
+  int32_t scan_variant;  /* tuning: phase-1 scan loop, 0 = default, 1: one warp vote per cofacet
+                            vertex, 2: per 4 vertices, 3: per 4 vertices then the unresolved
+                            columns resolved warp-cooperatively in the same kernel; same results */
   int32_t sparse_mode;   /* -1/0 = auto (output-sensitive when <= 25% of the edges are under the
                             threshold, or when the dense index space is too large),
                             1 = always dense, 2 = always output-sensitive; same results */

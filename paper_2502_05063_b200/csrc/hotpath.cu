@@ -111,6 +111,7 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
     if (B.clr && surv) cleared = bit_test(B.clr, cidx);  // a death of dimension d-1
     clr_acc += __popc(__ballot_sync(0xffffffffu, cleared));
     bool active = surv && !cleared;
+    bool nohit = false;  // resolved in-kernel: no equal-diameter cofacet at all
     int hitv = -1;
     int examined = 0;  // cofacet vertices this lane examined
     // Lemma 5.3.6 condition 1, lane-parallel: the first v with every new edge <= diam(s)
@@ -180,6 +181,45 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
       // vertices this lane examined: up to its hit, or the whole budget
       examined = hitv >= 0 ? n - hitv : (active ? steps : 0);
     }
+    if (p.variant == 2 && B.clr) {
+      // columns still unresolved after the short lock-step scan: the whole warp resolves
+      // them one at a time, 32 cofacet vertices per step (phase 2 folded into phase 1 —
+      // no queue, no divergence tail)
+      uint32_t mrem = __ballot_sync(0xffffffffu, active);
+      while (mrem) {
+        const int src = __ffs(mrem) - 1;
+        mrem &= mrem - 1;
+        const int v0s = __shfl_sync(0xffffffffu, v0, src);
+        const uint32_t rss = __shfl_sync(0xffffffffu, rs, src);
+        const uint32_t* __restrict__ rowv0 = T.rank + (size_t)v0s * (size_t)n;
+        int hv = -1;
+        for (int base = steps; base < n; base += 32) {
+          const int j = base + lane;
+          const int v = n - 1 - j;
+          const uint32_t msh = __shfl_sync(0xffffffffu, mup0, j & 31);  // every lane takes part
+          uint32_t m = VR_RINF;
+          if (j < 32) {
+            m = msh;
+          } else if (v >= 0) {
+            m = 0;
+#pragma unroll
+            for (int i = 1; i <= D; ++i) m = (v == u[i]) ? VR_RINF : umax(m, __ldg(rowu[i] + v));
+          }
+          const bool hit = v >= 0 && v != v0s && m <= rss && umax(m, __ldg(rowv0 + (v >= 0 ? v : 0))) <= rss;
+          const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+          if (bal) {
+            hv = n - 1 - (base + __ffs(bal) - 1);
+            break;
+          }
+        }
+        if (lane == src) {
+          hitv = hv;
+          active = false;
+          examined = hv >= 0 ? n - hv : n;
+          if (hv < 0) nohit = true;
+        }
+      }
+    }
     scan_acc += (unsigned long long)__reduce_add_sync(0xffffffffu, (unsigned)examined);
     // condition 2 for lanes that found t = s ∪ {hitv}: no facet t \ {w}, w > hitv (the
     // lex-smaller facets), with diam = diam(s)
@@ -225,7 +265,7 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
     const uint64_t key = ((uint64_t)(p.maxr - rs) << p.cbits) | cidx;
     // not apparent and not cleared: a residual column (bitmap mode only — without a
     // bitmap clearing is decided in phase 2)
-    const bool to_resid = B.clr && hitv >= 0 && !app;
+    const bool to_resid = B.clr && ((hitv >= 0 && !app) || nohit);
     const bool to_queue = active || (!B.clr && hitv >= 0 && !app);
     const unsigned long long rslot = warp_append(to_resid, &B.ctr->residual);
     if (to_resid && rslot < B.rcap) B.resid[rslot] = key;
