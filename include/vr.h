@@ -215,6 +215,39 @@ int vr_host_residual(const uint32_t* rank, const float* values, int64_t nvalues,
                      uint64_t* birth_cidx, uint64_t* death_cidx, int64_t* emergent);
 
 /* ----------------------------------------------------------------------------------
+ * HYPHA (PAPER.md Ch.4, Algs 3-10): pivots of an EXPLICIT Z/2
+ * boundary matrix given in CSC — col_ptr[ncols+1] (int64), rows[] ascending within each
+ * column and strictly below the column (rows[k] < j: a filtration's boundary matrix is
+ * strictly upper triangular).  GPU-scan (leftmost 1s, 0-addition pivots, clearing marks,
+ * unstable columns) on the current device, then on the host optional compression
+ * (VR_HYPHA_COMPRESSION) and the reduction of the unstable columns (twist order when
+ * dims[] — the dimension of every column — is given, else left to right).
+ * Clearing (VR_HYPHA_CLEARING, and the twist order) and compression use ∂∂ = 0: set them
+ * only for a boundary matrix; with flags = 0 and dims = NULL any strictly upper-triangular
+ * Z/2 matrix is reduced exactly (Alg 2's pivots).
+ * low_out[j] = the pivot row of column j in the reduced matrix, or -1 (a zero column).
+ * Returns VR_EINPUT for a malformed matrix.
+ * ---------------------------------------------------------------------------------- */
+#define VR_HYPHA_COMPRESSION 1
+#define VR_HYPHA_CLEARING 2
+typedef struct {
+  int64_t stable;      /* columns the GPU scan found final (zero, 0-addition pivots, cleared) */
+  int64_t unstable;    /* columns left for the host */
+  int64_t cleared;     /* nonzero columns zeroed by clearing (Lemma 4.2.3) */
+  int64_t compressed;  /* entries removed by compression (Lemma 4.2.4/4.2.5) */
+  int64_t additions;   /* column additions on the host */
+  double ms_gpu_scan;  /* device time of the three scan kernels (CUDA events) */
+  double ms_host;      /* host phase: compression + reduction */
+  double ms_compress_scan; /* of which FIND-COMPRESSIBLE over all rows */
+  double ms_reduce;    /* of which the reduction of the unstable columns */
+  double ms_total;     /* the whole call: checks, H2D, scan, D2H, host phase */
+  double ms_prepare;   /* of which before the scan (col_ptr checks, buffers, H2D issue) */
+  int64_t threads;     /* host threads of the reduction */
+} vr_hypha_stats;
+int vr_hypha_pivots(const int64_t* col_ptr, const int32_t* rows, int64_t ncols, const int32_t* dims, int32_t flags,
+                    int32_t* low_out, vr_hypha_stats* stats);
+
+/* ----------------------------------------------------------------------------------
  * Component entry (tests): the library's device radix sort on
  * caller keys.  keys: HOST pointer to n uint64 values, sorted ascending in place on bits
  * [begin_bit, end_bit) (LSD, stable; bits outside the range do not take part in the

@@ -154,6 +154,19 @@ def reduce_columns(columns: list[list[int]]) -> list[int]:
     return low[: len(columns)].tolist()
 
 
+def reduce_csc(col_ptr: np.ndarray, rows: np.ndarray) -> np.ndarray:
+    """reduce_columns on a CSC matrix (col_ptr int64[ncols+1], rows int32[])."""
+    lib = _load()
+    ptr = np.ascontiguousarray(col_ptr, np.int64)
+    rw = np.ascontiguousarray(rows, np.int32)
+    n = ptr.size - 1
+    low = np.empty(max(n, 1), np.int32)
+    rc = lib.oracle_reduce_columns(n, ptr.ctypes.data, rw.ctypes.data if rw.size else None, low.ctypes.data)
+    if rc != 0:
+        raise ValueError("bad matrix")
+    return low[:n]
+
+
 def enclosing_radius(lower_tri: np.ndarray, n: int) -> float:
     lt = np.ascontiguousarray(lower_tri, dtype=np.float32)
     return float(_load().oracle_enclosing_radius(lt.ctypes.data if lt.size else None, n))

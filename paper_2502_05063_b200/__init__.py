@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-__all__ = ["barcodes", "barcodes_device", "radix_sort_u64", "Plan", "Barcode", "VRError", "lib_path", "load"]
+__all__ = ["barcodes", "barcodes_device", "radix_sort_u64", "hypha_pivots", "Plan", "Barcode", "VRError", "lib_path", "load"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_HERE, "libvr.so")
@@ -90,6 +90,7 @@ def load() -> ctypes.CDLL:
         "vr_plan_timing": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double)]),
         "vr_plan_free": (None, [vp]),
         "vr_radix_sort_u64": (ctypes.c_int, [vp, i64, i32, i32]),
+        "vr_hypha_pivots": (ctypes.c_int, [vp, vp, i64, vp, i32, vp, vp]),
         "vr_dist_begin": (ctypes.c_int, [vp, i64, i32, f32, vp, vp, i32, i32, ctypes.POINTER(vp)]),
         "vr_dist_dim_local": (ctypes.c_int, [vp, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
         "vr_dist_copy_keys": (ctypes.c_int, [vp, i32, vp]),
@@ -205,6 +206,30 @@ def _device_ptr_and_stream(t, n, stream):
     else:
         st = getattr(stream, "cuda_stream", stream)
     return ctypes.c_void_p(ptr or None), ctypes.c_void_p(st or None)
+
+
+class _HyphaStats(ctypes.Structure):
+    _fields_ = [("stable", ctypes.c_int64), ("unstable", ctypes.c_int64), ("cleared", ctypes.c_int64),
+                ("compressed", ctypes.c_int64), ("additions", ctypes.c_int64), ("ms_gpu_scan", ctypes.c_double),
+                ("ms_host", ctypes.c_double), ("ms_compress_scan", ctypes.c_double), ("ms_reduce", ctypes.c_double),
+                ("ms_total", ctypes.c_double), ("ms_prepare", ctypes.c_double), ("threads", ctypes.c_int64)]
+
+
+def hypha_pivots(col_ptr, rows, dims=None, compression: bool = True, clearing: bool = True):
+    """HYPHA (Ch.4) on an explicit CSC boundary matrix: (low per column, stats dict).
+    For a matrix that is not a boundary matrix pass dims=None, compression=clearing=False."""
+    lib = load()
+    cp = np.ascontiguousarray(col_ptr, dtype=np.int64)
+    rw = np.ascontiguousarray(rows, dtype=np.int32)
+    n = cp.size - 1
+    dm = None if dims is None else np.ascontiguousarray(dims, dtype=np.int32)
+    low = np.zeros(max(n, 1), np.int32)
+    st = _HyphaStats()
+    _check(lib.vr_hypha_pivots(cp.ctypes.data, rw.ctypes.data if rw.size else None, n,
+                               dm.ctypes.data if dm is not None else None,
+                               (1 if compression else 0) | (2 if clearing else 0),
+                               low.ctypes.data, ctypes.byref(st)))
+    return low[:n], {f: getattr(st, f) for f, _ in _HyphaStats._fields_}
 
 
 def radix_sort_u64(keys: np.ndarray, begin_bit: int = 0, end_bit: int = 64) -> np.ndarray:

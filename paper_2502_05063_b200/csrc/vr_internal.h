@@ -5,6 +5,8 @@
 #include <vector>
 #include <cuda_runtime.h>
 
+#include "../../include/vr.h"
+
 namespace vr {
 
 // ---------------------------------------------------------------- sort.cu
@@ -112,5 +114,11 @@ struct ResidualStats {
 };
 void residual_reduce(const HostMatrix& M, int d, uint32_t maxr, int cbits, const uint64_t* keys, uint64_t nkeys,
                      int mode, HostPairs& out, std::vector<uint64_t>& deaths_sorted, ResidualStats& st);
+
+// HYPHA host phase (hypha_host.cpp): compression + reduction of the unstable columns;
+// Lookup (row -> pivot column, -1) holds the GPU pivots on entry and every pivot on exit.
+void hypha_host_reduce(const int64_t* col_ptr, const int32_t* rows, int64_t n, const int32_t* dims, int32_t flags,
+                       const int32_t* Left, int32_t* Lookup, const uint8_t* stable, const int32_t* u, int64_t nu,
+                       vr_hypha_stats& st);
 
 }  // namespace vr
