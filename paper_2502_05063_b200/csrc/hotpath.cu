@@ -84,7 +84,7 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
     if (v >= 0) {
       m = 0;
 #pragma unroll
-      for (int i = 1; i <= D; ++i) m = (v == u[i]) ? VR_RINF : umax(m, __ldg(rowu[i] + v));
+      for (int i = 1; i <= D; ++i) m = umax(m, __ldg(rowu[i] + v));  // R[u_i][u_i] = RINF
     }
     mup0 = m;
   }
@@ -138,30 +138,26 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
         }
       }
     } else {
-      // one vote per 4 vertices; loads only for lanes whose prefix part allows a hit
+      // one vote per 4 vertices.  Inside the 32-vertex window the prefix part m comes from
+      // mup0 by a uniform-index shuffle and the step is branch-free: the load R[v][v0] is
+      // unconditional (row v, column v0 < n — in range, coalesced over the warp)
       const size_t nn = (size_t)n;
+      const int wsteps4 = (steps < 32 ? steps : 32) & ~3;
       int j = 0;
-      for (; j < steps4; j += 4, pv -= 4 * nn) {
+      bool any_active = true;
+      for (; j < wsteps4; j += 4, pv -= 4 * nn) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int jj = j + q;
-          const int v = n - 1 - jj;
-          uint32_t m;
-          if (jj < 32) {
-            m = __shfl_sync(0xffffffffu, mup0, jj & 31);
-          } else {
-            m = 0;
-#pragma unroll
-            for (int i = 1; i <= D; ++i) m = (v == u[i]) ? VR_RINF : umax(m, __ldg(rowu[i] + v));
-          }
-          if (active && m <= rs && v != v0 && umax(m, __ldg(pv - (size_t)q * nn)) <= rs) {
-            hitv = v;
-            active = false;
-          }
+          const int v = n - 1 - (j + q);
+          const uint32_t m = __shfl_sync(0xffffffffu, mup0, j + q);
+          const uint32_t r = __ldg(pv - (size_t)q * nn);
+          const bool hit = active & (umax(m, r) <= rs);  // v = v0: R[v0][v0] = RINF
+          hitv = hit ? v : hitv;
+          active = active & !hit;
         }
-        if (!__any_sync(0xffffffffu, active)) break;
+        if (!__any_sync(0xffffffffu, active)) { any_active = false; break; }
       }
-      if (j >= steps4) {  // remainder (only when n < steps and n % 4 != 0)
+      if (any_active) {  // the rest of the budget, one vertex at a time (steps > 32 or n < 32)
         for (; j < steps; ++j, pv -= nn) {
           const int v = n - 1 - j;
           uint32_t m;
@@ -176,6 +172,7 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
             hitv = v;
             active = false;
           }
+          if (!__any_sync(0xffffffffu, active)) break;
         }
       }
       // vertices this lane examined: up to its hit, or the whole budget

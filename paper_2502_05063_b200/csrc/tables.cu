@@ -10,7 +10,7 @@
 //   4. tb_finalize  : R = min_i rowmax_i, t = threshold or R when threshold is
 //                     +inf (Prop 5.2.13), m = #edges with d <= t (inclusive, Eq 5.3).
 //   5. tb_rank      : rank[i][j] = index of the first sorted edge with the value d(i,j)
-//                     (a lower_bound), or RINF when d(i,j) > t.  Equal distances get equal
+//                     (a lower_bound), or RINF when d(i,j) > t or i = j.  Equal distances get equal
 //                     ranks and the order is kept, so rank comparisons are the paper's
 //                     diameter comparisons, exactly (reading A11: no arithmetic on values).
 #include <cstdint>
@@ -93,7 +93,7 @@ __global__ void tb_rank(const float* __restrict__ lt, int64_t n, const uint64_t*
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     uint32_t r;
     if (i == j) {
-      r = 0;
+      r = VR_RINF;  // no self-pairs: a scan over cofacet vertices v needs no v != s_i test
     } else {
       const uint32_t b = dist_bits(lt_at(lt, i, j));
       if (b > tb) {

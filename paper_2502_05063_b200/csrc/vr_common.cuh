@@ -35,14 +35,23 @@ __device__ __forceinline__ uint32_t rank_at(const Tables& T, int i, int j) {
 }
 
 // Largest v in [k-1, hi-1] with C(v, k) <= x  (C(., k) is non-decreasing; C(k-1, k) = 0).
-// This is the per-vertex binary search of the combinatorial number system (A31).
+// This is the per-vertex search of the combinatorial number system (A31): a float
+// estimate v ~ (k! x)^(1/k) + (k-1)/2 (C(v,k) ~ (v-(k-1)/2)^k / k!), then exact integer
+// steps on the binomial table — one or two table reads instead of a binary search.
 __device__ __forceinline__ int cns_find(const Tables& T, uint64_t x, int k, int hi) {
-  int lo = k - 1, h = hi - 1;  // invariant: C(lo,k) <= x
-  while (lo < h) {
-    int mid = (lo + h + 1) >> 1;
-    if (binom(T, mid, k) <= x) lo = mid; else h = mid - 1;
+  int g;
+  if (k == 1) {
+    g = x < (uint64_t)hi ? (int)x : hi - 1;
+  } else {
+    float kf = 1.f;
+    for (int i = 2; i <= k; ++i) kf *= (float)i;
+    const float est = (k == 2) ? sqrtf(2.f * (float)x) + 0.5f : __powf(kf * (float)x, 1.f / (float)k) + 0.5f * (float)(k - 1);
+    g = (int)est;
+    g = g < k - 1 ? k - 1 : (g > hi - 1 ? hi - 1 : g);
   }
-  return lo;
+  while (g > k - 1 && binom(T, g, k) > x) --g;
+  while (g + 1 < hi && binom(T, g + 1, k) <= x) ++g;
+  return g;
 }
 
 // Eq 5.6 decode: cidx of a dim-d simplex -> vertices s[0] > s[1] > ... > s[d].
