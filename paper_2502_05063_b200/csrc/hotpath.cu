@@ -45,9 +45,20 @@ namespace vr {
 constexpr int HP_THREADS = 256;
 
 // ------------------------------------------------------------------ phase 1: enumerate
+// Row-invariant parts of the upper prefix U = {u_D > ... > u_2}, reused by consecutive rows
+// that differ only in u_1 (colex-consecutive rows): pair maxima over U (all, and avoiding
+// each u_j), the cidx part sum_{i>=2} C(u_i, i+1), and the window maximum over U.
+template <int D>
+struct UpperCache {
+  int key[D + 2];
+  bool valid = false;
+  uint32_t pmU, pmU_ex[D + 1], mupU;
+  uint64_t cU;
+};
+
 template <int D>
 __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p, const HotBuffers& B, const int (&u)[D + 2],
-                                            unsigned long long& surv_acc, unsigned long long& app_acc,
+                                            UpperCache<D>& uc, unsigned long long& surv_acc, unsigned long long& app_acc,
                                             unsigned long long& scan_acc, unsigned long long& clr_acc) {
   const int lane = threadIdx.x & 31;
   const int n = T.n;
@@ -56,38 +67,64 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
   const uint32_t* __restrict__ rowu[D + 1];
 #pragma unroll
   for (int i = 1; i <= D; ++i) rowu[i] = T.rank + (size_t)u[i] * (size_t)n;
-  // prefix pair maxima: pm_up over all prefix pairs, pm_ex[j] over pairs avoiding u[j]
-  uint32_t pm_up = 0;
-  uint32_t pm_ex[D + 1];
+  bool same = uc.valid;
 #pragma unroll
-  for (int j = 0; j <= D; ++j) pm_ex[j] = 0;
+  for (int i = 2; i <= D; ++i) same = same && uc.key[i] == u[i];
+  if (!same) {
+    uc.valid = true;
+    uc.pmU = 0;
+    uc.cU = 0;
 #pragma unroll
-  for (int a = 1; a <= D; ++a)
+    for (int j = 0; j <= D; ++j) uc.pmU_ex[j] = 0;
 #pragma unroll
-    for (int b = a + 1; b <= D; ++b) {
-      const uint32_t r = __ldg(rowu[a] + u[b]);
-      pm_up = umax(pm_up, r);
-#pragma unroll
-      for (int j = 1; j <= D; ++j)
-        if (j != a && j != b) pm_ex[j] = umax(pm_ex[j], r);
+    for (int i = 2; i <= D; ++i) {
+      uc.key[i] = u[i];
+      uc.cU += binom(T, u[i], i + 1);
     }
-  if (pm_up == VR_RINF) return;  // every simplex of the row is over the threshold
-  uint64_t cbase = 0;
 #pragma unroll
-  for (int i = 1; i <= D; ++i) cbase += binom(T, u[i], i + 1);
+    for (int a = 2; a <= D; ++a)
+#pragma unroll
+      for (int b = a + 1; b <= D; ++b) {
+        const uint32_t r = __ldg(rowu[a] + u[b]);
+        uc.pmU = umax(uc.pmU, r);
+#pragma unroll
+        for (int j = 2; j <= D; ++j)
+          if (j != a && j != b) uc.pmU_ex[j] = umax(uc.pmU_ex[j], r);
+      }
+    const int v = n - 1 - lane;
+    uint32_t m = v >= 0 ? 0u : VR_RINF;
+    if (v >= 0) {
+#pragma unroll
+      for (int i = 2; i <= D; ++i) m = umax(m, __ldg(rowu[i] + v));  // R[u_i][u_i] = RINF
+    }
+    uc.mupU = m;
+  }
+  if (uc.pmU == VR_RINF) return;  // every simplex of the row is over the threshold
+  // prefix pair maxima: pm_up over all prefix pairs, pm_ex[j] over pairs avoiding u[j]
+  uint32_t r1[D + 1];
+  uint32_t pm_up = uc.pmU;
+#pragma unroll
+  for (int b = 2; b <= D; ++b) {
+    r1[b] = __ldg(rowu[1] + u[b]);
+    pm_up = umax(pm_up, r1[b]);
+  }
+  if (pm_up == VR_RINF) return;
+  uint32_t pm_ex[D + 1];
+  pm_ex[0] = 0;
+  pm_ex[1] = uc.pmU;
+#pragma unroll
+  for (int j = 2; j <= D; ++j) {
+    uint32_t m = uc.pmU_ex[j];
+#pragma unroll
+    for (int b = 2; b <= D; ++b)
+      if (b != j) m = umax(m, r1[b]);
+    pm_ex[j] = m;
+  }
+  const uint64_t cbase = uc.cU + binom(T, u[1], 2);
   // window of the first 32 cofacet vertices v = n-1-lane: mup = max_i R[u_i][v]
   // (RINF for a prefix vertex, so the warp skips it)
-  uint32_t mup0;
-  {
-    const int v = n - 1 - lane;
-    uint32_t m = VR_RINF;
-    if (v >= 0) {
-      m = 0;
-#pragma unroll
-      for (int i = 1; i <= D; ++i) m = umax(m, __ldg(rowu[i] + v));  // R[u_i][u_i] = RINF
-    }
-    mup0 = m;
-  }
+  const int vw = n - 1 - lane;
+  const uint32_t mup0 = vw >= 0 ? umax(uc.mupU, __ldg(rowu[1] + vw)) : VR_RINF;
   const int steps = p.steps < n ? p.steps : n;
   const int steps4 = steps & ~3;  // whole groups of 4; the rest (n < steps) one by one
   const uint32_t* __restrict__ rowtop = T.rank + (size_t)(n - 1) * (size_t)n;  // row of v = n-1
@@ -289,6 +326,7 @@ __global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p,
   const uint64_t W = (uint64_t)p.shard_world;
   const uint64_t all = p.row_end - p.row_begin;
   const uint64_t nrows = all > (uint64_t)p.shard_rank ? (all - (uint64_t)p.shard_rank + W - 1) / W : 0;  // this shard's rows
+  UpperCache<D> uc;  // kept across grabs: a warp's next grab often shares the upper prefix
   while (true) {
     unsigned long long g0 = 0;
     if (lane == 0) g0 = atomicAdd(&B.ctr->row_next, (unsigned long long)GRAB);
@@ -324,7 +362,7 @@ __global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p,
         for (int j = D; j >= 1; --j)
           if (j < top) u[j] = u[top] - (top - j);
       }
-      process_row<D>(T, p, B, u, surv_acc, app_acc, scan_acc, clr_acc);
+      process_row<D>(T, p, B, u, uc, surv_acc, app_acc, scan_acc, clr_acc);
     }
   }
   if (lane == 0) {

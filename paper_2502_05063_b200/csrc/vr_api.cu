@@ -15,7 +15,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -44,6 +46,124 @@ struct VrError : std::runtime_error {
     }                                                                                               \
   } while (0)
 
+// Process-wide cache of device blocks: cudaMalloc/cudaFree cost milliseconds each (and
+// cudaFree synchronises the device), so a plan's buffers go back to this cache when the
+// plan is freed and the next call of the same shape reuses them.  Best fit within 25% of
+// the request; on an allocation failure the cache is emptied and the allocation retried.
+class DevCache {
+ public:
+  static DevCache& get() {
+    static DevCache c;
+    return c;
+  }
+  void* alloc(size_t& b) {
+    b = round(b);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      auto it = free_.lower_bound(Key{dev, b});
+      if (it != free_.end() && it->first.dev == dev && it->first.bytes <= b + b / 4) {
+        void* p = it->second;
+        b = it->first.bytes;
+        cached_ -= b;
+        free_.erase(it);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      trim(dev);
+      CUDA_TRY(cudaMalloc(&p, b));
+    }
+    return p;
+  }
+  void release(void* p, size_t b) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu_);
+    if (cached_ + b > kCap) {
+      cudaFree(p);
+      return;
+    }
+    free_.emplace(Key{dev, b}, p);
+    cached_ += b;
+  }
+  void trim(int dev) {
+    std::lock_guard<std::mutex> g(mu_);
+    for (auto it = free_.begin(); it != free_.end();) {
+      if (it->first.dev == dev) {
+        cudaFree(it->second);
+        cached_ -= it->first.bytes;
+        it = free_.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+
+ private:
+  struct Key {
+    int dev;
+    size_t bytes;
+    bool operator<(const Key& o) const { return dev != o.dev ? dev < o.dev : bytes < o.bytes; }
+  };
+  static size_t round(size_t b) {
+    if (b < 256) return 256;
+    if (b < (2u << 20)) return (b + 255) & ~(size_t)255;
+    return (b + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1);
+  }
+  static constexpr size_t kCap = (size_t)48 << 30;  // at most 48 GiB kept cached
+  std::mutex mu_;
+  std::multimap<Key, void*> free_;
+  size_t cached_ = 0;
+};
+
+}  // namespace
+
+namespace vr {
+// pinned host blocks: exact-size reuse (the same workload repeats its shapes)
+namespace {
+std::mutex g_pin_mu;
+std::multimap<size_t, void*> g_pin_free;
+size_t g_pin_cached = 0;
+constexpr size_t kPinCap = (size_t)16 << 30;
+}  // namespace
+void* pinned_acquire(size_t& bytes) {
+  bytes = (bytes + 4095) & ~(size_t)4095;
+  {
+    std::lock_guard<std::mutex> g(g_pin_mu);
+    auto it = g_pin_free.lower_bound(bytes);
+    if (it != g_pin_free.end() && it->first <= bytes + bytes / 4) {
+      void* p = it->second;
+      bytes = it->first;
+      g_pin_cached -= bytes;
+      g_pin_free.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    p = std::malloc(bytes);  // pageable fallback (still correct, slower copies)
+    if (!p) throw std::bad_alloc();
+    bytes |= 1;              // low bit marks a malloc block
+  }
+  return p;
+}
+void pinned_release(void* p, size_t bytes) {
+  if (bytes & 1) { std::free(p); return; }
+  std::lock_guard<std::mutex> g(g_pin_mu);
+  if (g_pin_cached + bytes > kPinCap) { cudaFreeHost(p); return; }
+  g_pin_free.emplace(bytes, p);
+  g_pin_cached += bytes;
+}
+}  // namespace vr
+
+namespace {
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -56,8 +176,9 @@ struct DevBuf {
     return *this;
   }
   ~DevBuf() { release(); }
+  // the owner must have synchronised the stream that used the buffer
   void release() {
-    if (p) cudaFree(p);
+    if (p) DevCache::get().release(p, bytes);
     p = nullptr;
     bytes = 0;
   }
@@ -65,7 +186,7 @@ struct DevBuf {
     if (b <= bytes && p) return;
     release();
     if (b == 0) b = 16;
-    CUDA_TRY(cudaMalloc(&p, b));
+    p = DevCache::get().alloc(b);
     bytes = b;
   }
   template <class T> T* as() const { return (T*)p; }
@@ -144,6 +265,7 @@ struct vr_plan {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stage_ev[4];
   int used_events[4] = {0, 0, 0, 0};
   ~vr_plan() {
+    if (st) cudaStreamSynchronize(st);  // the device buffers go back to DevCache
     for (auto& v : stage_ev)
       for (auto& e : v) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     for (auto& e : ev)

@@ -1,5 +1,6 @@
 // vr_internal.h — host-side interfaces between the libvr translation units (not exported).
 #pragma once
+#include <algorithm>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -91,10 +92,53 @@ struct HostPairs {
     birth.push_back(b); death.push_back(d); birth_cidx.push_back(bc); death_cidx.push_back(dc);
   }
 };
+// Page-locked host array (cudaHostAlloc) from a process-wide cache, so the n*n rank
+// matrix comes back at full PCIe/C2C bandwidth and the next call reuses the pages.
+void* pinned_acquire(size_t& bytes);
+void pinned_release(void* p, size_t bytes);
+template <class T>
+class PinnedVec {
+ public:
+  PinnedVec() = default;
+  PinnedVec(const PinnedVec&) = delete;
+  PinnedVec& operator=(const PinnedVec&) = delete;
+  PinnedVec(PinnedVec&& o) noexcept { swap(o); }
+  PinnedVec& operator=(PinnedVec&& o) noexcept { if (this != &o) { reset(); swap(o); } return *this; }
+  ~PinnedVec() { reset(); }
+  void resize(size_t n) {  // contents are not preserved nor initialised
+    if (n * sizeof(T) > cap_) {
+      reset();
+      size_t b = n * sizeof(T);
+      p_ = (T*)pinned_acquire(b);
+      cap_ = b;
+    }
+    n_ = n;
+  }
+  template <class It> void assign(It a, It b) {
+    resize((size_t)(b - a));
+    std::copy(a, b, p_);
+  }
+  T* data() { return p_; }
+  const T* data() const { return p_; }
+  size_t size() const { return n_; }
+  bool empty() const { return n_ == 0; }
+  T& operator[](size_t i) { return p_[i]; }
+  const T& operator[](size_t i) const { return p_[i]; }
+  void reset() {
+    if (p_) pinned_release(p_, cap_);
+    p_ = nullptr; n_ = 0; cap_ = 0;
+  }
+
+ private:
+  void swap(PinnedVec& o) { std::swap(p_, o.p_); std::swap(n_, o.n_); std::swap(cap_, o.cap_); }
+  T* p_ = nullptr;
+  size_t n_ = 0, cap_ = 0;
+};
+
 struct HostMatrix {
   int64_t n = 0;
   std::vector<float> value;     // value[rank] = the fp32 distance with that rank
-  std::vector<uint32_t> rank;   // n*n
+  PinnedVec<uint32_t> rank;     // n*n
   std::vector<uint64_t> binom;  // (kmax+1)*(n+1)
   int kmax = 0;
   // optional threshold-graph adjacency (output-sensitive mode): neighbours descending

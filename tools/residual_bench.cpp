@@ -24,6 +24,12 @@ static std::vector<T> rd(const std::string& f) {
   return v;
 }
 
+// the library's pinned-host cache lives in vr_api.cu; plain heap blocks here
+namespace vr {
+void* pinned_acquire(size_t& bytes) { return std::malloc(bytes); }
+void pinned_release(void* p, size_t) { std::free(p); }
+}  // namespace vr
+
 int main(int argc, char** argv) {
   std::string dir = argv[1];
   int d = std::atoi(argv[2]);
@@ -34,7 +40,10 @@ int main(int argc, char** argv) {
   std::fclose(fp);
   vr::HostMatrix M;
   M.n = n; M.kmax = kmax;
-  M.rank = rd<uint32_t>(dir + "/rank.bin");
+  {
+    auto v = rd<uint32_t>(dir + "/rank.bin");
+    M.rank.assign(v.begin(), v.end());
+  }
   M.value = rd<float>(dir + "/values.bin");
   M.binom.resize((size_t)(kmax + 1) * (size_t)(n + 1));
   for (int k = 0; k <= kmax; ++k)
