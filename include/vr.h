@@ -248,6 +248,68 @@ int vr_hypha_pivots(const int64_t* col_ptr, const int32_t* rows, int64_t ncols, 
                     int32_t* low_out, vr_hypha_stats* stats);
 
 /* ----------------------------------------------------------------------------------
+ * Min-cost flow (§6.3.7, Def 6.2.2 / Eq 6.38; SURVEY.md §8(f) NEXT-4 component):
+ * the uncapacitated transshipment problem — nodes 0..nodes-1 with integer supply (Σ = 0;
+ * positive = source), arcs tail[a] -> head[a] with cost[a] >= 0 (finite) and no capacity;
+ * *total_cost = min Σ cost·flow.  Primal network simplex with block search pivot (block
+ * √arcs), host C++, no GPU needed.  max_blocks > 0 stops after that many searched blocks
+ * (the C√(mn)+b criterion of P:7112; stats->optimal = 0 then); 0 = run to optimality.
+ * VR_EINPUT: supplies not balanced, an arc out of range / negative / non-finite cost, or
+ * an infeasible network.
+ * ---------------------------------------------------------------------------------- */
+typedef struct {
+  int64_t pivots;      /* basis changes */
+  int64_t degenerate;  /* of which with zero flow change */
+  int64_t blocks;      /* arc blocks searched */
+  int32_t optimal;     /* 1 = no arc with a negative reduced cost left */
+  int32_t infeasible;  /* 1 = an artificial arc still carries flow */
+} vr_mcf_stats;
+int vr_min_cost_flow(int64_t nodes, const int64_t* supply, int64_t arcs, const int32_t* tail, const int32_t* head,
+                     const double* cost, int64_t max_blocks, double* total_cost, vr_mcf_stats* stats);
+
+/* ----------------------------------------------------------------------------------
+ * PDoptFlow (PAPER.md Ch.6, Alg 22): the 1-Wasserstein distance
+ * (Eq 6.36, l2 ground metric, unmatched points go to the diagonal at (d-b)/√2) between two
+ * persistence diagrams A (nA points) and B (nB points), each point (birth, death) as two
+ * fp32 (the layout of vr_pair), finite.  s > 0: the (1+O(ε)) approximation — RWMD lower
+ * bound (Alg 20), δ-condensation (Alg 21, seeded perturbation), s-WSPD spanner on a split
+ * tree (Algs 23-25), diagonal arcs (Alg 26), min-cost flow by network simplex; the
+ * guaranteed band is stats.bound_lo·W1 <= *w1 <= stats.bound_hi·W1 (Prop 6.3.2 x
+ * Thm 6.3.6, for s > 2).  s <= 0 or VR_W1_EXACT: the exact W1 (complete network on the
+ * 0-condensed points).  VR_W1_NO_CONDENSE: spanner without δ-condensation.  max_blocks as
+ * in vr_min_cost_flow.  Device work on the current device, default stream.
+ * ---------------------------------------------------------------------------------- */
+#define VR_W1_EXACT 1
+#define VR_W1_NO_CONDENSE 2
+typedef struct {
+  int64_t points_a, points_b;  /* input points */
+  int64_t nodes;               /* network nodes (condensed points + the two diagonal nodes) */
+  int64_t arcs;                /* network arcs after de-duplication */
+  int64_t wspd_pairs;          /* s-WSPD pairs (biarcs) */
+  int64_t tree_height;         /* split tree height */
+  int64_t pivots, degenerate, blocks;
+  int32_t optimal;             /* 1 = the simplex ran to optimality */
+  int32_t condensed;           /* 1 = δ-condensation applied */
+  double rwmd;                 /* L of Alg 20 (0 in exact mode) */
+  double delta;                /* δ of Alg 21 line 7 (0 = not condensed) */
+  double eps_condense;         /* ε of Alg 21 line 3-6 */
+  double eps_spanner;          /* ε' = 4/s + 4/(s-2) (Thm 6.3.6) */
+  double bound_lo, bound_hi;   /* guaranteed band around the exact W1 */
+  double ms_h2d, ms_rwmd, ms_condense, ms_tree, ms_wspd, ms_arcs, ms_d2h, ms_build, ms_simplex, ms_total;
+} vr_w1_stats;
+int vr_w1(const float* A, int64_t nA, const float* B, int64_t nB, double s, uint64_t seed, int32_t flags,
+          int64_t max_blocks, double* w1, vr_w1_stats* stats);
+/* the network of Alg 22 lines 1-5 (tests, inspection): nodes = condensed points then ā
+   (absorbs A) then b̄ (feeds B); xy of the diagonal nodes is NaN */
+typedef struct vr_w1_net vr_w1_net;
+int vr_w1_network(const float* A, int64_t nA, const float* B, int64_t nB, double s, uint64_t seed, int32_t flags,
+                  vr_w1_net** out, vr_w1_stats* stats);
+int64_t vr_w1_net_nodes(const vr_w1_net* net);
+int64_t vr_w1_net_arcs(const vr_w1_net* net);
+void vr_w1_net_get(const vr_w1_net* net, double* xy, int64_t* supply, int32_t* tail, int32_t* head, double* cost);
+void vr_w1_net_free(vr_w1_net* net);
+
+/* ----------------------------------------------------------------------------------
  * Component entry (tests): the library's device radix sort on
  * caller keys.  keys: HOST pointer to n uint64 values, sorted ascending in place on bits
  * [begin_bit, end_bit) (LSD, stable; bits outside the range do not take part in the

@@ -104,7 +104,9 @@ def min_cost_flow(supply, tail, head, cost) -> float:
     cols = np.concatenate([np.arange(m), np.arange(m)])
     vals = np.concatenate([np.ones(m), -np.ones(m)])
     Aeq = coo_matrix((vals, (rows, cols)), shape=(n, m)).tocsr()
-    res = linprog(cost, A_eq=Aeq, b_eq=supply, bounds=(0, None), method="highs")
+    # HiGHS' default feasibility tolerances (1e-7) are coarser than the 1e-9 parity bar
+    res = linprog(cost, A_eq=Aeq, b_eq=supply, bounds=(0, None), method="highs",
+                  options={"primal_feasibility_tolerance": 1e-10, "dual_feasibility_tolerance": 1e-10})
     if res.status != 0:
         raise ValueError(f"min-cost flow LP failed: {res.message}")
     return float(res.fun)

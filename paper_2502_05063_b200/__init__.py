@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-__all__ = ["barcodes", "barcodes_device", "radix_sort_u64", "hypha_pivots", "Plan", "Barcode", "VRError", "lib_path", "load"]
+__all__ = ["barcodes", "barcodes_device", "radix_sort_u64", "hypha_pivots", "min_cost_flow", "w1", "w1_network", "Plan", "Barcode", "VRError", "lib_path", "load"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_HERE, "libvr.so")
@@ -91,6 +91,13 @@ def load() -> ctypes.CDLL:
         "vr_plan_free": (None, [vp]),
         "vr_radix_sort_u64": (ctypes.c_int, [vp, i64, i32, i32]),
         "vr_hypha_pivots": (ctypes.c_int, [vp, vp, i64, vp, i32, vp, vp]),
+        "vr_min_cost_flow": (ctypes.c_int, [i64, vp, i64, vp, vp, vp, i64, vp, vp]),
+        "vr_w1": (ctypes.c_int, [vp, i64, vp, i64, ctypes.c_double, ctypes.c_uint64, i32, i64, vp, vp]),
+        "vr_w1_network": (ctypes.c_int, [vp, i64, vp, i64, ctypes.c_double, ctypes.c_uint64, i32, vp, vp]),
+        "vr_w1_net_nodes": (i64, [vp]),
+        "vr_w1_net_arcs": (i64, [vp]),
+        "vr_w1_net_get": (None, [vp, vp, vp, vp, vp, vp]),
+        "vr_w1_net_free": (None, [vp]),
         "vr_dist_begin": (ctypes.c_int, [vp, i64, i32, f32, vp, vp, i32, i32, ctypes.POINTER(vp)]),
         "vr_dist_dim_local": (ctypes.c_int, [vp, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
         "vr_dist_copy_keys": (ctypes.c_int, [vp, i32, vp]),
@@ -230,6 +237,84 @@ def hypha_pivots(col_ptr, rows, dims=None, compression: bool = True, clearing: b
                                (1 if compression else 0) | (2 if clearing else 0),
                                low.ctypes.data, ctypes.byref(st)))
     return low[:n], {f: getattr(st, f) for f, _ in _HyphaStats._fields_}
+
+
+class _McfStats(ctypes.Structure):
+    _fields_ = [("pivots", ctypes.c_int64), ("degenerate", ctypes.c_int64), ("blocks", ctypes.c_int64),
+                ("optimal", ctypes.c_int32), ("infeasible", ctypes.c_int32)]
+
+
+def min_cost_flow(supply, tail, head, cost, max_blocks: int = 0):
+    """Uncapacitated min-cost flow (network simplex, block search): (total cost, stats)."""
+    lib = load()
+    sp = np.ascontiguousarray(supply, dtype=np.int64)
+    t = np.ascontiguousarray(tail, dtype=np.int32)
+    h = np.ascontiguousarray(head, dtype=np.int32)
+    c = np.ascontiguousarray(cost, dtype=np.float64)
+    out = ctypes.c_double(0.0)
+    st = _McfStats()
+    _check(lib.vr_min_cost_flow(sp.size, sp.ctypes.data if sp.size else None, t.size, t.ctypes.data if t.size else None,
+                                h.ctypes.data if h.size else None, c.ctypes.data if c.size else None, int(max_blocks),
+                                ctypes.byref(out), ctypes.byref(st)))
+    return out.value, {f: getattr(st, f) for f, _ in _McfStats._fields_}
+
+
+W1_EXACT = 1
+W1_NO_CONDENSE = 2
+
+
+class _W1Stats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int64) for k in ("points_a", "points_b", "nodes", "arcs", "wspd_pairs", "tree_height",
+                                                "pivots", "degenerate", "blocks")] + \
+               [("optimal", ctypes.c_int32), ("condensed", ctypes.c_int32)] + \
+               [(k, ctypes.c_double) for k in ("rwmd", "delta", "eps_condense", "eps_spanner", "bound_lo", "bound_hi",
+                                                 "ms_h2d", "ms_rwmd", "ms_condense", "ms_tree", "ms_wspd", "ms_arcs",
+                                                 "ms_d2h", "ms_build", "ms_simplex", "ms_total")]
+
+
+def _diagram(P):
+    P = np.ascontiguousarray(np.asarray(P, dtype=np.float32).reshape(-1, 2))
+    return P, P.shape[0]
+
+
+def _w1_flags(exact, condense):
+    return (W1_EXACT if exact else 0) | (0 if condense else W1_NO_CONDENSE)
+
+
+def w1(A, B, s: float = 18.0, seed: int = 0, exact: bool = False, condense: bool = True, max_blocks: int = 0):
+    """PDoptFlow (Ch.6): W1 between diagrams A, B ((n, 2) birth/death): (value, stats)."""
+    lib = load()
+    A, na = _diagram(A)
+    B, nb = _diagram(B)
+    out = ctypes.c_double(0.0)
+    st = _W1Stats()
+    _check(lib.vr_w1(A.ctypes.data if na else None, na, B.ctypes.data if nb else None, nb, float(s), int(seed) & (2**64 - 1),
+                     _w1_flags(exact, condense), int(max_blocks), ctypes.byref(out), ctypes.byref(st)))
+    return out.value, {f: getattr(st, f) for f, _ in _W1Stats._fields_}
+
+
+def w1_network(A, B, s: float = 18.0, seed: int = 0, exact: bool = False, condense: bool = True):
+    """The transshipment network PDoptFlow builds (Alg 22 lines 1-5), as numpy arrays."""
+    lib = load()
+    A, na = _diagram(A)
+    B, nb = _diagram(B)
+    h = ctypes.c_void_p()
+    st = _W1Stats()
+    _check(lib.vr_w1_network(A.ctypes.data if na else None, na, B.ctypes.data if nb else None, nb, float(s),
+                             int(seed) & (2**64 - 1), _w1_flags(exact, condense), ctypes.byref(h), ctypes.byref(st)))
+    try:
+        N = lib.vr_w1_net_nodes(h)
+        M = lib.vr_w1_net_arcs(h)
+        xy = np.zeros((max(N, 1), 2), np.float64)
+        sup = np.zeros(max(N, 1), np.int64)
+        t = np.zeros(max(M, 1), np.int32)
+        hd = np.zeros(max(M, 1), np.int32)
+        c = np.zeros(max(M, 1), np.float64)
+        lib.vr_w1_net_get(h, xy.ctypes.data, sup.ctypes.data, t.ctypes.data, hd.ctypes.data, c.ctypes.data)
+    finally:
+        lib.vr_w1_net_free(h)
+    return {"xy": xy[:N], "supply": sup[:N], "tail": t[:M], "head": hd[:M], "cost": c[:M],
+            "stats": {f: getattr(st, f) for f, _ in _W1Stats._fields_}}
 
 
 def radix_sort_u64(keys: np.ndarray, begin_bit: int = 0, end_bit: int = 64) -> np.ndarray:

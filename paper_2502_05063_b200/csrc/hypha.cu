@@ -76,7 +76,6 @@ __global__ void k_set_unstable(const uint8_t* __restrict__ stable, int64_t n, in
 }  // namespace vr
 
 namespace {
-thread_local std::string g_hypha_err;
 
 // device workspace kept across calls (grown on demand), one per device
 struct HyphaWs {
@@ -175,7 +174,7 @@ extern "C" int vr_hypha_pivots(const int64_t* col_ptr, const int32_t* rows, int6
     if (stats) *stats = st;
     return VR_OK;
   } catch (const std::exception& e) {
-    g_hypha_err = e.what();
+    vr::set_last_error(e.what());
     return VR_EDEVICE;
   }
 }

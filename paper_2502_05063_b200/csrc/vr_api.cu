@@ -164,6 +164,16 @@ void pinned_release(void* p, size_t bytes) {
 
 namespace {
 
+}  // namespace
+
+namespace vr {
+void set_last_error(const std::string& msg) { g_err = msg; }
+void* dev_acquire(size_t& bytes) { return DevCache::get().alloc(bytes); }
+void dev_release(void* p, size_t bytes) { DevCache::get().release(p, bytes); }
+}  // namespace vr
+
+namespace {
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;

@@ -95,6 +95,11 @@ struct HostPairs {
 // Page-locked host array (cudaHostAlloc) from a process-wide cache, so the n*n rank
 // matrix comes back at full PCIe/C2C bandwidth and the next call reuses the pages.
 void* pinned_acquire(size_t& bytes);
+// message returned by vr_last_error() (thread-local)
+void set_last_error(const std::string& msg);
+// device blocks from the process-wide cache (vr_api.cu); bytes is rounded up on return
+void* dev_acquire(size_t& bytes);
+void dev_release(void* p, size_t bytes);
 void pinned_release(void* p, size_t bytes);
 template <class T>
 class PinnedVec {
@@ -164,5 +169,14 @@ void residual_reduce(const HostMatrix& M, int d, uint32_t maxr, int cbits, const
 void hypha_host_reduce(const int64_t* col_ptr, const int32_t* rows, int64_t n, const int32_t* dims, int32_t flags,
                        const int32_t* Left, int32_t* Lookup, const uint8_t* stable, const int32_t* u, int64_t nu,
                        vr_hypha_stats& st);
+
+// Uncapacitated min-cost flow, primal network simplex with block search (netsimplex.cpp).
+struct McfResult {
+  double cost = 0;
+  int64_t pivots = 0, degenerate = 0, blocks = 0;
+  bool optimal = false, infeasible = false, unbounded = false;
+};
+McfResult network_simplex(int64_t nodes, const int64_t* supply, int64_t arcs, const int32_t* tail, const int32_t* head,
+                          const double* cost, int64_t max_blocks);
 
 }  // namespace vr
