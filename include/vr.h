@@ -263,6 +263,8 @@ typedef struct {
   int64_t blocks;      /* arc blocks searched */
   int32_t optimal;     /* 1 = no arc with a negative reduced cost left */
   int32_t infeasible;  /* 1 = an artificial arc still carries flow */
+  double ms_pricing;   /* time in the block search */
+  double ms_update;    /* time in the basis updates */
 } vr_mcf_stats;
 int vr_min_cost_flow(int64_t nodes, const int64_t* supply, int64_t arcs, const int32_t* tail, const int32_t* head,
                      const double* cost, int64_t max_blocks, double* total_cost, vr_mcf_stats* stats);
@@ -281,21 +283,26 @@ int vr_min_cost_flow(int64_t nodes, const int64_t* supply, int64_t arcs, const i
  * ---------------------------------------------------------------------------------- */
 #define VR_W1_EXACT 1
 #define VR_W1_NO_CONDENSE 2
+#define VR_W1_WARM_DIAGONAL 4 /* start the simplex from the all-to-diagonal basis (default: big-M) */
 typedef struct {
   int64_t points_a, points_b;  /* input points */
   int64_t nodes;               /* network nodes (condensed points + the two diagonal nodes) */
   int64_t arcs;                /* network arcs after de-duplication */
   int64_t wspd_pairs;          /* s-WSPD pairs (biarcs) */
   int64_t tree_height;         /* split tree height */
+  int64_t wspd_levels;         /* frontier passes of the level-synchronous WSPD */
   int64_t pivots, degenerate, blocks;
   int32_t optimal;             /* 1 = the simplex ran to optimality */
   int32_t condensed;           /* 1 = δ-condensation applied */
+  int32_t warm_start;          /* 1 = the simplex started from the all-to-diagonal basis */
+  int32_t pad_;
   double rwmd;                 /* L of Alg 20 (0 in exact mode) */
   double delta;                /* δ of Alg 21 line 7 (0 = not condensed) */
   double eps_condense;         /* ε of Alg 21 line 3-6 */
   double eps_spanner;          /* ε' = 4/s + 4/(s-2) (Thm 6.3.6) */
   double bound_lo, bound_hi;   /* guaranteed band around the exact W1 */
   double ms_h2d, ms_rwmd, ms_condense, ms_tree, ms_wspd, ms_arcs, ms_d2h, ms_build, ms_simplex, ms_total;
+  double ms_pricing, ms_update; /* of ms_simplex: block search, basis update */
 } vr_w1_stats;
 int vr_w1(const float* A, int64_t nA, const float* B, int64_t nB, double s, uint64_t seed, int32_t flags,
           int64_t max_blocks, double* w1, vr_w1_stats* stats);

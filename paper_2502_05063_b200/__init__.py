@@ -241,7 +241,8 @@ def hypha_pivots(col_ptr, rows, dims=None, compression: bool = True, clearing: b
 
 class _McfStats(ctypes.Structure):
     _fields_ = [("pivots", ctypes.c_int64), ("degenerate", ctypes.c_int64), ("blocks", ctypes.c_int64),
-                ("optimal", ctypes.c_int32), ("infeasible", ctypes.c_int32)]
+                ("optimal", ctypes.c_int32), ("infeasible", ctypes.c_int32), ("ms_pricing", ctypes.c_double),
+                ("ms_update", ctypes.c_double)]
 
 
 def min_cost_flow(supply, tail, head, cost, max_blocks: int = 0):
@@ -265,11 +266,13 @@ W1_NO_CONDENSE = 2
 
 class _W1Stats(ctypes.Structure):
     _fields_ = [(k, ctypes.c_int64) for k in ("points_a", "points_b", "nodes", "arcs", "wspd_pairs", "tree_height",
-                                                "pivots", "degenerate", "blocks")] + \
-               [("optimal", ctypes.c_int32), ("condensed", ctypes.c_int32)] + \
+                                                "wspd_levels", "pivots", "degenerate", "blocks")] + \
+               [("optimal", ctypes.c_int32), ("condensed", ctypes.c_int32), ("warm_start", ctypes.c_int32),
+                ("pad_", ctypes.c_int32)] + \
                [(k, ctypes.c_double) for k in ("rwmd", "delta", "eps_condense", "eps_spanner", "bound_lo", "bound_hi",
                                                  "ms_h2d", "ms_rwmd", "ms_condense", "ms_tree", "ms_wspd", "ms_arcs",
-                                                 "ms_d2h", "ms_build", "ms_simplex", "ms_total")]
+                                                 "ms_d2h", "ms_build", "ms_simplex", "ms_total",
+                                                 "ms_pricing", "ms_update")]
 
 
 def _diagram(P):
@@ -277,11 +280,15 @@ def _diagram(P):
     return P, P.shape[0]
 
 
-def _w1_flags(exact, condense):
-    return (W1_EXACT if exact else 0) | (0 if condense else W1_NO_CONDENSE)
+W1_WARM_DIAGONAL = 4
 
 
-def w1(A, B, s: float = 18.0, seed: int = 0, exact: bool = False, condense: bool = True, max_blocks: int = 0):
+def _w1_flags(exact, condense, warm=False):
+    return (W1_EXACT if exact else 0) | (0 if condense else W1_NO_CONDENSE) | (W1_WARM_DIAGONAL if warm else 0)
+
+
+def w1(A, B, s: float = 18.0, seed: int = 0, exact: bool = False, condense: bool = True, max_blocks: int = 0,
+       warm: bool = False):
     """PDoptFlow (Ch.6): W1 between diagrams A, B ((n, 2) birth/death): (value, stats)."""
     lib = load()
     A, na = _diagram(A)
@@ -289,7 +296,7 @@ def w1(A, B, s: float = 18.0, seed: int = 0, exact: bool = False, condense: bool
     out = ctypes.c_double(0.0)
     st = _W1Stats()
     _check(lib.vr_w1(A.ctypes.data if na else None, na, B.ctypes.data if nb else None, nb, float(s), int(seed) & (2**64 - 1),
-                     _w1_flags(exact, condense), int(max_blocks), ctypes.byref(out), ctypes.byref(st)))
+                     _w1_flags(exact, condense, warm), int(max_blocks), ctypes.byref(out), ctypes.byref(st)))
     return out.value, {f: getattr(st, f) for f, _ in _W1Stats._fields_}
 
 

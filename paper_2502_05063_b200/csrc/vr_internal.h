@@ -174,9 +174,12 @@ void hypha_host_reduce(const int64_t* col_ptr, const int32_t* rows, int64_t n, c
 struct McfResult {
   double cost = 0;
   int64_t pivots = 0, degenerate = 0, blocks = 0;
-  bool optimal = false, infeasible = false, unbounded = false;
+  bool optimal = false, infeasible = false, unbounded = false, warm_start = false;
+  double ms_pricing = 0, ms_update = 0;
 };
+// init_pred / init_root (optional): a feasible spanning tree to start from (see the .cpp)
 McfResult network_simplex(int64_t nodes, const int64_t* supply, int64_t arcs, const int32_t* tail, const int32_t* head,
-                          const double* cost, int64_t max_blocks);
+                          const double* cost, int64_t max_blocks, const int32_t* init_pred = nullptr,
+                          int32_t init_root = -1);
 
 }  // namespace vr

@@ -191,41 +191,44 @@ __device__ __forceinline__ bool well_separated(const TNode& a, const TNode& b, d
 
 __device__ __forceinline__ double max_len(const TNode& a) { return fmax(a.x1 - a.x0, a.y1 - a.y0); }
 
-// FIND-PAIRS(w.left, w.right) for every internal node w, with an explicit stack of node
-// pairs in global scratch (depth <= 2·height + 2).  write = false: count (Alg 24);
-// write = true: emit (rep(u), rep(v)) at the thread's offset (Alg 25).
-template <bool WRITE>
-__global__ void k_wspd(const TNode* __restrict__ T, const int32_t* __restrict__ internal, int64_t ni, double s,
-                       int2* __restrict__ scratch, int stack_cap, uint32_t* __restrict__ counts,
-                       const uint64_t* __restrict__ offsets, int2* __restrict__ pairs, int* __restrict__ overflow) {
-  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int2* stk = scratch + tid * stack_cap;
-  for (int64_t k = tid; k < ni; k += nthreads) {
-    const TNode& w = T[internal[k]];
-    int sp = 0;
-    stk[sp++] = make_int2(w.left, w.right);
-    uint32_t cnt = 0;
-    uint64_t out = WRITE ? offsets[k] : 0;
-    while (sp > 0) {
-      const int2 uv = stk[--sp];
+// FIND-PAIRS of Algs 24/25, level-synchronous: the frontier holds node pairs (u, v) still
+// to examine (initially (w.left, w.right) for every internal node w, Alg 23); a separated
+// pair is emitted as (rep(u), rep(v)), otherwise the node with the longer box side is
+// split and both child pairs go to the next frontier.  The pairs emitted are exactly those
+// of the per-node recursion, and every level is one parallel pass, so the long chains of
+// the nodes near the root (the load imbalance of one thread per node) disappear.
+__global__ void k_wspd_level(const TNode* __restrict__ T, const int2* __restrict__ F, uint64_t nf, double s,
+                             int2* __restrict__ Fn, unsigned long long* __restrict__ nfn, int2* __restrict__ P,
+                             unsigned long long* __restrict__ np) {
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < nf; base += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = base + threadIdx.x;
+    bool emit = false, split = false;
+    int2 out = make_int2(0, 0), c0 = out, c1 = out;
+    if (i < nf) {
+      const int2 uv = F[i];
       const TNode& u = T[uv.x];
       const TNode& v = T[uv.y];
       if (well_separated(u, v, s)) {
-        if (WRITE) pairs[out++] = make_int2(u.rep, v.rep);
-        ++cnt;
-        continue;
-      }
-      if (sp + 2 > stack_cap) { atomicOr(overflow, 1); break; }
-      if (max_len(u) > max_len(v)) {
-        stk[sp++] = make_int2(u.right, uv.y);
-        stk[sp++] = make_int2(u.left, uv.y);
+        emit = true;
+        out = make_int2(u.rep, v.rep);
       } else {
-        stk[sp++] = make_int2(uv.x, v.right);
-        stk[sp++] = make_int2(uv.x, v.left);
+        split = true;
+        if (max_len(u) > max_len(v)) { c0 = make_int2(u.left, uv.y); c1 = make_int2(u.right, uv.y); }
+        else { c0 = make_int2(uv.x, v.left); c1 = make_int2(uv.x, v.right); }
       }
     }
-    if (!WRITE) counts[k] = cnt;
+    const unsigned long long pe = warp_append(emit, np);
+    if (emit) P[pe] = out;
+    const unsigned mask = __ballot_sync(0xffffffffu, split);
+    unsigned long long fb = 0;
+    const int lane = threadIdx.x & 31;
+    if (lane == 0 && mask) fb = atomicAdd(nfn, 2ull * (unsigned long long)__popc(mask));
+    fb = __shfl_sync(0xffffffffu, fb, 0);
+    if (split) {
+      const unsigned long long o = fb + 2ull * (unsigned long long)__popc(mask & lanemask_lt());
+      Fn[o] = c0;
+      Fn[o + 1] = c1;
+    }
   }
 }
 
@@ -410,8 +413,8 @@ int build_split_tree(const std::vector<double2>& P, std::vector<TNode>& T, std::
 struct W1Net {
   std::vector<double2> pos;       // N real nodes
   std::vector<int64_t> supply;    // N + 2 (ā = N, b̄ = N + 1)
-  std::vector<int32_t> tail, head;
-  std::vector<double> cost;
+  PinnedVec<int32_t> tail, head;  // page-locked: the arc arrays come back at full bandwidth
+  PinnedVec<double> cost;
 };
 
 void w1_build(const float* A, int64_t nA, const float* B, int64_t nB, double s, uint64_t seed, int32_t flags, W1Net& net,
@@ -537,31 +540,40 @@ void w1_build(const float* A, int64_t nA, const float* B, int64_t nB, double s, 
     Dev dT(std::max<size_t>(T.size(), 1) * sizeof(TNode)), dInt((size_t)std::max<int64_t>(ni, 1) * 4);
     if (!T.empty()) chk(cudaMemcpyAsync(dT.p, T.data(), T.size() * sizeof(TNode), cudaMemcpyHostToDevice, cs));
     if (ni) chk(cudaMemcpyAsync(dInt.p, internal.data(), (size_t)ni * 4, cudaMemcpyHostToDevice, cs));
-    const int stack_cap = 2 * height + 4;
-    const unsigned wg = grid_for(ni, 128);
-    const int64_t nthreads = (int64_t)wg * 128;
-    Dev dStack((size_t)nthreads * (size_t)stack_cap * sizeof(int2)), dCounts((size_t)std::max<int64_t>(ni, 1) * 4),
-        dOff((size_t)std::max<int64_t>(ni, 1) * 8), dOvf(16);
-    chk(cudaMemsetAsync(dOvf.p, 0, 16, cs));
     uint64_t npairs = 0;
     Dev dPairs;
     if (ni) {
-      k_wspd<false><<<wg, 128, 0, cs>>>(dT.as<TNode>(), dInt.as<int32_t>(), ni, s, dStack.as<int2>(), stack_cap,
-                                          dCounts.as<uint32_t>(), nullptr, nullptr, dOvf.as<int>());
-      chk(cudaGetLastError());
-      // exclusive prefix sum of the per-node counts (Alg 23 line 5), 64-bit
-      std::vector<uint32_t> cnt((size_t)ni);
-      chk(cudaMemcpy(cnt.data(), dCounts.p, (size_t)ni * 4, cudaMemcpyDeviceToHost));
-      std::vector<uint64_t> off((size_t)ni);
-      for (int64_t k = 0; k < ni; ++k) { off[(size_t)k] = npairs; npairs += cnt[(size_t)k]; }
-      chk(cudaMemcpy(dOff.p, off.data(), (size_t)ni * 8, cudaMemcpyHostToDevice));
-      dPairs.alloc(std::max<uint64_t>(npairs, 1) * sizeof(int2));
-      k_wspd<true><<<wg, 128, 0, cs>>>(dT.as<TNode>(), dInt.as<int32_t>(), ni, s, dStack.as<int2>(), stack_cap, nullptr,
-                                         dOff.as<uint64_t>(), dPairs.as<int2>(), dOvf.as<int>());
-      chk(cudaGetLastError());
-      int ovf = 0;
-      chk(cudaMemcpy(&ovf, dOvf.p, 4, cudaMemcpyDeviceToHost));
-      if (ovf) throw std::runtime_error("WSPD stack overflow");
+      std::vector<int2> f0((size_t)ni);
+      for (int64_t k = 0; k < ni; ++k) f0[(size_t)k] = make_int2(T[(size_t)internal[(size_t)k]].left, T[(size_t)internal[(size_t)k]].right);
+      uint64_t nf = (uint64_t)ni, pcap = std::max<uint64_t>(4 * (uint64_t)ni, 1024);
+      Dev dF(nf * sizeof(int2)), dCounters(16);
+      dPairs.alloc(pcap * sizeof(int2));
+      chk(cudaMemcpyAsync(dF.p, f0.data(), nf * sizeof(int2), cudaMemcpyHostToDevice, cs));
+      chk(cudaMemsetAsync(dCounters.p, 0, 16, cs));
+      while (nf) {
+        if (npairs + nf > pcap) {  // at most one emitted pair per frontier pair
+          const uint64_t ncap = std::max<uint64_t>(2 * pcap, npairs + nf);
+          Dev grown(ncap * sizeof(int2));
+          if (npairs) chk(cudaMemcpyAsync(grown.p, dPairs.p, npairs * sizeof(int2), cudaMemcpyDeviceToDevice, cs));
+          std::swap(grown.p, dPairs.p);
+          std::swap(grown.bytes, dPairs.bytes);
+          pcap = ncap;
+          chk(cudaStreamSynchronize(cs));
+        }
+        Dev dFn(2 * nf * sizeof(int2));
+        chk(cudaMemsetAsync(dCounters.p, 0, 8, cs));  // next frontier size; [1] = pairs so far
+        k_wspd_level<<<grid_for((int64_t)nf), 256, 0, cs>>>(dT.as<TNode>(), dF.as<int2>(), nf, s, dFn.as<int2>(),
+                                                            dCounters.as<unsigned long long>(), dPairs.as<int2>(),
+                                                            dCounters.as<unsigned long long>() + 1);
+        chk(cudaGetLastError());
+        unsigned long long c[2];
+        chk(cudaMemcpy(c, dCounters.p, 16, cudaMemcpyDeviceToHost));
+        nf = c[0];
+        npairs = c[1];
+        std::swap(dF.p, dFn.p);
+        std::swap(dF.bytes, dFn.bytes);
+        ++st.wspd_levels;
+      }
     }
     st.wspd_pairs = (int64_t)npairs;
     st.ms_wspd = ms_since(tt);
@@ -662,9 +674,9 @@ extern "C" void vr_w1_net_get(const vr_w1_net* h, double* xy, int64_t* supply, i
     for (size_t i = N; i < N + 2; ++i) xy[2 * i] = xy[2 * i + 1] = NAN;  // ā, b̄
   }
   if (supply) std::copy(n.supply.begin(), n.supply.end(), supply);
-  if (tail) std::copy(n.tail.begin(), n.tail.end(), tail);
-  if (head) std::copy(n.head.begin(), n.head.end(), head);
-  if (cost) std::copy(n.cost.begin(), n.cost.end(), cost);
+  if (tail) std::copy(n.tail.data(), n.tail.data() + n.tail.size(), tail);
+  if (head) std::copy(n.head.data(), n.head.data() + n.head.size(), head);
+  if (cost) std::copy(n.cost.data(), n.cost.data() + n.cost.size(), cost);
 }
 extern "C" void vr_w1_net_free(vr_w1_net* h) { delete h; }
 
@@ -678,8 +690,32 @@ extern "C" int vr_w1(const float* A, int64_t nA, const float* B, int64_t nB, dou
     vr_w1_stats st{};
     vr::w1_build(A, nA, B, nB, s, seed, flags, net, st);
     const auto t0 = std::chrono::steady_clock::now();
-    const vr::McfResult r = vr::network_simplex((int64_t)net.supply.size(), net.supply.data(), (int64_t)net.tail.size(),
-                                                net.tail.data(), net.head.data(), net.cost.data(), max_blocks);
+    // optional warm start (VR_W1_WARM_DIAGONAL): the all-to-diagonal basis — every node with net supply > 0
+    // drains into ā, every other node is fed from b̄, and b̄ -> ā carries the rest; rooted at
+    // b̄, zero flows point away from the root (strongly feasible)
+    const int64_t NN = (int64_t)net.supply.size();
+    const int64_t N = NN - 2;
+    std::vector<int32_t> pred((size_t)NN, -1), to_abar((size_t)std::max<int64_t>(N, 1), -1),
+        from_bbar((size_t)std::max<int64_t>(N, 1), -1);
+    int32_t bb_ab = -1;
+    for (size_t a = 0; a < net.tail.size(); ++a) {
+      const int32_t t = net.tail[a], h = net.head[a];
+      if (h == N && t < N) to_abar[(size_t)t] = (int32_t)a;
+      else if (t == N + 1 && h < N) from_bbar[(size_t)h] = (int32_t)a;
+      else if (t == N + 1 && h == N) bb_ab = (int32_t)a;
+    }
+    bool ok = bb_ab >= 0 && (flags & VR_W1_WARM_DIAGONAL);
+    pred[(size_t)N] = bb_ab;
+    for (int64_t v = 0; v < N && ok; ++v) {
+      pred[(size_t)v] = net.supply[(size_t)v] > 0 ? to_abar[(size_t)v] : from_bbar[(size_t)v];
+      ok = pred[(size_t)v] >= 0;
+    }
+    const vr::McfResult r = vr::network_simplex(NN, net.supply.data(), (int64_t)net.tail.size(), net.tail.data(),
+                                                net.head.data(), net.cost.data(), max_blocks, ok ? pred.data() : nullptr,
+                                                ok ? (int32_t)(N + 1) : -1);
+    st.warm_start = r.warm_start ? 1 : 0;
+    st.ms_pricing = r.ms_pricing;
+    st.ms_update = r.ms_update;
     st.ms_simplex = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     st.pivots = r.pivots;
     st.degenerate = r.degenerate;

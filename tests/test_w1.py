@@ -136,6 +136,15 @@ def test_rwmd_supplies_and_snapping(seed):
     assert net["supply"][:-2].sum() == len(A) - len(B)
 
 
+@pytest.mark.parametrize("seed", range(3))
+def test_warm_diagonal_start(seed):
+    A, B = _pairs(seed + 40)
+    a, st = _vr().w1(A, B, s=6, seed=seed, warm=True)
+    b, _ = _vr().w1(A, B, s=6, seed=seed)
+    assert st["warm_start"] == 1
+    assert a == pytest.approx(b, rel=1e-9, abs=1e-12)
+
+
 def test_determinism_and_seeds():
     vr = _vr()
     A, B = PD.gaussian(400, 1), PD.gaussian(350, 2)
