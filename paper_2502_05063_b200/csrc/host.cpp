@@ -22,6 +22,9 @@
 //                     only zeros to the left of f (Def 5.3.4), so no column left of f can
 //                     ever have its pivot there.
 #include <algorithm>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 #include <atomic>
 #include <thread>
 #include <functional>
@@ -91,10 +94,45 @@ struct Entry {
   bool operator==(const Entry& o) const { return r == o.r && cidx == o.cidx; }
 };
 
+// Dense scan of first_equal_cofacet_vertex, 8 vertices per step (AVX2): the first v
+// (descending) with max_q rows[q][v] <= r, skipping members of S.
+#if defined(__x86_64__)
+__attribute__((target("avx2"))) int64_t first_equal_dense_avx2(const uint32_t* const* rows, const int* S, int K, uint32_t r,
+                                                              int64_t n) {
+  const __m256i vr = _mm256_set1_epi32((int)(r ^ 0x80000000u));
+  const __m256i flip = _mm256_set1_epi32((int)0x80000000u);
+  int64_t v = n;
+  while (v >= 8) {
+    const int64_t b = v - 8;  // lanes b .. b+7
+    __m256i m = _mm256_loadu_si256((const __m256i*)(rows[0] + b));
+    for (int q = 1; q < K; ++q) m = _mm256_max_epu32(m, _mm256_loadu_si256((const __m256i*)(rows[q] + b)));
+    // m <= r (unsigned): !(m > r), signed compare after flipping the sign bit
+    const __m256i gt = _mm256_cmpgt_epi32(_mm256_xor_si256(m, flip), vr);
+    unsigned ok = ~(unsigned)_mm256_movemask_ps(_mm256_castsi256_ps(gt)) & 0xFFu;
+    while (ok) {
+      const int lane = 31 - __builtin_clz(ok);  // highest vertex first
+      const int64_t c = b + lane;
+      bool member = false;
+      for (int q = 0; q < K; ++q) member = member || S[q] == c;
+      if (!member) return c;
+      ok &= ~(1u << lane);
+    }
+    v = b;
+  }
+  for (int64_t c = v - 1; c >= 0; --c) {
+    bool ok = true;
+    for (int q = 0; q < K && ok; ++q) ok = (c != S[q]) && rows[q][c] <= r;
+    if (ok) return c;
+  }
+  return -1;
+}
+const bool g_host_avx2 = __builtin_cpu_supports("avx2");
+#endif
+
 struct Ctx {
   const HostMatrix& M;
   int d;  // column dimension
-  std::unordered_map<uint64_t, int64_t> apparent_memo;  // row cidx -> partner column cidx or -1
+  int64_t apparent_checks = 0;  // apparent_partner evaluations (the callers memoize)
   Ctx(const HostMatrix& m, int dd) : M(m), d(dd) {}
 
   void decode(uint64_t cidx, int k /*vertices*/, int* v) const {
@@ -181,6 +219,9 @@ struct Ctx {
       }
       return -1;
     }
+#if defined(__x86_64__)
+    if (g_host_avx2) return first_equal_dense_avx2(rows, S, K, r, M.n);
+#endif
     for (int64_t v = M.n - 1; v >= 0; --v) {
       bool ok = true;
       for (int q = 0; q < K && ok; ++q) ok = (v != S[q]) && rows[q][v] <= r;
@@ -190,8 +231,7 @@ struct Ctx {
   }
   // Is row t (a (d+1)-simplex of rank rt) the apparent cofacet of some column f?  Returns f.
   int64_t apparent_partner(uint64_t tcidx, uint32_t rt) {
-    auto it = apparent_memo.find(tcidx);
-    if (it != apparent_memo.end()) return it->second;
+    ++apparent_checks;
     int t[16];
     decode(tcidx, d + 2, t);
     int64_t res = -1;
@@ -211,7 +251,6 @@ struct Ctx {
       }
       break;  // only the youngest facet can be the apparent partner
     }
-    apparent_memo.emplace(tcidx, res);
     return res;
   }
   uint32_t diam_rank(const int* s) const {
@@ -462,6 +501,7 @@ void residual_reduce_t(const HostMatrix& M, int d, uint32_t maxr, int cbits, con
     }
   }
   std::sort(deaths_sorted.begin(), deaths_sorted.end());
+  st.apparent_checks += cx.apparent_checks;
 }
 
 // ------------------------------------------------------------------ parallel (speculative)

@@ -159,7 +159,7 @@ void dim0_union_find(int64_t n, const uint64_t* edges_sorted, uint64_t m, int kb
 // Residual reduction of the non-apparent, non-cleared columns of dimension d given in
 // coboundary order (keys ascending).  mode 0 = reduction matrix (V), 1 = oblivious.
 struct ResidualStats {
-  int64_t emergent = 0, additions = 0, coboundaries = 0;
+  int64_t emergent = 0, additions = 0, coboundaries = 0, apparent_checks = 0;
 };
 void residual_reduce(const HostMatrix& M, int d, uint32_t maxr, int cbits, const uint64_t* keys, uint64_t nkeys,
                      int mode, HostPairs& out, std::vector<uint64_t>& deaths_sorted, ResidualStats& st);

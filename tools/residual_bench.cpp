@@ -68,8 +68,8 @@ int main(int argc, char** argv) {
     std::printf("key rank %u\n", maxr - (unsigned)(keys[i] >> cbits));
     (void)cm;
   }
-  std::printf("d=%d mode=%d columns=%zu emergent=%lld additions=%lld coboundaries=%lld pairs=%zu positive=%zu ms=%.1f\n",
-              d, mode, keys.size(), (long long)st.emergent, (long long)st.additions, (long long)st.coboundaries,
+  std::printf("d=%d mode=%d columns=%zu emergent=%lld additions=%lld coboundaries=%lld apparent_checks=%lld pairs=%zu positive=%zu ms=%.1f\n",
+              d, mode, keys.size(), (long long)st.emergent, (long long)st.additions, (long long)st.coboundaries, (long long)st.apparent_checks,
               hp.birth.size(), pos, ms);
   return 0;
 }
