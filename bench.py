@@ -283,8 +283,16 @@ def run_ours(args, rank, world, local_rank):
     dom = max(kern, key=lambda k: kern[k][1])
     ops, ms = kern[dom]
     achieved = ops / (ms / 1000.0) / 1e12 if ms > 0 else None
+    traffic = None
+    try:  # DRAM bytes per step of the dominant kernel, from the committed ncu full capture
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        if dom in tr and cfg.name == "c2_s3_192" and D == 3:
+            traffic = sum(tr[dom].values())
+    except Exception:
+        pass
     roof = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": alu_peak, "unit": "Tops/s",
-            "frac": (achieved / alu_peak) if achieved else None, "traffic": None,
+            "frac": (achieved / alu_peak) if achieved else None, "traffic": traffic,
+            "traffic_unit": "DRAM bytes per step (all launches of the kernel), ncu --set full capture",
             "ops_per_step": ops, "ms_per_step": ms,
             "all": {k: {"ops": o, "ms": m, "tops": (o / (m / 1000.0) / 1e12) if m > 0 else None}
                     for k, (o, m) in kern.items()},

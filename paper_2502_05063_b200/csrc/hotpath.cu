@@ -43,6 +43,7 @@
 namespace vr {
 
 constexpr int HP_THREADS = 256;
+constexpr int64_t kWinMaxN = 544;  // shared-memory window up to n*144 B = 78 KB (3 CTAs/SM)
 
 // ------------------------------------------------------------------ phase 1: enumerate
 // Row-invariant parts of the upper prefix U = {u_D > ... > u_2}, reused by consecutive rows
@@ -58,7 +59,8 @@ struct UpperCache {
 
 template <int D>
 __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p, const HotBuffers& B, const int (&u)[D + 2],
-                                            UpperCache<D>& uc, unsigned long long& surv_acc, unsigned long long& app_acc,
+                                            UpperCache<D>& uc, const uint32_t* __restrict__ Wt, uint32_t* __restrict__ mw,
+                                            unsigned long long& surv_acc, unsigned long long& app_acc,
                                             unsigned long long& scan_acc, unsigned long long& clr_acc) {
   const int lane = threadIdx.x & 31;
   const int n = T.n;
@@ -125,6 +127,11 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
   // (RINF for a prefix vertex, so the warp skips it)
   const int vw = n - 1 - lane;
   const uint32_t mup0 = vw >= 0 ? umax(uc.mupU, __ldg(rowu[1] + vw)) : VR_RINF;
+  if (Wt) {  // the row's window maxima in shared memory, read 4 at a time by every lane
+    __syncwarp();
+    mw[lane] = mup0;
+    __syncwarp();
+  }
   const int steps = p.steps < n ? p.steps : n;
   const int steps4 = steps & ~3;  // whole groups of 4; the rest (n < steps) one by one
   const uint32_t* __restrict__ rowtop = T.rank + (size_t)(n - 1) * (size_t)n;  // row of v = n-1
@@ -176,23 +183,47 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
       }
     } else {
       // one vote per 4 vertices.  Inside the 32-vertex window the prefix part m comes from
-      // mup0 by a uniform-index shuffle and the step is branch-free: the load R[v][v0] is
-      // unconditional (row v, column v0 < n — in range, coalesced over the warp)
+      // mup0 and the new-edge rank R[v][v0] from the rank matrix; with the shared-memory
+      // window (p.win) both come 4 steps at a time: m4 = mw[j..j+3] (a broadcast) and
+      // r4 = Wt[v0][j..j+3] (the transposed window row of v0), so a step is a max, a
+      // compare and a select.  Otherwise m is shuffled from mup0 and R[v][v0] loaded
+      // (unconditionally: row v, column v0 < n — in range, coalesced over the warp).
       const size_t nn = (size_t)n;
       const int wsteps4 = (steps < 32 ? steps : 32) & ~3;
       int j = 0;
       bool any_active = true;
-      for (; j < wsteps4; j += 4, pv -= 4 * nn) {
+      if (Wt) {
+        const uint32_t* wrow = Wt + (size_t)(v0 < n ? v0 : n - 1) * 36;
+        int hitj = -1;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int v = n - 1 - (j + q);
-          const uint32_t m = __shfl_sync(0xffffffffu, mup0, j + q);
-          const uint32_t r = __ldg(pv - (size_t)q * nn);
-          const bool hit = active & (umax(m, r) <= rs);  // v = v0: R[v0][v0] = RINF
-          hitv = hit ? v : hitv;
-          active = active & !hit;
+        for (int g = 0; g < 8; ++g) {
+          const int jj = 4 * g;
+          if (jj >= wsteps4) break;
+          const uint4 m4 = *reinterpret_cast<const uint4*>(mw + jj);
+          const uint4 r4 = *reinterpret_cast<const uint4*>(wrow + jj);
+          bool h;
+          h = active & (umax(m4.x, r4.x) <= rs); hitj = h ? jj + 0 : hitj; active = active & !h;
+          h = active & (umax(m4.y, r4.y) <= rs); hitj = h ? jj + 1 : hitj; active = active & !h;
+          h = active & (umax(m4.z, r4.z) <= rs); hitj = h ? jj + 2 : hitj; active = active & !h;
+          h = active & (umax(m4.w, r4.w) <= rs); hitj = h ? jj + 3 : hitj; active = active & !h;
+          j = jj + 4;
+          if (!__any_sync(0xffffffffu, active)) { any_active = false; break; }
         }
-        if (!__any_sync(0xffffffffu, active)) { any_active = false; break; }
+        if (hitj >= 0) hitv = n - 1 - hitj;
+        pv -= (size_t)j * nn;
+      } else {
+        for (; j < wsteps4; j += 4, pv -= 4 * nn) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int v = n - 1 - (j + q);
+            const uint32_t m = __shfl_sync(0xffffffffu, mup0, j + q);
+            const uint32_t r = __ldg(pv - (size_t)q * nn);
+            const bool hit = active & (umax(m, r) <= rs);  // v = v0: R[v0][v0] = RINF
+            hitv = hit ? v : hitv;
+            active = active & !hit;
+          }
+          if (!__any_sync(0xffffffffu, active)) { any_active = false; break; }
+        }
       }
       if (any_active) {  // the rest of the budget, one vertex at a time (steps > 32 or n < 32)
         for (; j < steps; ++j, pv -= nn) {
@@ -262,12 +293,23 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
       app = true;
       uint32_t b[D + 1];
       uint32_t bup = 0;
+      const int jh = n - 1 - hitv;
+      uint32_t b0;
+      if (Wt && jh < 32) {  // R[u_i][hitv] = Wt[u_i][jh], R[hitv][v0] = Wt[v0][jh]
 #pragma unroll
-      for (int i = 1; i <= D; ++i) {
-        b[i] = __ldg(rowu[i] + hitv);
-        bup = umax(bup, b[i]);
+        for (int i = 1; i <= D; ++i) {
+          b[i] = Wt[(size_t)u[i] * 36 + jh];
+          bup = umax(bup, b[i]);
+        }
+        b0 = Wt[(size_t)v0 * 36 + jh];
+      } else {
+#pragma unroll
+        for (int i = 1; i <= D; ++i) {
+          b[i] = __ldg(rowu[i] + hitv);
+          bup = umax(bup, b[i]);
+        }
+        b0 = __ldg(rowtop - (size_t)jh * (size_t)n + v0);
       }
-      const uint32_t b0 = __ldg(rowtop - (size_t)(n - 1 - hitv) * (size_t)n + v0);
       if (v0 > hitv && umax(pm_up, bup) == rs) app = false;
 #pragma unroll
       for (int j = 1; j <= D; ++j) {
@@ -319,6 +361,23 @@ template <int D>
 __global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p, HotBuffers B) {
   const int GRAB = p.grab;
   const int lane = threadIdx.x & 31;
+  // shared-memory scan window (p.win): Wt[v][j] = R[n-1-j][v] for the 32 highest vertices
+  // (row stride 36 words: 16-byte aligned uint4 reads, conflict-free over 8-lane phases),
+  // then one 32-word row-maximum buffer per warp
+  extern __shared__ __align__(16) uint32_t hp_smem[];
+  uint32_t* Wt = nullptr;
+  uint32_t* mw = nullptr;
+  if (p.win) {
+    const int n = T.n;
+    for (int idx = threadIdx.x; idx < 32 * n; idx += blockDim.x) {
+      const int jj = idx / n, v = idx - jj * n;  // coalesced over v
+      const int row = n - 1 - jj;
+      hp_smem[(size_t)v * 36 + jj] = row >= 0 ? __ldg(T.rank + (size_t)row * (size_t)n + v) : VR_RINF;
+    }
+    __syncthreads();
+    Wt = hp_smem;
+    mw = hp_smem + (size_t)n * 36 + (size_t)(threadIdx.x >> 5) * 32;
+  }
   unsigned long long surv_acc = 0, app_acc = 0, scan_acc = 0, clr_acc = 0;
   // Rows are handed out from the LAST row down: the work of a row grows with its
   // smallest prefix vertex u_1 (row length), which grows with the row index, so the
@@ -362,7 +421,7 @@ __global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p,
         for (int j = D; j >= 1; --j)
           if (j < top) u[j] = u[top] - (top - j);
       }
-      process_row<D>(T, p, B, u, uc, surv_acc, app_acc, scan_acc, clr_acc);
+      process_row<D>(T, p, B, u, uc, Wt, mw, surv_acc, app_acc, scan_acc, clr_acc);
     }
   }
   if (lane == 0) {
@@ -528,7 +587,20 @@ static void enumerate_d(const DimParams& p, const Tables& T, const HotBuffers& B
   const uint64_t cap = (uint64_t)sm_count() * 8;  // 8 resident CTAs of 256 threads per SM
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  k_enumerate<D><<<(unsigned)blocks, HP_THREADS, 0, st>>>(T, p, B);
+  DimParams q = p;
+  size_t smem = 0;
+  if (q.variant == 1 && q.n >= 32 && q.n <= kWinMaxN) {
+    q.win = 1;
+    smem = (size_t)q.n * 36 * 4 + (HP_THREADS / 32) * 32 * 4;
+    static bool attr = false;  // per instantiation
+    if (!attr) {
+      cudaFuncSetAttribute(k_enumerate<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kWinMaxN * 36 * 4 + 1024));
+      attr = true;
+    }
+  } else {
+    q.win = 0;
+  }
+  k_enumerate<D><<<(unsigned)blocks, HP_THREADS, smem, st>>>(T, q, B);
 }
 
 template <int D>

@@ -42,6 +42,7 @@ struct DimParams {
   int shard_rank = 0;  // interleaved row shard: rows r with (row_end-1-r) % shard_world == shard_rank
   int shard_world = 1;
   uint64_t row_begin, row_end;  // prefix rows [row_begin, row_end) of the d-simplices
+  int win = 0;         // 1: k_enumerate stages the 32-vertex scan window in shared memory
 };
 struct DimCounters {   // device counters (unsigned long long each)
   unsigned long long survivors, apparent1, apparent2, cleared, queued, residual, row_next, app_pairs, scanned, scanned2, rows_out;
