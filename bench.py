@@ -265,7 +265,7 @@ def run_ours(args, rank, world, local_rank):
         tm = plan.timing()
     per = {k: stage[k] / args.steps for k in stage}
     # roofline of the dominant kernel: k_enumerate is ALU-bound —
-    # algorithmic work = rank comparisons of the method, sum_d (d+1)*(candidates_d + scanned_d);
+    # algorithmic work = SURVEY.md 8(d)'s integer-op figure (computed by the library);
     # peak = 148 SMs x 4 SMSPs x 16 lanes/clk (ALU pipe, IMNMX/ISETP) x measured max SM clock.
     peaks = {}
     try:
@@ -297,7 +297,9 @@ def run_ours(args, rank, world, local_rank):
             "all": {k: {"ops": o, "ms": m, "tops": (o / (m / 1000.0) / 1e12) if m > 0 else None}
                     for k, (o, m) in kern.items()},
             "peak_source": "derived: 148 SM x 64 ALU lanes/clk x sm_max_mhz (MEASURED_PEAKS.json); "
-                           "work = rank comparisons (d+1 per candidate and per scanned cofacet vertex)"}
+                           "work = SURVEY.md 8(d) per-unit figures: 2 integer ops per rank read (d per candidate, "
+                           "(d+1) per scanned cofacet vertex, C(d+2,2) per tested column) + (d+1)*ceil(log2 n) "
+                           "decode compares per tested column"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,

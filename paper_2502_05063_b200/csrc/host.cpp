@@ -127,6 +127,13 @@ __attribute__((target("avx2"))) int64_t first_equal_dense_avx2(const uint32_t* c
   return -1;
 }
 const bool g_host_avx2 = __builtin_cpu_supports("avx2");
+// out[i] = max(rs, max_q rows[q][lo + i]), i = 0..7
+__attribute__((target("avx2"))) void block_max8_avx2(const uint32_t* const* rows, int K, int64_t lo, uint32_t rs,
+                                                     uint32_t* out) {
+  __m256i m = _mm256_set1_epi32((int)rs);
+  for (int q = 0; q < K; ++q) m = _mm256_max_epu32(m, _mm256_loadu_si256((const __m256i*)(rows[q] + lo)));
+  _mm256_store_si256((__m256i*)out, m);
+}
 #endif
 
 struct Ctx {
@@ -184,19 +191,35 @@ struct Ctx {
       }
       return;
     }
+    // blocks of 8 vertices: the rank maxima of a block in one vector pass, then the
+    // (sequential) cofacet-index bookkeeping and the emits
     uint64_t below = cidx, above = 0;
     int k = d + 1, j = 0;
-    for (int64_t v = M.n - 1; v >= 0; --v) {
-      while (j <= d && v == s[j]) {
-        below -= M.C(s[j], k);
-        above += M.C(s[j], k + 1);
-        --k; ++j; --v;
+    alignas(32) uint32_t rb[8];
+    for (int64_t v = M.n - 1; v >= 0;) {
+      const int64_t lo = v >= 7 ? v - 7 : 0;
+#if defined(__x86_64__)
+      if (g_host_avx2 && v - lo == 7) block_max8_avx2(rows, d + 1, lo, rs, rb);
+      else
+#endif
+        for (int64_t u = lo; u <= v; ++u) {
+          uint32_t r = rs;
+          for (int q = 0; q <= d; ++q) r = std::max(r, rows[q][u]);
+          rb[u - lo] = r;
+        }
+      for (int64_t u = v; u >= lo; --u) {
+        if (j <= d && u == s[j]) {  // a vertex of s: one more vertex above the next cofacets
+          below -= M.C(s[j], k);
+          above += M.C(s[j], k + 1);
+          --k;
+          ++j;
+          continue;
+        }
+        const uint32_t r = rb[u - lo];
+        if (r == VR_RINF_H) continue;
+        if (!emit(Entry{r, above + M.C(u, k + 1) + below})) return;
       }
-      if (v < 0) break;
-      uint32_t r = rs;
-      for (int q = 0; q <= d; ++q) r = std::max(r, rows[q][v]);
-      if (r == VR_RINF_H) continue;
-      if (!emit(Entry{r, above + M.C(v, k + 1) + below})) return;
+      v = lo - 1;
     }
   }
   // first v (descending) not in S (K vertices) with max_{w in S} R[w][v] <= r, or -1

@@ -709,8 +709,21 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
   P.work_candidates += (double)cand;
   P.work_scanned += (double)hc.scanned;
   P.work_scanned2 += (double)hc.scanned2;
-  P.work_rank_ops += (double)(d + 1) * ((double)cand + (double)hc.scanned);
-  P.work_rank_ops2 += (double)(d + 1) * (double)hc.scanned2;
+  // algorithmic integer work, SURVEY.md §8(d) per-unit figures: 2 ops per rank read;
+  // a1 reads d ranks per candidate (hoisted prefix maxima); a5 reads (d+1) per scanned
+  // cofacet vertex plus C(d+2,2) for the facet check, and decodes each tested column with
+  // (d+1)·⌈log2 n⌉ compares
+  {
+    int lg = 0;
+    while (((int64_t)1 << lg) < n) ++lg;
+    const double tested = (double)hc.survivors - (double)hc.cleared;
+    const double cd2 = (double)(d + 2) * (double)(d + 1) / 2.0;
+    double queued = 0;
+    for (auto& c : dr.chunks) queued += (double)c.queued;
+    P.work_rank_ops += 2.0 * d * (double)cand + 2.0 * (d + 1) * (double)hc.scanned + 2.0 * cd2 * tested +
+                       (double)(d + 1) * lg * tested;
+    P.work_rank_ops2 += 2.0 * (d + 1) * (double)hc.scanned2 + (double)(d + 1) * lg * queued;
+  }
   P.survivors_total += stt.survivors;
   P.apparent_total += stt.apparent;
   return resid_count;
