@@ -207,13 +207,18 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint64_t* __restr
 // Tile ranking shared by the kernels below: stable per-warp-segment multisplit of keys_s
 // (cnt valid keys) on digit `shift`, writing the keys in digit order to sorted_s and the
 // tile's digit starts to dstart.  All 256 threads of the block must call it.
+// Stable in-shared-memory counting pass over cnt keys.  The keys are cut into RS_WARPS
+// contiguous warp segments of `seg` = cnt/RS_WARPS rounded up to whole warps, so a short
+// tile costs only the iterations it needs (the histogram, the prefix over warps and the
+// multisplit ranking all stay stable: earlier segments = earlier warps).
 __device__ __forceinline__ void rs_tile_rank(const uint64_t* keys_s, uint64_t* sorted_s, int cnt, int shift, uint32_t dmask,
                                              uint32_t* whist, uint32_t* dstart, uint32_t* warp_tot, uint32_t* total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int seg = ((cnt + RS_WARPS * 32 - 1) / (RS_WARPS * 32)) * 32;
   for (int i = threadIdx.x; i < RS_WARPS * RS_BINS; i += RS_THREADS) whist[i] = 0;
   __syncthreads();
-  const int seg0 = w * RS_SEG;
-  for (int i = seg0 + lane; i < seg0 + RS_SEG; i += 32)
+  const int seg0 = w * seg;
+  for (int i = seg0 + lane; i < seg0 + seg; i += 32)
     if (i < cnt) atomicAdd(&whist[w * RS_BINS + ((uint32_t)(keys_s[i] >> shift) & dmask)], 1u);
   __syncthreads();
   {
@@ -228,7 +233,7 @@ __device__ __forceinline__ void rs_tile_rank(const uint64_t* keys_s, uint64_t* s
     dstart[b] = block_exclusive_scan_256(run, warp_tot, total);
   }
   __syncthreads();
-  for (int i0 = seg0; i0 < seg0 + RS_SEG; i0 += 32) {
+  for (int i0 = seg0; i0 < seg0 + seg && i0 < cnt; i0 += 32) {
     const int i = i0 + lane;
     const bool valid = i < cnt;
     const uint64_t k = valid ? keys_s[i] : 0ull;
@@ -244,12 +249,13 @@ __device__ __forceinline__ void rs_tile_rank(const uint64_t* keys_s, uint64_t* s
   __syncthreads();
 }
 
-// Whole sort of n <= RS_TILE keys in one CTA, every pass in shared memory, one launch.
+// Whole sort of n <= RS_SMALL_CAP keys in one CTA, every pass in shared memory, one launch.
+constexpr int RS_SMALL_CAP = 2 * RS_TILE;
 __global__ void __launch_bounds__(RS_THREADS) rs_small(uint64_t* __restrict__ keys, int n, int begin_bit, int end_bit) {
   extern __shared__ __align__(16) unsigned char rs_smem[];
   uint64_t* A = (uint64_t*)rs_smem;
-  uint64_t* Bk = A + RS_TILE;
-  uint32_t* whist = (uint32_t*)(Bk + RS_TILE);
+  uint64_t* Bk = A + RS_SMALL_CAP;
+  uint32_t* whist = (uint32_t*)(Bk + RS_SMALL_CAP);
   uint32_t* dstart = whist + RS_WARPS * RS_BINS;
   __shared__ uint32_t warp_tot[SC_THREADS / 32];
   __shared__ uint32_t total;
@@ -371,14 +377,15 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit,
                          cudaStream_t st, int64_t* launches) {
   if (n <= 1 || end_bit <= begin_bit) return keys;
   const size_t smem = 2 * RS_TILE * sizeof(uint64_t) + (RS_WARPS * RS_BINS + 2 * RS_BINS) * sizeof(uint32_t);
+  const size_t smem_small = 2 * RS_SMALL_CAP * sizeof(uint64_t) + (RS_WARPS * RS_BINS + 2 * RS_BINS) * sizeof(uint32_t);
   if (!g_rs_attr_done) {
     cudaFuncSetAttribute(rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(rs_scatter_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(rs_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(rs_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_small);
     g_rs_attr_done = true;
   }
-  if (n <= (size_t)RS_TILE) {  // one CTA, all passes in shared memory
-    rs_small<<<1, RS_THREADS, smem, st>>>(keys, (int)n, begin_bit, end_bit);
+  if (n <= (size_t)RS_SMALL_CAP) {  // one CTA, all passes in shared memory
+    rs_small<<<1, RS_THREADS, smem_small, st>>>(keys, (int)n, begin_bit, end_bit);
     if (launches) *launches += 1;
     return keys;
   }

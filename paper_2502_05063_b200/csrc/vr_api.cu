@@ -557,7 +557,11 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
   p.maxr = P.maxr;
   p.cbits = cbits;
   p.steps = steps;
-  p.grab = P.world > 1 ? 1 : (P.opt.rows_per_grab > 0 ? P.opt.rows_per_grab : (n < 384 ? 4 : 1));
+  // rows per atomic grab: 4 amortises the grab and the upper-prefix work at small n; few
+  // rows (e.g. dimension 1: n rows) need every row on its own warp to fill the GPU
+  p.grab = P.world > 1 ? 1
+                       : (P.opt.rows_per_grab > 0 ? P.opt.rows_per_grab
+                                                  : ((n < 384 && binom_host((uint64_t)n, (uint64_t)d) >= 8192) ? 4 : 1));
   p.variant = P.opt.scan_variant > 0 ? P.opt.scan_variant - 1 : 1;
   // shards: dense rows (and the vertex rows of sparse dimension 1) are interleaved over
   // the ranks; sparse rows of d >= 2 are this rank's own survivors of d-1, which already

@@ -152,6 +152,23 @@ def test_apparent_phase_split_invariance(steps):
         assert a.stats[d]["apparent"] == b.stats[d]["apparent"]
 
 
+@pytest.mark.parametrize("grab", [1, 3, 16])
+@pytest.mark.parametrize("D", [1, 2, 3])
+def test_row_scheduling_invariance(grab, D):
+    # rows_per_grab: rows per atomic grab; the scan window in shared memory is used at
+    # n <= 544 and the global path above — both must agree
+    for n in (70, 600):
+        if n == 600 and D == 3:
+            continue
+        lt = G.random_cloud(n, 5)
+        a = vr.barcodes(lt, n, D, rows_per_grab=grab, index_pairs=True)
+        b = vr.barcodes(lt, n, D, index_pairs=True)
+        for d in range(D + 1):
+            assert np.array_equal(a.pairs[d], b.pairs[d])
+            assert {tuple(x) for x in a.index_pairs[d].tolist()} == {tuple(x) for x in b.index_pairs[d].tolist()}
+            assert a.stats[d]["survivors"] == b.stats[d]["survivors"]
+
+
 def test_residual_modes_agree():
     cfg = G.CONFIGS["c2_s3_192"]
     lt = cfg.lower_tri(60)
