@@ -37,7 +37,9 @@ __global__ void tb_edge_keys(const float* __restrict__ lt, uint64_t N, int kbits
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += (uint64_t)gridDim.x * blockDim.x) {
     float x = __ldg(lt + k);
     if (!(x >= 0.0f)) atomicOr(&out->err, 1u);  // NaN or negative
-    keys[k] = ((uint64_t)dist_bits(x) << kbits) | (N - 1 - k);
+    // stored at N-1-k: the array is then ordered by ~cidx, and a STABLE sort on the 31
+    // distance bits alone yields (distance, ~cidx) order — 4 radix passes instead of 6
+    keys[N - 1 - k] = ((uint64_t)dist_bits(x) << kbits) | (N - 1 - k);
   }
 }
 
@@ -128,7 +130,7 @@ void launch_tables(const float* d_lt, int64_t n, float threshold, uint64_t* keys
   if (N) {
     unsigned g = (unsigned)((N + 255) / 256 < 148u * 16u ? (N + 255) / 256 : 148u * 16u);
     tb_edge_keys<<<g, 256, 0, st>>>(d_lt, N, kbits, keys64, d_out);
-    sorted = radix_sort_u64(keys64, alt64, N, 0, 31 + kbits, sort_temp, st, launches);
+    sorted = radix_sort_u64(keys64, alt64, N, kbits, 31 + kbits, sort_temp, st, launches);
     *launches += 1;
   }
   tb_rowmax<<<(unsigned)n, 256, 0, st>>>(d_lt, n, rowmax);
