@@ -33,8 +33,10 @@ namespace vr {
 
 // also validates the matrix (rows strictly above the diagonal and ascending): a bad entry
 // raises *bad and is skipped, and the call returns VR_EINPUT
+// (also writes low(j), the last row of column j or -1, so k_set_lookup reads it coalesced)
 __global__ void k_set_leftmost(const int64_t* __restrict__ col_ptr, const int32_t* __restrict__ rows, int64_t n,
-                               int32_t* __restrict__ left, uint8_t* __restrict__ stable, int* __restrict__ bad) {
+                               int32_t* __restrict__ left, uint8_t* __restrict__ stable, int32_t* __restrict__ low,
+                               int* __restrict__ bad) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t a = col_ptr[j], b = col_ptr[j + 1];
     if (a == b) stable[j] = 1;
@@ -45,16 +47,15 @@ __global__ void k_set_leftmost(const int64_t* __restrict__ col_ptr, const int32_
       prev = r;
       atomicMin(left + r, (int32_t)j);
     }
+    low[j] = prev;
   }
 }
 
-__global__ void k_set_lookup(const int64_t* __restrict__ col_ptr, const int32_t* __restrict__ rows, int64_t n,
-                             const int32_t* __restrict__ left, int32_t* __restrict__ lookup, uint8_t* __restrict__ stable,
-                             int clearing) {
+__global__ void k_set_lookup(const int32_t* __restrict__ lows, int64_t n, const int32_t* __restrict__ left,
+                             int32_t* __restrict__ lookup, uint8_t* __restrict__ stable, int clearing) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t a = col_ptr[j], b = col_ptr[j + 1];
-    if (a == b) continue;
-    const int32_t low = rows[b - 1];  // rows ascending: the last is low(j)
+    const int32_t low = lows[j];  // rows ascending: the last is low(j); -1 = empty column
+    if (low < 0) continue;
     if (left[low] == (int32_t)j) {
       lookup[low] = (int32_t)j;
       stable[j] = 1;
@@ -135,6 +136,7 @@ extern "C" int vr_hypha_pivots(const int64_t* col_ptr, const int32_t* rows, int6
       auto* d_stable = (uint8_t*)ws.get(4, (size_t)n);
       auto* d_u = (int32_t*)ws.get(5, (size_t)n * 4);
       auto* d_cnt = (unsigned long long*)ws.get(6, 16);
+      auto* d_low = (int32_t*)ws.get(7, (size_t)n * 4);
       int* d_bad = (int*)(d_cnt + 1);
       if (!ws.e0) { chk(cudaEventCreate(&ws.e0)); chk(cudaEventCreate(&ws.e1)); }
       chk(cudaMemcpyAsync(d_ptr, col_ptr, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, 0));
@@ -146,8 +148,8 @@ extern "C" int vr_hypha_pivots(const int64_t* col_ptr, const int32_t* rows, int6
       cudaMemsetAsync(d_stable, 0, (size_t)n, 0);
       cudaMemsetAsync(d_cnt, 0, 16, 0);
       const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 16);
-      k_set_leftmost<<<grid, 256>>>(d_ptr, d_rows, n, d_left, d_stable, d_bad);
-      k_set_lookup<<<grid, 256>>>(d_ptr, d_rows, n, d_left, d_lookup, d_stable, (flags & VR_HYPHA_CLEARING) ? 1 : 0);
+      k_set_leftmost<<<grid, 256>>>(d_ptr, d_rows, n, d_left, d_stable, d_low, d_bad);
+      k_set_lookup<<<grid, 256>>>(d_low, n, d_left, d_lookup, d_stable, (flags & VR_HYPHA_CLEARING) ? 1 : 0);
       k_set_unstable<<<grid, 256>>>(d_stable, n, d_u, d_cnt);
       cudaEventRecord(ws.e1, 0);
       chk(cudaGetLastError());

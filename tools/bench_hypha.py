@@ -34,10 +34,10 @@ from datagen import clouds as G  # noqa: E402
 
 def scan_bytes(ptr, nnz, unstable):
     n = ptr.size - 1
-    # memsets (left, lookup 4 B, stable 1 B) + k_set_leftmost (col_ptr, rows, left written once)
-    # + k_set_lookup (col_ptr, low entry, left gather, lookup write, stable write)
+    # memsets (left, lookup 4 B, stable 1 B) + k_set_leftmost (col_ptr, rows, left written
+    # once, low written) + k_set_lookup (low, left gather, lookup write, stable write)
     # + k_set_unstable (stable read, u write)
-    return 9 * n + (8 * n + 4 * nnz + 4 * n) + (8 * n + 4 * n + 4 * n + 4 * n + 1 * n) + (1 * n + 4 * unstable)
+    return 9 * n + (8 * n + 4 * nnz + 4 * n + 4 * n) + (4 * n + 4 * n + 4 * n + 1 * n) + (1 * n + 4 * unstable)
 
 
 def main():

@@ -7,7 +7,7 @@ from datagen import clouds as G
 for name in sys.argv[1:]:
     cfg = G.CONFIGS[name]
     lt = torch.from_numpy(cfg.lower_tri()).cuda()
-    for grab in (1, 2, 4, 8, 16, 32, 64):
+    for grab in [int(g) for g in os.environ.get("GRABS", "1,2,4,8,16,32,64").split(",")]:
         plan = vr.Plan(lt, cfg.n, cfg.max_dim, cfg.threshold, rows_per_grab=grab)
         for _ in range(3):
             plan.replay()
