@@ -53,6 +53,19 @@ int main(int argc, char** argv) {
       else for (int i = 1; i <= k; ++i) c = c * (unsigned __int128)(v - k + i) / (unsigned)i;
       M.binom[(size_t)k * (size_t)(n + 1) + (size_t)v] = (uint64_t)c;
     }
+  if (std::getenv("VR_ADJ")) {  // threshold-graph adjacency as the output-sensitive mode builds it
+    M.adj_off.assign((size_t)n + 1, 0);
+    for (long long v = 0; v < n; ++v) {
+      for (long long w = n - 1; w >= 0; --w)
+        if (w != v && M.rank[(size_t)v * n + w] != 0xFFFFFFFFu) M.adj.push_back((uint16_t)w);
+      M.adj_off[(size_t)v + 1] = (uint32_t)M.adj.size();
+    }
+    if (!std::getenv("VR_NO_ADJ_RANK")) {
+      M.adj_rank.resize(M.adj.size());
+      for (long long v = 0; v < n; ++v)
+        for (uint32_t k = M.adj_off[(size_t)v]; k < M.adj_off[(size_t)v + 1]; ++k) M.adj_rank[k] = M.R(v, M.adj[k]);
+    }
+  }
   auto keys = rd<uint64_t>(dir + "/keys_d" + std::to_string(d) + ".bin");
   vr::HostPairs hp; std::vector<uint64_t> deaths; vr::ResidualStats st;
   auto t0 = std::chrono::steady_clock::now();
