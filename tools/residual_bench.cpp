@@ -60,11 +60,6 @@ int main(int argc, char** argv) {
         if (w != v && M.rank[(size_t)v * n + w] != 0xFFFFFFFFu) M.adj.push_back((uint16_t)w);
       M.adj_off[(size_t)v + 1] = (uint32_t)M.adj.size();
     }
-    if (!std::getenv("VR_NO_ADJ_RANK")) {
-      M.adj_rank.resize(M.adj.size());
-      for (long long v = 0; v < n; ++v)
-        for (uint32_t k = M.adj_off[(size_t)v]; k < M.adj_off[(size_t)v + 1]; ++k) M.adj_rank[k] = M.R(v, M.adj[k]);
-    }
   }
   auto keys = rd<uint64_t>(dir + "/keys_d" + std::to_string(d) + ".bin");
   vr::HostPairs hp; std::vector<uint64_t> deaths; vr::ResidualStats st;
