@@ -35,6 +35,10 @@
 //       binary search in the dimension-(d-1) residual deaths.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "vr_common.cuh"
@@ -432,6 +436,256 @@ __global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p,
   }
 }
 
+// ------------------------------------------------------------------ phase 1, flattened
+// Dense dimensions with the shared-memory window: the candidates of a "super-row" (all
+// d-simplices sharing the upper vertices u_D > ... > u_2) are the pairs (u_1, v_0),
+// v_0 < u_1 < u_2, numbered i = C(u_1, 2) + v_0 — so cidx = sum_{i>=2} C(u_i, i+1) + i —
+// and cut into chunks of FL_CHUNK consecutive i.  A warp takes one chunk per grab (largest
+// super-rows first) and its 32 lanes take consecutive i, across row boundaries: no ragged
+// row tails, and the per-row setup (prefix maxima, window, cidx base) becomes per-chunk.
+// Per lane the row-dependent parts (R[u_1][u_b], R[u_1][v] in the window) are read for the
+// lane's own u_1 (mostly shared by the warp).  Same tests and outputs as process_row.
+constexpr int FL_CHUNK = 1024;
+
+template <int D>
+__global__ void __launch_bounds__(HP_THREADS) k_enumerate_flat(Tables T, DimParams p, HotBuffers B,
+                                                               const uint32_t* __restrict__ chunk_start, uint32_t nsuper,
+                                                               uint32_t nchunks) {
+  const int lane = threadIdx.x & 31;
+  const int n = T.n;
+  extern __shared__ __align__(16) uint32_t hp_smem[];
+  for (int idx = threadIdx.x; idx < 32 * n; idx += blockDim.x) {
+    const int jj = idx / n, v = idx - jj * n;
+    const int row = n - 1 - jj;
+    hp_smem[(size_t)v * 36 + jj] = row >= 0 ? __ldg(T.rank + (size_t)row * (size_t)n + v) : VR_RINF;
+  }
+  __syncthreads();
+  const uint32_t* Wt = hp_smem;
+  uint32_t* mw = hp_smem + (size_t)n * 36 + (size_t)(threadIdx.x >> 5) * 32;  // window max over u_2..u_D
+  unsigned long long surv_acc = 0, app_acc = 0, scan_acc = 0, clr_acc = 0;
+  const int steps = p.steps < n ? p.steps : n;
+  const int wsteps4 = (steps < 32 ? steps : 32) & ~3;
+  const uint32_t* __restrict__ rowtop = T.rank + (size_t)(n - 1) * (size_t)n;
+  while (true) {
+    unsigned long long g0 = 0;
+    if (lane == 0) g0 = atomicAdd(&B.ctr->row_next, 1ull);
+    g0 = __shfl_sync(0xffffffffu, g0, 0);
+    if (g0 >= nchunks) break;
+    const uint32_t c = nchunks - 1 - (uint32_t)g0;
+    // super-row of chunk c: the last t with chunk_start[t] <= c
+    uint32_t lo = 0, hi = nsuper - 1;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (__ldg(chunk_start + mid) <= c) lo = mid; else hi = mid - 1;
+    }
+    const uint32_t t = lo;
+    int u[D + 2];
+    uint64_t cU = 0;
+    int u2 = n;
+    {
+      uint64_t x = t;
+      int h = n;
+#pragma unroll
+      for (int i = D; i >= 2; --i) {
+        const int vv = cns_find(T, x, i - 1, h);
+        u[i] = vv;
+        x -= binom(T, vv, i - 1);
+        cU += binom(T, vv, i + 1);
+        h = vv;
+      }
+      if (D >= 2) u2 = u[2];
+    }
+    const uint64_t cnt_sr = (uint64_t)u2 * (uint64_t)(u2 - 1) / 2;
+    const uint64_t i0 = (uint64_t)(c - __ldg(chunk_start + t)) * FL_CHUNK;
+    const uint64_t iend = (i0 + FL_CHUNK < cnt_sr) ? i0 + FL_CHUNK : cnt_sr;
+    // upper-prefix parts: pair maxima over u_2..u_D (all / avoiding u_j), window maxima
+    uint32_t pmU = 0, pmU_ex[D + 1];
+#pragma unroll
+    for (int j = 0; j <= D; ++j) pmU_ex[j] = 0;
+#pragma unroll
+    for (int a = 2; a <= D; ++a)
+#pragma unroll
+      for (int b = a + 1; b <= D; ++b) {
+        const uint32_t r = rank_at(T, u[a], u[b]);
+        pmU = umax(pmU, r);
+#pragma unroll
+        for (int j = 2; j <= D; ++j)
+          if (j != a && j != b) pmU_ex[j] = umax(pmU_ex[j], r);
+      }
+    {
+      const int v = n - 1 - lane;
+      uint32_t m = v >= 0 ? 0u : VR_RINF;
+#pragma unroll
+      for (int q = 2; q <= D; ++q) m = v >= 0 ? umax(m, Wt[(size_t)u[q] * 36 + lane]) : m;  // R[u_q][v]
+      __syncwarp();
+      mw[lane] = m;
+      __syncwarp();
+    }
+    if (pmU == VR_RINF) continue;  // every simplex of the super-row is over the threshold
+    for (uint64_t base = i0; base < iend; base += 32) {
+      const uint64_t i = base + (uint64_t)lane;
+      const bool valid = i < iend;
+      // (u_1, v_0) from i = C(u_1, 2) + v_0
+      int u1 = 1, v0 = 0;
+      if (valid) {
+        u1 = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)i)) * 0.5f);
+        while ((uint64_t)u1 * (uint64_t)(u1 - 1) / 2 > i) --u1;
+        while ((uint64_t)(u1 + 1) * (uint64_t)u1 / 2 <= i) ++u1;
+        v0 = (int)(i - (uint64_t)u1 * (uint64_t)(u1 - 1) / 2);
+      }
+      u[1] = u1;
+      const uint32_t* __restrict__ rowu1 = T.rank + (size_t)u1 * (size_t)n;
+      uint32_t a[D + 1];
+      uint32_t r1[D + 1];
+      uint32_t pm_up = pmU;
+#pragma unroll
+      for (int b = 2; b <= D; ++b) {
+        r1[b] = __ldg(rowu1 + u[b]);
+        pm_up = umax(pm_up, r1[b]);
+      }
+      uint32_t rs = pm_up;
+      a[1] = valid ? __ldg(rowu1 + v0) : VR_RINF;
+      rs = umax(rs, a[1]);
+#pragma unroll
+      for (int q = 2; q <= D; ++q) {
+        a[q] = valid ? rank_at(T, u[q], v0) : VR_RINF;
+        rs = umax(rs, a[q]);
+      }
+      const bool surv = valid && rs != VR_RINF;
+      const uint32_t msurv = __ballot_sync(0xffffffffu, surv);
+      if (!msurv) continue;
+      surv_acc += __popc(msurv);
+      const uint64_t cidx = cU + i;
+      bool cleared = false;
+      if (B.clr && surv) cleared = bit_test(B.clr, cidx);
+      clr_acc += __popc(__ballot_sync(0xffffffffu, cleared));
+      bool active = surv && !cleared;
+      int hitv = -1;
+      // scan: m_j = max(upper window mw[j], R[u_1][v_j] = Wt[u_1][j]), R[v_j][v_0] = Wt[v_0][j]
+      const uint32_t* wrow0 = Wt + (size_t)v0 * 36;
+      const uint32_t* wrow1 = Wt + (size_t)u1 * 36;
+      int j = 0;
+      bool any_active = true;
+      {
+        int hitj = -1;
+#pragma unroll
+        for (int gq = 0; gq < 8; ++gq) {
+          const int jj = 4 * gq;
+          if (jj >= wsteps4) break;
+          const uint4 mu = *reinterpret_cast<const uint4*>(mw + jj);
+          const uint4 m1 = *reinterpret_cast<const uint4*>(wrow1 + jj);
+          const uint4 r4 = *reinterpret_cast<const uint4*>(wrow0 + jj);
+          bool h;
+          h = active & (umax(umax(mu.x, m1.x), r4.x) <= rs); hitj = h ? jj + 0 : hitj; active = active & !h;
+          h = active & (umax(umax(mu.y, m1.y), r4.y) <= rs); hitj = h ? jj + 1 : hitj; active = active & !h;
+          h = active & (umax(umax(mu.z, m1.z), r4.z) <= rs); hitj = h ? jj + 2 : hitj; active = active & !h;
+          h = active & (umax(umax(mu.w, m1.w), r4.w) <= rs); hitj = h ? jj + 3 : hitj; active = active & !h;
+          j = jj + 4;
+          if (!__any_sync(0xffffffffu, active)) { any_active = false; break; }
+        }
+        if (hitj >= 0) hitv = n - 1 - hitj;
+      }
+      if (any_active) {  // beyond the window (steps > 32, or n % 4 leftovers)
+        for (; j < steps; ++j) {
+          const int v = n - 1 - j;
+          uint32_t m = 0;
+#pragma unroll
+          for (int q = 1; q <= D; ++q) m = umax(m, (q == 1) ? __ldg(rowu1 + v) : rank_at(T, u[q], v));
+          if (active && m <= rs && umax(m, __ldg(rowtop - (size_t)j * (size_t)n + v0)) <= rs) {
+            hitv = v;
+            active = false;
+          }
+          if (!__any_sync(0xffffffffu, active)) break;
+        }
+      }
+      const int examined = hitv >= 0 ? n - hitv : (active ? steps : 0);
+      scan_acc += (unsigned long long)__reduce_add_sync(0xffffffffu, (unsigned)examined);
+      // condition 2 (as in process_row)
+      bool app = false;
+      if (hitv >= 0) {
+        app = true;
+        uint32_t pm_ex[D + 1];
+        pm_ex[0] = 0;
+        pm_ex[1] = pmU;
+#pragma unroll
+        for (int jx = 2; jx <= D; ++jx) {
+          uint32_t m = pmU_ex[jx];
+#pragma unroll
+          for (int b = 2; b <= D; ++b)
+            if (b != jx) m = umax(m, r1[b]);
+          pm_ex[jx] = m;
+        }
+        uint32_t bb[D + 1];
+        uint32_t bup = 0;
+        const int jh = n - 1 - hitv;
+        uint32_t b0;
+        if (jh < 32) {
+#pragma unroll
+          for (int q = 1; q <= D; ++q) {
+            bb[q] = Wt[(size_t)u[q] * 36 + jh];
+            bup = umax(bup, bb[q]);
+          }
+          b0 = Wt[(size_t)v0 * 36 + jh];
+        } else {
+#pragma unroll
+          for (int q = 1; q <= D; ++q) {
+            bb[q] = rank_at(T, u[q], hitv);
+            bup = umax(bup, bb[q]);
+          }
+          b0 = rank_at(T, hitv, v0);
+        }
+        if (v0 > hitv && umax(pm_up, bup) == rs) app = false;
+#pragma unroll
+        for (int jx = 1; jx <= D; ++jx) {
+          if (u[jx] > hitv) {
+            uint32_t m = umax(pm_ex[jx], b0);
+#pragma unroll
+            for (int q = 1; q <= D; ++q)
+              if (q != jx) m = umax(m, umax(a[q], bb[q]));
+            if (m == rs) app = false;
+          }
+        }
+      }
+      app_acc += __popc(__ballot_sync(0xffffffffu, app));
+      if (app && (B.clr_next || B.app_pairs)) {
+        int sv[D + 1];
+#pragma unroll
+        for (int q = 0; q < D; ++q) sv[q] = u[D - q];
+        sv[D] = v0;
+        const uint64_t tc = cofacet_cidx<D>(T, sv, hitv);
+        if (B.clr_next) bit_set(B.clr_next, tc);
+        if (B.app_pairs) {
+          const unsigned long long slot = atomicAdd(&B.ctr->app_pairs, 1ull);
+          if (slot < B.app_cap) {
+            B.app_pairs[2 * slot] = cidx;
+            B.app_pairs[2 * slot + 1] = tc;
+          }
+        }
+      }
+      const uint64_t key = ((uint64_t)(p.maxr - rs) << p.cbits) | cidx;
+      const bool to_resid = B.clr && hitv >= 0 && !app;
+      const bool to_queue = active || (!B.clr && hitv >= 0 && !app);
+      const unsigned long long rslot = warp_append(to_resid, &B.ctr->residual);
+      if (to_resid && rslot < B.rcap) B.resid[rslot] = key;
+      const unsigned long long qslot = warp_append(to_queue, &B.ctr->queued);
+      if (to_queue && qslot < B.qcap) {
+        int sv[D + 1];
+#pragma unroll
+        for (int q = 0; q < D; ++q) sv[q] = u[D - q];
+        sv[D] = v0;
+        B.qkey[qslot] = key;
+        B.qvert[qslot] = pack_vertices<D>(sv);
+      }
+    }
+  }
+  if (lane == 0) {
+    if (surv_acc) atomicAdd(&B.ctr->survivors, surv_acc);
+    if (app_acc) atomicAdd(&B.ctr->apparent1, app_acc);
+    if (scan_acc) atomicAdd(&B.ctr->scanned, scan_acc);
+    if (clr_acc) atomicAdd(&B.ctr->cleared, clr_acc);
+  }
+}
+
 // ------------------------------------------------------------------ phase 2: resolve
 // First v <= start (descending) not in S with max_{w in S} R[w][v] <= r, or -1.
 // Lanes take v = base - lane: each load R[w][v] is a coalesced row segment.
@@ -579,6 +833,60 @@ static int sm_count() {
   return g_sms;
 }
 
+static uint64_t binom_u64(uint64_t v, int k) {
+  if ((uint64_t)k > v) return 0;
+  unsigned __int128 c = 1;
+  for (int i = 1; i <= k; ++i) c = c * (unsigned __int128)(v - (uint64_t)k + (uint64_t)i) / (unsigned __int128)i;
+  return (uint64_t)c;
+}
+static bool getenv_flag(const char* name) { return std::getenv(name) != nullptr; }
+
+// Chunk table of k_enumerate_flat for (n, D): chunk_start[t] = chunks of the super-rows
+// before t (super-rows in colex order of u_D > ... > u_2; one super-row when D = 1).  It
+// depends only on (n, D), so it is built once per process on the host and kept on the
+// device (like the binomial table).
+struct FlatTable {
+  uint32_t* d_start = nullptr;
+  uint32_t nsuper = 0, nchunks = 0;
+};
+static const FlatTable* flat_table(int64_t n, int D) {
+  static std::mutex mu;
+  static std::map<std::pair<int64_t, int>, FlatTable> cache;
+  std::lock_guard<std::mutex> g(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_pair(n * 64 + dev, D);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second.d_start ? &it->second : nullptr;
+  FlatTable ft;
+  const uint64_t ns = D >= 2 ? binom_u64((uint64_t)n, D - 1) : 1;
+  if (ns == 0 || ns > (4u << 20)) { cache[key] = ft; return nullptr; }
+  std::vector<uint32_t> start((size_t)ns);
+  uint64_t acc = 0;
+  // walk the (D-1)-subsets in colex order; u_2 = the smallest element
+  std::vector<int> sub((size_t)std::max(D - 1, 0));
+  for (int k = 0; k < D - 1; ++k) sub[(size_t)k] = k;  // ascending: sub[0] = u_2
+  for (uint64_t t = 0; t < ns; ++t) {
+    start[(size_t)t] = (uint32_t)acc;
+    const uint64_t u2 = D >= 2 ? (uint64_t)sub[0] : (uint64_t)n;
+    const uint64_t cnt = u2 * (u2 >= 1 ? u2 - 1 : 0) / 2;
+    acc += (cnt + FL_CHUNK - 1) / FL_CHUNK;
+    if (acc >= (1ull << 31)) { cache[key] = ft; return nullptr; }
+    // colex successor
+    for (int k = 0; k < D - 1; ++k) {
+      if (k + 1 < D - 1 && sub[(size_t)k] + 1 == sub[(size_t)k + 1]) { sub[(size_t)k] = k; continue; }
+      ++sub[(size_t)k];
+      break;
+    }
+  }
+  if (cudaMalloc(&ft.d_start, (size_t)ns * 4) != cudaSuccess) { cudaGetLastError(); cache[key] = FlatTable{}; return nullptr; }
+  cudaMemcpy(ft.d_start, start.data(), (size_t)ns * 4, cudaMemcpyHostToDevice);
+  ft.nsuper = (uint32_t)ns;
+  ft.nchunks = (uint32_t)acc;
+  cache[key] = ft;
+  return &cache[key];
+}
+
 template <int D>
 static void enumerate_d(const DimParams& p, const Tables& T, const HotBuffers& B, cudaStream_t st) {
   const uint64_t rows = p.row_end - p.row_begin;
@@ -599,6 +907,26 @@ static void enumerate_d(const DimParams& p, const Tables& T, const HotBuffers& B
     }
   } else {
     q.win = 0;
+  }
+  // flattened chunks pay off where rows are short next to their setup: d >= 3 (rows of
+  // d = 1, 2 are long — up to n — and the row kernel keeps their loads row-coalesced)
+  if (D >= 3 && q.win && q.variant == 1 && q.shard_world == 1 && q.row_begin == 0 &&
+      q.row_end == binom_u64((uint64_t)q.n, D) && !getenv_flag("VR_NO_FLAT")) {
+    const FlatTable* ft = flat_table(q.n, D);
+    if (ft) {
+      static bool attr_f = false;
+      if (!attr_f) {
+        cudaFuncSetAttribute(k_enumerate_flat<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kWinMaxN * 36 * 4 + 1024));
+        attr_f = true;
+      }
+      const uint64_t warps = ft->nchunks;
+      uint64_t fb = (warps * 32 + HP_THREADS - 1) / HP_THREADS;
+      if (fb > cap) fb = cap;
+      if (fb < 1) fb = 1;
+      k_enumerate_flat<D><<<(unsigned)fb, HP_THREADS, smem, st>>>(T, q, B, ft->d_start, ft->nsuper, ft->nchunks);
+      return;
+    }
   }
   k_enumerate<D><<<(unsigned)blocks, HP_THREADS, smem, st>>>(T, q, B);
 }
