@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p,
 constexpr int FL_CHUNK = 1024;
 
 template <int D>
-__global__ void __launch_bounds__(HP_THREADS) k_enumerate_flat(Tables T, DimParams p, HotBuffers B,
+__global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimParams p, HotBuffers B,
                                                                const uint32_t* __restrict__ chunk_start, uint32_t nsuper,
                                                                uint32_t nchunks) {
   const int lane = threadIdx.x & 31;
@@ -522,17 +522,25 @@ __global__ void __launch_bounds__(HP_THREADS) k_enumerate_flat(Tables T, DimPara
       __syncwarp();
     }
     if (pmU == VR_RINF) continue;  // every simplex of the super-row is over the threshold
+    // (u_1, v_0) of i = C(u_1, 2) + v_0: decoded once per chunk (i < C(n,2) < 2^31), then
+    // advanced by 32 per iteration (v_0 += 32, carried into u_1)
+    int cu1, cv0;
+    {
+      const uint32_t ii = (uint32_t)(i0 + (uint64_t)lane);
+      int x = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)ii)) * 0.5f);
+      while ((uint32_t)x * (uint32_t)(x - 1) / 2 > ii) --x;
+      while ((uint32_t)(x + 1) * (uint32_t)x / 2 <= ii) ++x;
+      cu1 = x;
+      cv0 = (int)(ii - (uint32_t)x * (uint32_t)(x - 1) / 2);
+    }
     for (uint64_t base = i0; base < iend; base += 32) {
       const uint64_t i = base + (uint64_t)lane;
       const bool valid = i < iend;
-      // (u_1, v_0) from i = C(u_1, 2) + v_0
-      int u1 = 1, v0 = 0;
-      if (valid) {
-        u1 = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)i)) * 0.5f);
-        while ((uint64_t)u1 * (uint64_t)(u1 - 1) / 2 > i) --u1;
-        while ((uint64_t)(u1 + 1) * (uint64_t)u1 / 2 <= i) ++u1;
-        v0 = (int)(i - (uint64_t)u1 * (uint64_t)(u1 - 1) / 2);
+      if (base != i0) {
+        cv0 += 32;
+        while (cv0 >= cu1) { cv0 -= cu1; ++cu1; }
       }
+      const int u1 = valid ? cu1 : 1, v0 = valid ? cv0 : 0;
       u[1] = u1;
       const uint32_t* __restrict__ rowu1 = T.rank + (size_t)u1 * (size_t)n;
       uint32_t a[D + 1];
