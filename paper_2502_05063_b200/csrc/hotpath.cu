@@ -462,7 +462,9 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
   __syncthreads();
   const uint32_t* Wt = hp_smem;
   uint32_t* mw = hp_smem + (size_t)n * 36 + (size_t)(threadIdx.x >> 5) * 32;  // window max over u_2..u_D
-  unsigned long long surv_acc = 0, app_acc = 0, scan_acc = 0, clr_acc = 0;
+  // per-lane counters, reduced once at the end (no warp collective per iteration)
+  uint32_t surv_c = 0, app_c = 0, clr_c = 0;
+  unsigned long long scan_c = 0;
   const int steps = p.steps < n ? p.steps : n;
   const int wsteps4 = (steps < 32 ? steps : 32) & ~3;
   const uint32_t* __restrict__ rowtop = T.rank + (size_t)(n - 1) * (size_t)n;
@@ -533,6 +535,8 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
       cu1 = x;
       cv0 = (int)(ii - (uint32_t)x * (uint32_t)(x - 1) / 2);
     }
+    int r1_u1 = -1;
+    uint32_t r1[D + 1], r1_pm = 0;
     for (uint64_t base = i0; base < iend; base += 32) {
       const uint64_t i = base + (uint64_t)lane;
       const bool valid = i < iend;
@@ -544,13 +548,16 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
       u[1] = u1;
       const uint32_t* __restrict__ rowu1 = T.rank + (size_t)u1 * (size_t)n;
       uint32_t a[D + 1];
-      uint32_t r1[D + 1];
-      uint32_t pm_up = pmU;
+      if (u1 != r1_u1) {  // R[u_1][u_b] only when the lane's u_1 moved on
+        r1_u1 = u1;
+        r1_pm = pmU;
 #pragma unroll
-      for (int b = 2; b <= D; ++b) {
-        r1[b] = __ldg(rowu1 + u[b]);
-        pm_up = umax(pm_up, r1[b]);
+        for (int b = 2; b <= D; ++b) {
+          r1[b] = __ldg(rowu1 + u[b]);
+          r1_pm = umax(r1_pm, r1[b]);
+        }
       }
+      const uint32_t pm_up = r1_pm;
       uint32_t rs = pm_up;
       a[1] = valid ? __ldg(rowu1 + v0) : VR_RINF;
       rs = umax(rs, a[1]);
@@ -562,11 +569,11 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
       const bool surv = valid && rs != VR_RINF;
       const uint32_t msurv = __ballot_sync(0xffffffffu, surv);
       if (!msurv) continue;
-      surv_acc += __popc(msurv);
+      surv_c += surv;
       const uint64_t cidx = cU + i;
       bool cleared = false;
       if (B.clr && surv) cleared = bit_test(B.clr, cidx);
-      clr_acc += __popc(__ballot_sync(0xffffffffu, cleared));
+      clr_c += cleared;
       bool active = surv && !cleared;
       int hitv = -1;
       // scan: m_j = max(upper window mw[j], R[u_1][v_j] = Wt[u_1][j]), R[v_j][v_0] = Wt[v_0][j]
@@ -607,7 +614,7 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
         }
       }
       const int examined = hitv >= 0 ? n - hitv : (active ? steps : 0);
-      scan_acc += (unsigned long long)__reduce_add_sync(0xffffffffu, (unsigned)examined);
+      scan_c += (unsigned)examined;
       // condition 2 (as in process_row)
       bool app = false;
       if (hitv >= 0) {
@@ -654,7 +661,7 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
           }
         }
       }
-      app_acc += __popc(__ballot_sync(0xffffffffu, app));
+      app_c += app;
       if (app && (B.clr_next || B.app_pairs)) {
         int sv[D + 1];
 #pragma unroll
@@ -686,6 +693,12 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
       }
     }
   }
+  const unsigned long long surv_acc = __reduce_add_sync(0xffffffffu, surv_c);
+  const unsigned long long app_acc = __reduce_add_sync(0xffffffffu, app_c);
+  const unsigned long long clr_acc = __reduce_add_sync(0xffffffffu, clr_c);
+  unsigned long long scan_acc = scan_c;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) scan_acc += __shfl_xor_sync(0xffffffffu, scan_acc, o);
   if (lane == 0) {
     if (surv_acc) atomicAdd(&B.ctr->survivors, surv_acc);
     if (app_acc) atomicAdd(&B.ctr->apparent1, app_acc);
