@@ -292,9 +292,9 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
     scan_acc += (unsigned long long)__reduce_add_sync(0xffffffffu, (unsigned)examined);
     // condition 2 for lanes that found t = s ∪ {hitv}: no facet t \ {w}, w > hitv (the
     // lex-smaller facets), with diam = diam(s)
-    bool app = false;
-    if (hitv >= 0) {
-      app = true;
+    // (a hit above every vertex of s has no lex-smaller facet to test: apparent at once)
+    bool app = hitv >= 0;
+    if (hitv >= 0 && hitv < u[D]) {
       uint32_t b[D + 1];
       uint32_t bup = 0;
       const int jh = n - 1 - hitv;
@@ -616,9 +616,8 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
       const int examined = hitv >= 0 ? n - hitv : (active ? steps : 0);
       scan_c += (unsigned)examined;
       // condition 2 (as in process_row)
-      bool app = false;
-      if (hitv >= 0) {
-        app = true;
+      bool app = hitv >= 0;
+      if (hitv >= 0 && hitv < u[D]) {  // else no vertex of s above the hit: apparent
         uint32_t pm_ex[D + 1];
         pm_ex[0] = 0;
         pm_ex[1] = pmU;
