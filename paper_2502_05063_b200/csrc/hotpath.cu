@@ -153,11 +153,11 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
     const bool surv = valid && rs != VR_RINF;  // diam(s) <= t (Eq 5.3, Alg 17 line 3)
     const uint32_t msurv = __ballot_sync(0xffffffffu, surv);
     if (!msurv) continue;
-    surv_acc += __popc(msurv);
+    surv_acc += surv;  // lane-local counts, reduced once per warp at the end
     const uint64_t cidx = cbase + (uint64_t)v0;
     bool cleared = false;
     if (B.clr && surv) cleared = bit_test(B.clr, cidx);  // a death of dimension d-1
-    clr_acc += __popc(__ballot_sync(0xffffffffu, cleared));
+    clr_acc += cleared;
     bool active = surv && !cleared;
     bool nohit = false;  // resolved in-kernel: no equal-diameter cofacet at all
     int hitv = -1;
@@ -289,7 +289,7 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
         }
       }
     }
-    scan_acc += (unsigned long long)__reduce_add_sync(0xffffffffu, (unsigned)examined);
+    scan_acc += (unsigned)examined;
     // condition 2 for lanes that found t = s ∪ {hitv}: no facet t \ {w}, w > hitv (the
     // lex-smaller facets), with diam = diam(s)
     // (a hit above every vertex of s has no lex-smaller facet to test: apparent at once)
@@ -326,7 +326,7 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
         }
       }
     }
-    app_acc += __popc(__ballot_sync(0xffffffffu, app));
+    app_acc += app;
     if (app && (B.clr_next || B.app_pairs)) {
       int s[D + 1];
 #pragma unroll
@@ -427,6 +427,13 @@ __global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p,
       }
       process_row<D>(T, p, B, u, uc, Wt, mw, surv_acc, app_acc, scan_acc, clr_acc);
     }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    surv_acc += __shfl_xor_sync(0xffffffffu, surv_acc, o);
+    app_acc += __shfl_xor_sync(0xffffffffu, app_acc, o);
+    scan_acc += __shfl_xor_sync(0xffffffffu, scan_acc, o);
+    clr_acc += __shfl_xor_sync(0xffffffffu, clr_acc, o);
   }
   if (lane == 0) {
     if (surv_acc) atomicAdd(&B.ctr->survivors, surv_acc);
