@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter_fused(const uint64_t* _
 // histogram -> grid sync -> offsets + stable scatter -> grid sync, per 8-bit digit.
 __global__ void __launch_bounds__(RS_THREADS) rs_coop(uint64_t* __restrict__ a, uint64_t* __restrict__ b, size_t n,
                                                      int begin_bit, int end_bit, uint32_t* __restrict__ tile_hist,
-                                                     uint32_t ntiles) {
+                                                     uint32_t ntiles, int tile) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char rs_smem[];
@@ -325,13 +325,14 @@ __global__ void __launch_bounds__(RS_THREADS) rs_coop(uint64_t* __restrict__ a, 
   __shared__ uint32_t warp_tot[SC_THREADS / 32];
   __shared__ uint32_t total;
   __shared__ uint32_t h[RS_BINS];
-  const size_t base = (size_t)blockIdx.x * RS_TILE;
-  const int cnt = (int)((n - base) < (size_t)RS_TILE ? (n - base) : (size_t)RS_TILE);
+  // tile <= RS_TILE keys per CTA: smaller tiles put more SMs on a mid-size sort
+  const size_t base = (size_t)blockIdx.x * (size_t)tile;
+  const int cnt = (int)((n - base) < (size_t)tile ? (n - base) : (size_t)tile);
   uint64_t* src = a;
   uint64_t* dst = b;
   for (int shift = begin_bit; shift < end_bit; shift += 8) {
     const uint32_t dmask = end_bit - shift >= 8 ? 0xFFu : ((1u << (end_bit - shift)) - 1u);
-    for (int i = threadIdx.x; i < RS_TILE; i += RS_THREADS) keys_s[i] = i < cnt ? src[base + i] : ~0ull;
+    for (int i = threadIdx.x; i < cnt; i += RS_THREADS) keys_s[i] = src[base + i];
     h[threadIdx.x] = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < cnt; i += RS_THREADS) atomicAdd(&h[(uint32_t)(keys_s[i] >> shift) & dmask], 1u);
@@ -364,7 +365,7 @@ __global__ void __launch_bounds__(RS_THREADS) rs_coop(uint64_t* __restrict__ a, 
 static size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
 size_t radix_sort_temp_bytes(size_t n) {
-  size_t ntiles = (n + RS_TILE - 1) / RS_TILE;
+  size_t ntiles = (n + 1023) / 1024;  // the cooperative path may use tiles down to 1024 keys
   size_t hist = (size_t)RS_BINS * ntiles;
   return align256(hist * sizeof(uint32_t)) + scan_temp_bytes(hist);
 }
@@ -403,8 +404,25 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit,
   }
   if ((int)ntiles <= coop_cap) {  // every pass in one cooperative launch
     const int passes = (end_bit - begin_bit + 7) / 8;
-    void* args[] = {(void*)&keys, (void*)&alt, (void*)&n, (void*)&begin_bit, (void*)&end_bit, (void*)&hist, (void*)&ntiles};
-    cudaLaunchCooperativeKernel((void*)rs_coop, dim3(ntiles), dim3(RS_THREADS), args, smem, st);
+    // halve the tile while the grid stays small: a pass's latency scales with the keys per
+    // CTA, but every CTA also walks all ntiles histograms, so stop at 32 tiles
+    int tile = RS_TILE;
+    uint32_t nt = ntiles;
+    int sms = 148;
+    {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    while (tile > 1024) {
+      const uint32_t nt2 = (uint32_t)((n + (size_t)(tile / 2) - 1) / (size_t)(tile / 2));
+      if ((int)nt2 > coop_cap || (int)nt2 > sms || nt2 > 32) break;
+      tile /= 2;
+      nt = nt2;
+    }
+    void* args[] = {(void*)&keys, (void*)&alt, (void*)&n, (void*)&begin_bit, (void*)&end_bit, (void*)&hist, (void*)&nt,
+                    (void*)&tile};
+    cudaLaunchCooperativeKernel((void*)rs_coop, dim3(nt), dim3(RS_THREADS), args, smem, st);
     if (launches) *launches += 1;
     return (passes & 1) ? alt : keys;
   }
