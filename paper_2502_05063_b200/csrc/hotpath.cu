@@ -347,16 +347,18 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
     // bitmap clearing is decided in phase 2)
     const bool to_resid = B.clr && ((hitv >= 0 && !app) || nohit);
     const bool to_queue = active || (!B.clr && hitv >= 0 && !app);
-    const unsigned long long rslot = warp_append(to_resid, &B.ctr->residual);
-    if (to_resid && rslot < B.rcap) B.resid[rslot] = key;
-    const unsigned long long qslot = warp_append(to_queue, &B.ctr->queued);
-    if (to_queue && qslot < B.qcap) {
-      int s[D + 1];
+    if (__any_sync(0xffffffffu, to_resid | to_queue)) {  // rare: skip the appends' collectives
+      const unsigned long long rslot = warp_append(to_resid, &B.ctr->residual);
+      if (to_resid && rslot < B.rcap) B.resid[rslot] = key;
+      const unsigned long long qslot = warp_append(to_queue, &B.ctr->queued);
+      if (to_queue && qslot < B.qcap) {
+        int s[D + 1];
 #pragma unroll
-      for (int i = 0; i < D; ++i) s[i] = u[D - i];
-      s[D] = v0;
-      B.qkey[qslot] = key;
-      B.qvert[qslot] = pack_vertices<D>(s);
+        for (int i = 0; i < D; ++i) s[i] = u[D - i];
+        s[D] = v0;
+        B.qkey[qslot] = key;
+        B.qvert[qslot] = pack_vertices<D>(s);
+      }
     }
   }
 }
@@ -686,16 +688,18 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
       const uint64_t key = ((uint64_t)(p.maxr - rs) << p.cbits) | cidx;
       const bool to_resid = B.clr && hitv >= 0 && !app;
       const bool to_queue = active || (!B.clr && hitv >= 0 && !app);
-      const unsigned long long rslot = warp_append(to_resid, &B.ctr->residual);
-      if (to_resid && rslot < B.rcap) B.resid[rslot] = key;
-      const unsigned long long qslot = warp_append(to_queue, &B.ctr->queued);
-      if (to_queue && qslot < B.qcap) {
-        int sv[D + 1];
+      if (__any_sync(0xffffffffu, to_resid | to_queue)) {  // rare: skip the appends' collectives
+        const unsigned long long rslot = warp_append(to_resid, &B.ctr->residual);
+        if (to_resid && rslot < B.rcap) B.resid[rslot] = key;
+        const unsigned long long qslot = warp_append(to_queue, &B.ctr->queued);
+        if (to_queue && qslot < B.qcap) {
+          int sv[D + 1];
 #pragma unroll
-        for (int q = 0; q < D; ++q) sv[q] = u[D - q];
-        sv[D] = v0;
-        B.qkey[qslot] = key;
-        B.qvert[qslot] = pack_vertices<D>(sv);
+          for (int q = 0; q < D; ++q) sv[q] = u[D - q];
+          sv[D] = v0;
+          B.qkey[qslot] = key;
+          B.qvert[qslot] = pack_vertices<D>(sv);
+        }
       }
     }
   }
