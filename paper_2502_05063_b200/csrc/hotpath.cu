@@ -939,9 +939,10 @@ static void enumerate_d(const DimParams& p, const Tables& T, const HotBuffers& B
   } else {
     q.win = 0;
   }
-  // flattened chunks pay off where rows are short next to their setup: d >= 3 (rows of
-  // d = 1, 2 are long — up to n — and the row kernel keeps their loads row-coalesced)
-  if (D >= 3 && q.win && q.variant == 1 && q.shard_world == 1 && q.row_begin == 0 &&
+  // flattened chunks from d = 2 on (measured: equal on c2, -8% on c4a); dimension 1 has
+  // one super-row of n long rows and stays on the row kernel (VR_FLAT_MIN_D overrides)
+  static const int flat_min_d = std::getenv("VR_FLAT_MIN_D") ? std::atoi(std::getenv("VR_FLAT_MIN_D")) : 2;
+  if (D >= flat_min_d && q.win && q.variant == 1 && q.shard_world == 1 && q.row_begin == 0 &&
       q.row_end == binom_u64((uint64_t)q.n, D) && !getenv_flag("VR_NO_FLAT")) {
     const FlatTable* ft = flat_table(q.n, D);
     if (ft) {
