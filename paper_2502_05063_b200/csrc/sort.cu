@@ -249,6 +249,33 @@ __device__ __forceinline__ void rs_tile_rank(const uint64_t* keys_s, uint64_t* s
   __syncthreads();
 }
 
+// Digit b's total over all tiles and the part in tiles before `me`, from the digit-major
+// tile histogram.  Loads are issued 8 at a time (independent, from L2 — the histogram was
+// written by other CTAs of this pass), so a pass waits one L2 latency per 8 tiles instead of
+// one per tile.
+__device__ __forceinline__ void digit_totals(const uint32_t* th, int b, uint32_t ntiles, uint32_t me, uint32_t& tot,
+                                             uint32_t& before) {
+  const uint32_t* row = th + (size_t)b * ntiles;
+  tot = 0;
+  before = 0;
+  uint32_t t = 0;
+  for (; t + 8 <= ntiles; t += 8) {
+    uint32_t c[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] = __ldcg(row + t + k);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      tot += c[k];
+      before += (t + (uint32_t)k < me) ? c[k] : 0u;
+    }
+  }
+  for (; t < ntiles; ++t) {
+    const uint32_t c = __ldcg(row + t);
+    tot += c;
+    before += t < me ? c : 0u;
+  }
+}
+
 // Whole sort of n <= RS_SMALL_CAP keys in one CTA, every pass in shared memory, one launch.
 constexpr int RS_SMALL_CAP = 2 * RS_TILE;
 __global__ void __launch_bounds__(RS_THREADS) rs_small(uint64_t* __restrict__ keys, int n, int begin_bit, int end_bit) {
@@ -290,12 +317,8 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter_fused(const uint64_t* _
   //                                          + sum over earlier tiles of digit b
   {
     const int b = threadIdx.x;
-    uint32_t tot_b = 0, before = 0;
-    for (uint32_t t = 0; t < ntiles; ++t) {
-      const uint32_t c = tile_hist[(size_t)b * ntiles + t];
-      tot_b += c;
-      if (t < blockIdx.x) before += c;
-    }
+    uint32_t tot_b, before;
+    digit_totals(tile_hist, b, ntiles, blockIdx.x, tot_b, before);
     const uint32_t dig_start = block_exclusive_scan_256(tot_b, warp_tot, &total);
     gofs[b] = dig_start + before;
   }
@@ -341,12 +364,8 @@ __global__ void __launch_bounds__(RS_THREADS) rs_coop(uint64_t* __restrict__ a, 
     grid.sync();
     {
       const int bb = threadIdx.x;
-      uint32_t tot_b = 0, before = 0;
-      for (uint32_t t = 0; t < ntiles; ++t) {
-        const uint32_t c = tile_hist[(size_t)bb * ntiles + t];
-        tot_b += c;
-        if (t < blockIdx.x) before += c;
-      }
+      uint32_t tot_b, before;
+      digit_totals(tile_hist, bb, ntiles, blockIdx.x, tot_b, before);
       const uint32_t dig_start = block_exclusive_scan_256(tot_b, warp_tot, &total);
       gofs[bb] = dig_start + before;
     }
