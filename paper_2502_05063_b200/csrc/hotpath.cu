@@ -477,12 +477,16 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
   const int steps = p.steps < n ? p.steps : n;
   const int wsteps4 = (steps < 32 ? steps : 32) & ~3;
   const uint32_t* __restrict__ rowtop = T.rank + (size_t)(n - 1) * (size_t)n;
+  // shards: chunk c belongs to rank (nchunks-1-c) mod world (the chunks partition the
+  // candidates, as the rows do for the row kernel)
+  const uint64_t SW = (uint64_t)p.shard_world, SR = (uint64_t)p.shard_rank;
+  const uint64_t mine = nchunks > SR ? ((uint64_t)nchunks - SR + SW - 1) / SW : 0;
   while (true) {
     unsigned long long g0 = 0;
     if (lane == 0) g0 = atomicAdd(&B.ctr->row_next, 1ull);
     g0 = __shfl_sync(0xffffffffu, g0, 0);
-    if (g0 >= nchunks) break;
-    const uint32_t c = nchunks - 1 - (uint32_t)g0;
+    if (g0 >= mine) break;
+    const uint32_t c = nchunks - 1 - (uint32_t)(g0 * SW + SR);
     // super-row of chunk c: the last t with chunk_start[t] <= c
     uint32_t lo = 0, hi = nsuper - 1;
     while (lo < hi) {
@@ -942,7 +946,7 @@ static void enumerate_d(const DimParams& p, const Tables& T, const HotBuffers& B
   // flattened chunks from d = 2 on (measured: equal on c2, -8% on c4a); dimension 1 has
   // one super-row of n long rows and stays on the row kernel (VR_FLAT_MIN_D overrides)
   static const int flat_min_d = std::getenv("VR_FLAT_MIN_D") ? std::atoi(std::getenv("VR_FLAT_MIN_D")) : 2;
-  if (D >= flat_min_d && q.win && q.variant == 1 && q.shard_world == 1 && q.row_begin == 0 &&
+  if (D >= flat_min_d && q.win && q.variant == 1 && q.row_begin == 0 &&
       q.row_end == binom_u64((uint64_t)q.n, D) && !getenv_flag("VR_NO_FLAT")) {
     const FlatTable* ft = flat_table(q.n, D);
     if (ft) {
@@ -952,7 +956,7 @@ static void enumerate_d(const DimParams& p, const Tables& T, const HotBuffers& B
                              (int)(kWinMaxN * 36 * 4 + 1024));
         attr_f = true;
       }
-      const uint64_t warps = ft->nchunks;
+      const uint64_t warps = (ft->nchunks + (uint64_t)q.shard_world - 1) / (uint64_t)q.shard_world;
       uint64_t fb = (warps * 32 + HP_THREADS - 1) / HP_THREADS;
       if (fb > cap) fb = cap;
       if (fb < 1) fb = 1;
