@@ -449,17 +449,18 @@ __global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p,
 // Dense dimensions with the shared-memory window: the candidates of a "super-row" (all
 // d-simplices sharing the upper vertices u_D > ... > u_2) are the pairs (u_1, v_0),
 // v_0 < u_1 < u_2, numbered i = C(u_1, 2) + v_0 — so cidx = sum_{i>=2} C(u_i, i+1) + i —
-// and cut into chunks of FL_CHUNK consecutive i.  A warp takes one chunk per grab (largest
+// and cut into chunks of `chunk` consecutive i (1024, or fewer — down to 128 — when the
+// dimension has too few candidates to give every SM ~24 warps).  A warp takes one chunk per grab (largest
 // super-rows first) and its 32 lanes take consecutive i, across row boundaries: no ragged
 // row tails, and the per-row setup (prefix maxima, window, cidx base) becomes per-chunk.
 // Per lane the row-dependent parts (R[u_1][u_b], R[u_1][v] in the window) are read for the
 // lane's own u_1 (mostly shared by the warp).  Same tests and outputs as process_row.
-constexpr int FL_CHUNK = 1024;
+constexpr int FL_CHUNK = 1024;  // largest chunk
 
 template <int D>
 __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimParams p, HotBuffers B,
                                                                const uint32_t* __restrict__ chunk_start, uint32_t nsuper,
-                                                               uint32_t nchunks) {
+                                                               uint32_t nchunks, int chunk) {
   const int lane = threadIdx.x & 31;
   const int n = T.n;
   extern __shared__ __align__(16) uint32_t hp_smem[];
@@ -511,8 +512,8 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
       if (D >= 2) u2 = u[2];
     }
     const uint64_t cnt_sr = (uint64_t)u2 * (uint64_t)(u2 - 1) / 2;
-    const uint64_t i0 = (uint64_t)(c - __ldg(chunk_start + t)) * FL_CHUNK;
-    const uint64_t iend = (i0 + FL_CHUNK < cnt_sr) ? i0 + FL_CHUNK : cnt_sr;
+    const uint64_t i0 = (uint64_t)(c - __ldg(chunk_start + t)) * (uint64_t)chunk;
+    const uint64_t iend = (i0 + (uint64_t)chunk < cnt_sr) ? i0 + (uint64_t)chunk : cnt_sr;
     // upper-prefix parts: pair maxima over u_2..u_D (all / avoiding u_j), window maxima
     uint32_t pmU = 0, pmU_ex[D + 1];
 #pragma unroll
@@ -883,6 +884,7 @@ static bool getenv_flag(const char* name) { return std::getenv(name) != nullptr;
 struct FlatTable {
   uint32_t* d_start = nullptr;
   uint32_t nsuper = 0, nchunks = 0;
+  int chunk = FL_CHUNK;
 };
 static const FlatTable* flat_table(int64_t n, int D) {
   static std::mutex mu;
@@ -898,6 +900,17 @@ static const FlatTable* flat_table(int64_t n, int D) {
   if (ns == 0 || ns > (4u << 20)) { cache[key] = ft; return nullptr; }
   std::vector<uint32_t> start((size_t)ns);
   uint64_t acc = 0;
+  // chunk size: 1024, or smaller (multiple of 32, >= 128) so that the dimension's
+  // candidates C(n, D+1) still give ~24 warps per SM
+  {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t total = binom_u64((uint64_t)n, D + 1);
+    uint64_t c = total / ((uint64_t)sms * 24);
+    c = (c + 31) / 32 * 32;
+    ft.chunk = (int)std::max<uint64_t>(128, std::min<uint64_t>((uint64_t)FL_CHUNK, c));
+  }
+  const uint64_t CH = (uint64_t)ft.chunk;
   // walk the (D-1)-subsets in colex order; u_2 = the smallest element
   std::vector<int> sub((size_t)std::max(D - 1, 0));
   for (int k = 0; k < D - 1; ++k) sub[(size_t)k] = k;  // ascending: sub[0] = u_2
@@ -905,7 +918,7 @@ static const FlatTable* flat_table(int64_t n, int D) {
     start[(size_t)t] = (uint32_t)acc;
     const uint64_t u2 = D >= 2 ? (uint64_t)sub[0] : (uint64_t)n;
     const uint64_t cnt = u2 * (u2 >= 1 ? u2 - 1 : 0) / 2;
-    acc += (cnt + FL_CHUNK - 1) / FL_CHUNK;
+    acc += (cnt + CH - 1) / CH;
     if (acc >= (1ull << 31)) { cache[key] = ft; return nullptr; }
     // colex successor
     for (int k = 0; k < D - 1; ++k) {
@@ -960,7 +973,7 @@ static void enumerate_d(const DimParams& p, const Tables& T, const HotBuffers& B
       uint64_t fb = (warps * 32 + HP_THREADS - 1) / HP_THREADS;
       if (fb > cap) fb = cap;
       if (fb < 1) fb = 1;
-      k_enumerate_flat<D><<<(unsigned)fb, HP_THREADS, smem, st>>>(T, q, B, ft->d_start, ft->nsuper, ft->nchunks);
+      k_enumerate_flat<D><<<(unsigned)fb, HP_THREADS, smem, st>>>(T, q, B, ft->d_start, ft->nsuper, ft->nchunks, ft->chunk);
       return;
     }
   }
