@@ -169,6 +169,22 @@ def test_row_scheduling_invariance(grab, D):
             assert a.stats[d]["survivors"] == b.stats[d]["survivors"]
 
 
+@pytest.mark.parametrize("n,D", [(33, 3), (100, 2), (100, 3), (544, 2), (545, 2)])
+def test_flat_kernel_equals_row_kernel(n, D, monkeypatch):
+    # k_enumerate_flat (d >= 2, n <= 544, shared-memory window) against the row kernel
+    # (VR_NO_FLAT); n = 545 is past the window limit, so both sides run the row kernel
+    lt = G.random_cloud(n, 21)
+    t = float(np.quantile(lt, 0.3)) if n > 200 else math.inf
+    a = vr.barcodes(lt, n, D, t, index_pairs=True)
+    monkeypatch.setenv("VR_NO_FLAT", "1")
+    b = vr.barcodes(lt, n, D, t, index_pairs=True)
+    for d in range(D + 1):
+        assert np.array_equal(a.pairs[d], b.pairs[d])
+        assert {tuple(x) for x in a.index_pairs[d].tolist()} == {tuple(x) for x in b.index_pairs[d].tolist()}
+        for k in ("survivors", "apparent", "cleared", "residual_columns"):
+            assert a.stats[d][k] == b.stats[d][k], (d, k)
+
+
 def test_residual_modes_agree():
     cfg = G.CONFIGS["c2_s3_192"]
     lt = cfg.lower_tri(60)
