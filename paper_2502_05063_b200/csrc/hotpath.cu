@@ -137,7 +137,6 @@ __device__ __forceinline__ void process_row(const Tables& T, const DimParams& p,
     __syncwarp();
   }
   const int steps = p.steps < n ? p.steps : n;
-  const int steps4 = steps & ~3;  // whole groups of 4; the rest (n < steps) one by one
   const uint32_t* __restrict__ rowtop = T.rank + (size_t)(n - 1) * (size_t)n;  // row of v = n-1
 
   for (int base = 0; base < v1; base += 32) {

@@ -81,7 +81,6 @@ __device__ __forceinline__ void sparse_row(const Tables& T, const DimParams& p, 
                                            const int (&u)[D + 2], unsigned long long& surv_acc, unsigned long long& app_acc,
                                            unsigned long long& scan_acc, unsigned long long& clr_acc) {
   const int lane = threadIdx.x & 31;
-  const int n = T.n;
   const int u1 = u[1];
   uint32_t pm_up = 0;
   uint32_t pm_ex[D + 1];
