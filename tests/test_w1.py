@@ -155,3 +155,24 @@ def test_determinism_and_seeds():
     for sd in (1, 2, 3):
         v, st = vr.w1(A, B, s=18, seed=sd)
         assert st["bound_lo"] * exact - 1e-9 <= v <= st["bound_hi"] * exact + 1e-9
+
+
+def test_w1_between_vr_barcodes():
+    # W1 between the diagrams the library produces — the H1
+    # diagrams of two noisy circles (config-1-shaped) — exact and approximate, vs the oracle
+    from datagen import clouds as G
+    vr = _vr()
+    rng = np.random.default_rng(4)
+    diags = []
+    for k in range(2):
+        th = rng.random(80) * 2 * np.pi
+        pts = np.stack([np.cos(th), np.sin(th)], 1) + rng.normal(0, 0.08 + 0.04 * k, (80, 2))
+        lt = G.lower_tri_from_points(pts)
+        bc = vr.barcodes(lt, 80, 1)
+        diags.append(np.concatenate([bc.pairs[0][np.isfinite(bc.pairs[0][:, 1])], bc.pairs[1]]))
+    A, B = diags
+    exact = W.w1_exact(A, B)
+    got, _ = vr.w1(A, B, exact=True)
+    assert got == pytest.approx(exact, rel=1e-9, abs=1e-12)
+    v, st = vr.w1(A, B, s=18)
+    assert st["bound_lo"] * exact - 1e-9 <= v <= st["bound_hi"] * exact + 1e-9

@@ -39,6 +39,17 @@ def main():
     for n in args.n:
         work.append((f"gaussian_{n}", PD.gaussian(n, 1), PD.gaussian(n, 2)))
     work.append(("clustered_50000", PD.clustered(50000, 3), PD.clustered(50000, 4)))
+    # the diagrams the library produces: all finite bars of config 3
+    # (trefoil tube, n = 1000, dims 0-2) against those of a re-sampled copy (seed + 100)
+    from datagen import clouds as G
+    c3 = G.CONFIGS["c3_trefoil1000"]
+    vd = []
+    for seed_shift in (0, 100):
+        cfg = c3 if seed_shift == 0 else G.Config(**{**c3.__dict__, "seed": c3.seed + seed_shift})
+        bc = vr.barcodes(cfg.lower_tri(), cfg.n, 2, cfg.threshold)
+        P = np.concatenate([p for p in bc.pairs])
+        vd.append(P[np.isfinite(P[:, 1])].astype(np.float32))
+    work.append(("vr_c3_bars_vs_resampled", vd[0], vd[1]))
     for name, A, B in work:
         for s in args.s:
             vr.w1(A[:100], B[:100], s=s)  # warm
