@@ -454,3 +454,25 @@ def test_full_size_sampled_apparent_pairs(name, D, thr, sparse):
         for k in rng.choice(len(rest), size=min(200, len(rest)), replace=False):
             s = int(rest[k, 0])
             assert O.apparent_one(lt, cfg.n, _decode(s, d + 1, cfg.n), t) == (False, None), (d, s)
+
+
+def test_apparent_rate_matches_paper_at_10000_points():
+    # PAPER.md §5.6.6: random-permutation distance matrices, dimension 1, n = 10000:
+    # average apparent fraction 0.991127743 (relative to the edges of the filtration, which
+    # the enclosing-radius cut keeps).  One sample here (the paper averages 10; the sample
+    # spread at this n is ~5e-5): the GPU hot path alone, through vr_dist_* at world 1.
+    import torch
+    from paper_2502_05063_b200.dist import LibBackend
+    n = 10000
+    N = n * (n - 1) // 2
+    perm = np.random.default_rng(1000).permutation(N).astype(np.uint32)
+    vals = (perm + np.uint32(0x3F800000)).view(np.float32)  # order-preserving (Obs 5.6.8)
+    lt = torch.from_numpy(vals).cuda()
+    be = LibBackend(lt, n, 1, math.inf, 0, 1)
+    try:
+        be.dim_local(1)
+        surv, app = be.counters(1)[:2]
+    finally:
+        be.close()
+    assert abs(app / surv - 0.991127743) < 3e-4
+    assert app / N <= (n - 2) / n  # Theorem 5.4.2 bound
