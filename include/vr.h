@@ -120,6 +120,15 @@ int vr_barcodes(const float* dist_lower_tri, int64_t n, int32_t max_dim, float t
 int vr_barcodes_device(const float* d_dist_lower_tri, int64_t n, int32_t max_dim, float threshold,
                        const vr_options* opt, void* stream, vr_result** out);
 
+/* Sparse-input entry (SPEC's sparse format): the distance matrix as
+ * nnz (rows[k], cols[k], dist[k]) entries, host pointers, rows[k] != cols[k] in [0, n),
+ * dist[k] finite and >= 0; a pair given twice keeps the smaller distance; absent pairs are
+ * absent edges (never in the complex).  The dense lower triangle is built on the device
+ * (+inf for absent pairs; any +inf entry in a dense input means the same).  With absent
+ * edges the enclosing radius is +inf, so threshold = +inf keeps every given edge. */
+int vr_barcodes_coo(int64_t n, int64_t nnz, const int32_t* rows, const int32_t* cols, const float* dist, int32_t max_dim,
+                    float threshold, const vr_options* opt, vr_result** out);
+
 int32_t vr_max_dim(const vr_result* r);
 int64_t vr_num_pairs(const vr_result* r, int32_t dim);
 const vr_pair* vr_pairs(const vr_result* r, int32_t dim);

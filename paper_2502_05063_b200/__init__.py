@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-__all__ = ["barcodes", "barcodes_device", "radix_sort_u64", "hypha_pivots", "min_cost_flow", "w1", "w1_network", "Plan", "Barcode", "VRError", "lib_path", "load"]
+__all__ = ["barcodes", "barcodes_coo", "barcodes_device", "radix_sort_u64", "hypha_pivots", "min_cost_flow", "w1", "w1_network", "Plan", "Barcode", "VRError", "lib_path", "load"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_HERE, "libvr.so")
@@ -74,6 +74,7 @@ def load() -> ctypes.CDLL:
     sig = {
         "vr_barcodes": (ctypes.c_int, [vp, i64, i32, f32, vp, ctypes.POINTER(vp)]),
         "vr_barcodes_device": (ctypes.c_int, [vp, i64, i32, f32, vp, vp, ctypes.POINTER(vp)]),
+        "vr_barcodes_coo": (ctypes.c_int, [i64, i64, vp, vp, vp, i32, f32, vp, ctypes.POINTER(vp)]),
         "vr_max_dim": (i32, [vp]),
         "vr_num_pairs": (i64, [vp, i32]),
         "vr_pairs": (vp, [vp, i32]),
@@ -175,6 +176,25 @@ def barcodes(dist_lower_tri, n: int, max_dim: int, threshold: float = math.inf, 
     o = _options(**opts)
     rc = lib.vr_barcodes(lt.ctypes.data if lt.size else None, n, max_dim, threshold, ctypes.byref(o), ctypes.byref(h))
     _check(rc)
+    try:
+        return _collect(h)
+    finally:
+        lib.vr_free(h)
+
+
+def barcodes_coo(n: int, rows, cols, dist, max_dim: int, threshold: float = math.inf, **opts) -> Barcode:
+    """vr_barcodes_coo: the distance matrix as (rows[k], cols[k], dist[k]) entries; absent
+    pairs are absent edges."""
+    lib = load()
+    r = np.ascontiguousarray(rows, dtype=np.int32)
+    c = np.ascontiguousarray(cols, dtype=np.int32)
+    d = np.ascontiguousarray(dist, dtype=np.float32)
+    if not (r.size == c.size == d.size):
+        raise ValueError("rows, cols and dist must have the same length")
+    h = ctypes.c_void_p()
+    o = _options(**opts)
+    _check(lib.vr_barcodes_coo(n, r.size, r.ctypes.data if r.size else None, c.ctypes.data if c.size else None,
+                               d.ctypes.data if d.size else None, max_dim, threshold, ctypes.byref(o), ctypes.byref(h)))
     try:
         return _collect(h)
     finally:

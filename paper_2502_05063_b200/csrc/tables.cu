@@ -75,7 +75,10 @@ __global__ void tb_finalize(const uint32_t* __restrict__ rowmax, int64_t n, floa
     uint32_t R = 0xFFFFFFFFu;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) R = red[w] < R ? red[w] : R;
     if (n < 2) R = 0;  // A27: n = 1 -> R = 0
-    const uint32_t tb = isinf(threshold) ? R : dist_bits(threshold);
+    // +inf entries are absent edges (a sparse input): never in the complex.  With such
+    // entries R is +inf as well, and then every finite edge is kept (no enclosing-radius cut)
+    const uint32_t tb0 = isinf(threshold) ? R : dist_bits(threshold);
+    const uint32_t tb = tb0 < 0x7F800000u ? tb0 : 0x7F7FFFFFu;
     // m = number of sorted keys whose fp32 bits are <= tb (upper bound)
     uint64_t lo = 0, hi = N;
     while (lo < hi) {
@@ -112,6 +115,30 @@ __global__ void tb_rank(const float* __restrict__ lt, int64_t n, const uint64_t*
     }
     rank[(size_t)i * (size_t)n + (size_t)j] = r;
   }
+}
+
+// sparse (COO) input -> dense lower triangle: +inf everywhere, then each entry (i, j, d),
+// i != j, at i(i-1)/2 + j for i > j; repeated pairs keep the smallest distance
+__global__ void coo_fill_inf(float* __restrict__ lt, uint64_t N) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += (uint64_t)gridDim.x * blockDim.x)
+    lt[k] = __int_as_float(0x7F800000);
+}
+__global__ void coo_scatter(const int32_t* __restrict__ ii, const int32_t* __restrict__ jj, const float* __restrict__ dd,
+                            int64_t nnz, float* __restrict__ lt) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = ii[k], b = jj[k];
+    if (a < b) { const int64_t t = a; a = b; b = t; }
+    const float x = dd[k] == 0.0f ? 0.0f : dd[k];
+    atomicMin(reinterpret_cast<unsigned int*>(lt) + a * (a - 1) / 2 + b, __float_as_uint(x));
+  }
+}
+void launch_coo_to_dense(const int32_t* ii, const int32_t* jj, const float* dd, int64_t nnz, int64_t n, float* lt,
+                         cudaStream_t st) {
+  const uint64_t N = (uint64_t)n * (uint64_t)(n - 1) / 2;
+  if (N) coo_fill_inf<<<(unsigned)((N + 255) / 256 < 148u * 16u ? (N + 255) / 256 : 148u * 16u), 256, 0, st>>>(lt, N);
+  if (nnz > 0)
+    coo_scatter<<<(unsigned)(((uint64_t)nnz + 255) / 256 < 148u * 16u ? ((uint64_t)nnz + 255) / 256 : 148u * 16u), 256, 0, st>>>(
+        ii, jj, dd, nnz, lt);
 }
 
 static int bits_for(uint64_t x) {  // number of bits to represent values 0..x

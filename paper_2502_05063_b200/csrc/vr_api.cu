@@ -926,6 +926,49 @@ int vr_barcodes_device(const float* d_lt, int64_t n, int32_t max_dim, float thre
   });
 }
 
+int vr_barcodes_coo(int64_t n, int64_t nnz, const int32_t* rows, const int32_t* cols, const float* dist, int32_t max_dim,
+                    float threshold, const vr_options* opt, vr_result** out) {
+  if (out) *out = nullptr;
+  return guarded([&] {
+    if (!out) throw VrError(VR_EINVAL, "out is NULL");
+    if (nnz < 0 || (nnz && (!rows || !cols || !dist))) throw VrError(VR_EINVAL, "COO arrays are NULL");
+    check_args(n >= 2 ? (const void*)1 : nullptr, n, max_dim, threshold);
+    for (int64_t k = 0; k < nnz; ++k) {
+      if (rows[k] < 0 || rows[k] >= n || cols[k] < 0 || cols[k] >= n || rows[k] == cols[k])
+        throw VrError(VR_EINPUT, "COO entry out of range or on the diagonal");
+      if (!(dist[k] >= 0.0f) || std::isinf(dist[k])) throw VrError(VR_EINPUT, "COO distance negative, NaN or infinite");
+    }
+    vr_options o = default_options(opt);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw VrError(VR_EDEVICE, "no CUDA device");
+    if (o.device < 0 || o.device >= ndev) throw VrError(VR_EINVAL, "options.device out of range");
+    CUDA_TRY(cudaSetDevice(o.device));
+    std::unique_ptr<vr_plan> P(new vr_plan());
+    P->n = n; P->D = max_dim; P->threshold = threshold; P->opt = o;
+    CUDA_TRY(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking));
+    struct SG { cudaStream_t s; ~SG() { cudaStreamDestroy(s); } } sg{P->st};
+    const size_t bytes = (size_t)n * (size_t)(n - 1) / 2 * sizeof(float);
+    P->lt_copy.ensure(std::max<size_t>(bytes, 4));
+    DevBuf dr, dc, dd;
+    dr.ensure(std::max<int64_t>(nnz, 1) * 4);
+    dc.ensure(std::max<int64_t>(nnz, 1) * 4);
+    dd.ensure(std::max<int64_t>(nnz, 1) * 4);
+    if (nnz) {
+      CUDA_TRY(cudaMemcpyAsync(dr.p, rows, (size_t)nnz * 4, cudaMemcpyHostToDevice, P->st));
+      CUDA_TRY(cudaMemcpyAsync(dc.p, cols, (size_t)nnz * 4, cudaMemcpyHostToDevice, P->st));
+      CUDA_TRY(cudaMemcpyAsync(dd.p, dist, (size_t)nnz * 4, cudaMemcpyHostToDevice, P->st));
+    }
+    vr::launch_coo_to_dense(dr.as<int32_t>(), dc.as<int32_t>(), dd.as<float>(), nnz, n, P->lt_copy.as<float>(), P->st);
+    CUDA_TRY(cudaGetLastError());
+    P->d_lt = P->lt_copy.as<float>();
+    run_full(*P);
+    CUDA_TRY(cudaStreamSynchronize(P->st));
+    std::unique_ptr<vr_result> R(std::move(P->R));
+    P.reset();
+    *out = R.release();
+  });
+}
+
 int vr_barcodes(const float* lt, int64_t n, int32_t max_dim, float threshold, const vr_options* opt, vr_result** out) {
   if (out) *out = nullptr;
   SectionTimer ST;

@@ -96,6 +96,9 @@ struct HostPairs {
 // Page-locked host array (cudaHostAlloc) from a process-wide cache, so the n*n rank
 // matrix comes back at full PCIe/C2C bandwidth and the next call reuses the pages.
 void* pinned_acquire(size_t& bytes);
+// COO input -> dense lower triangle on the device (+inf = absent edge)
+void launch_coo_to_dense(const int32_t* ii, const int32_t* jj, const float* dd, int64_t nnz, int64_t n, float* lt,
+                         cudaStream_t st);
 // message returned by vr_last_error() (thread-local)
 void set_last_error(const std::string& msg);
 // device blocks from the process-wide cache (vr_api.cu); bytes is rounded up on return

@@ -476,3 +476,30 @@ def test_apparent_rate_matches_paper_at_10000_points():
         be.close()
     assert abs(app / surv - 0.991127743) < 3e-4
     assert app / N <= (n - 2) / n  # Theorem 5.4.2 bound
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_sparse_coo_input(seed):
+    # SPEC's sparse input / SURVEY §8(f) NEXT-2: only some pairs given; absent pairs are
+    # absent edges.  Against the oracle on the dense matrix with those entries at +inf and
+    # a finite threshold (the largest given distance), and against the dense entry point
+    rng = np.random.default_rng(seed)
+    n, D = 24, 2
+    lt = G.random_cloud(n, 30 + seed)
+    keep = rng.random(lt.size) < 0.6
+    ii, jj = np.tril_indices(n, -1)
+    rows, cols, dist = ii[keep], jj[keep], lt[keep]
+    dense = np.where(keep, lt, np.float32(np.inf)).astype(np.float32)
+    t = float(dist.max())
+    got = vr.barcodes_coo(n, rows, cols, dist, D, index_pairs=True)          # threshold +inf
+    got2 = vr.barcodes_coo(n, cols, rows, dist, D, t)                        # transposed pairs
+    ref = O.barcode(dense, n, D, t)
+    for d in range(D + 1):
+        exp = ref.positive(d)
+        assert np.array_equal(got.pairs[d].view(np.uint32), exp.view(np.uint32)), d
+        assert np.array_equal(got2.pairs[d], got.pairs[d])
+    den = vr.barcodes(dense, n, D)
+    for d in range(D + 1):
+        assert np.array_equal(den.pairs[d], got.pairs[d])
+    with pytest.raises(Exception):
+        vr.barcodes_coo(n, [0], [0], [1.0], D)
