@@ -343,6 +343,16 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    # north_star: "next to the paper's quoted Ripser++ speedups with their GPU model (context
+    # only)" — PAPER.md Table 5.2, Tesla V100 32 GB + 2x Xeon E5-2680 v4,
+    # on the paper's own datasets (ours are synthetic look-alikes of the same n, d)
+    line["paper_context"] = {
+        "hardware": "Tesla V100 32GB HBM2 + 2x Xeon E5-2680 v4 (PAPER.md P:5741)",
+        "table": "PAPER.md Table 5.2 (P:5773-5779): total execution time, Ripser++ vs Ripser",
+        "sphere_3_192_d3": {"ripserpp_s": 2.43, "ripser_s": 36.96, "speedup": 15.21},
+        "dragon1000_d2": {"ripserpp_s": 5.79, "ripser_s": 48.98, "speedup": 8.46},
+        "o3_4096_d3_t1.4": {"ripserpp_s": 11.62, "ripser_s": 64.18, "speedup": 5.52},
+    }
     if not args.no_target and world == 1:
         # BASELINE.json north_star target: "the dim-2 n=4096 workload under 1 s on one B200"
         # (reading A22: config 5's o3-shaped cloud at max_dim = 2, t = 1.4), end to end
