@@ -548,18 +548,26 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
       cu1 = x;
       cv0 = (int)(ii - (uint32_t)x * (uint32_t)(x - 1) / 2);
     }
+    // n <= kWinMaxN here: every rank-matrix offset fits 32 bits, and the rows of the
+    // chunk-invariant vertices u_2..u_D are fixed for the whole chunk
+    const uint32_t* __restrict__ rowq[D + 1];
+#pragma unroll
+    for (int q = 2; q <= D; ++q) rowq[q] = T.rank + (uint32_t)u[q] * (uint32_t)n;
+    const uint32_t len = (uint32_t)(iend - i0);
+    const uint64_t c0 = cU + i0;  // cidx of the chunk's first candidate
+    uint32_t scan_chunk = 0;
     int r1_u1 = -1;
     uint32_t r1[D + 1], r1_pm = 0;
-    for (uint64_t base = i0; base < iend; base += 32) {
-      const uint64_t i = base + (uint64_t)lane;
-      const bool valid = i < iend;
-      if (base != i0) {
+    for (uint32_t off = 0; off < len; off += 32) {
+      const uint32_t il = off + (uint32_t)lane;
+      const bool valid = il < len;
+      if (off != 0) {
         cv0 += 32;
         while (cv0 >= cu1) { cv0 -= cu1; ++cu1; }
       }
       const int u1 = valid ? cu1 : 1, v0 = valid ? cv0 : 0;
       u[1] = u1;
-      const uint32_t* __restrict__ rowu1 = T.rank + (size_t)u1 * (size_t)n;
+      const uint32_t* __restrict__ rowu1 = T.rank + (uint32_t)u1 * (uint32_t)n;
       uint32_t a[D + 1];
       if (u1 != r1_u1) {  // R[u_1][u_b] only when the lane's u_1 moved on
         r1_u1 = u1;
@@ -576,14 +584,14 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
       rs = umax(rs, a[1]);
 #pragma unroll
       for (int q = 2; q <= D; ++q) {
-        a[q] = valid ? rank_at(T, u[q], v0) : VR_RINF;
+        a[q] = valid ? __ldg(rowq[q] + v0) : VR_RINF;
         rs = umax(rs, a[q]);
       }
       const bool surv = valid && rs != VR_RINF;
       const uint32_t msurv = __ballot_sync(0xffffffffu, surv);
       if (!msurv) continue;
       surv_c += surv;
-      const uint64_t cidx = cU + i;
+      const uint64_t cidx = c0 + il;
       bool cleared = false;
       if (B.clr && surv) cleared = bit_test(B.clr, cidx);
       clr_c += cleared;
@@ -618,8 +626,8 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
           const int v = n - 1 - j;
           uint32_t m = 0;
 #pragma unroll
-          for (int q = 1; q <= D; ++q) m = umax(m, (q == 1) ? __ldg(rowu1 + v) : rank_at(T, u[q], v));
-          if (active && m <= rs && umax(m, __ldg(rowtop - (size_t)j * (size_t)n + v0)) <= rs) {
+          for (int q = 1; q <= D; ++q) m = umax(m, __ldg((q == 1 ? rowu1 : rowq[q]) + v));
+          if (active && m <= rs && umax(m, __ldg(rowtop - (uint32_t)j * (uint32_t)n + v0)) <= rs) {
             hitv = v;
             active = false;
           }
@@ -627,7 +635,7 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
         }
       }
       const int examined = hitv >= 0 ? n - hitv : (active ? steps : 0);
-      scan_c += (unsigned)examined;
+      scan_chunk += (unsigned)examined;
       // condition 2 (as in process_row)
       bool app = hitv >= 0;
       if (hitv >= 0 && hitv < u[D]) {  // else no vertex of s above the hit: apparent
@@ -689,10 +697,10 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
           }
         }
       }
-      const uint64_t key = ((uint64_t)(p.maxr - rs) << p.cbits) | cidx;
       const bool to_resid = B.clr && hitv >= 0 && !app;
       const bool to_queue = active || (!B.clr && hitv >= 0 && !app);
       if (__any_sync(0xffffffffu, to_resid | to_queue)) {  // rare: skip the appends' collectives
+        const uint64_t key = ((uint64_t)(p.maxr - rs) << p.cbits) | cidx;
         const unsigned long long rslot = warp_append(to_resid, &B.ctr->residual);
         if (to_resid && rslot < B.rcap) B.resid[rslot] = key;
         const unsigned long long qslot = warp_append(to_queue, &B.ctr->queued);
@@ -706,6 +714,7 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
         }
       }
     }
+    scan_c += scan_chunk;
   }
   const unsigned long long surv_acc = __reduce_add_sync(0xffffffffu, surv_c);
   const unsigned long long app_acc = __reduce_add_sync(0xffffffffu, app_c);
