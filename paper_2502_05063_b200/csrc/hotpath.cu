@@ -476,7 +476,6 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
   unsigned long long scan_c = 0;
   const int steps = p.steps < n ? p.steps : n;
   const int wsteps4 = (steps < 32 ? steps : 32) & ~3;
-  const uint32_t* __restrict__ rowtop = T.rank + (size_t)(n - 1) * (size_t)n;
   // shards: chunk c belongs to rank (nchunks-1-c) mod world (the chunks partition the
   // candidates, as the rows do for the row kernel)
   const uint64_t SW = (uint64_t)p.shard_world, SR = (uint64_t)p.shard_rank;
@@ -550,11 +549,15 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
     }
     // n <= kWinMaxN here: every rank-matrix offset fits 32 bits, and the rows of the
     // chunk-invariant vertices u_2..u_D are fixed for the whole chunk
-    const uint32_t* __restrict__ rowq[D + 1];
+    const uint32_t* __restrict__ rk = T.rank;
+    uint32_t oq[D + 1];  // row offsets of u_2..u_D
 #pragma unroll
-    for (int q = 2; q <= D; ++q) rowq[q] = T.rank + (uint32_t)u[q] * (uint32_t)n;
+    for (int q = 2; q <= D; ++q) oq[q] = (uint32_t)u[q] * (uint32_t)n;
     const uint32_t len = (uint32_t)(iend - i0);
     const uint64_t c0 = cU + i0;  // cidx of the chunk's first candidate
+    // clearing-bitmap words of the chunk: bit c0 + il = bit (cb + il) of clrw
+    const uint32_t* __restrict__ clrw = B.clr ? B.clr + (c0 >> 5) : nullptr;
+    const uint32_t cb = (uint32_t)(c0 & 31);
     uint32_t scan_chunk = 0;
     int r1_u1 = -1;
     uint32_t r1[D + 1], r1_pm = 0;
@@ -567,24 +570,24 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
       }
       const int u1 = valid ? cu1 : 1, v0 = valid ? cv0 : 0;
       u[1] = u1;
-      const uint32_t* __restrict__ rowu1 = T.rank + (uint32_t)u1 * (uint32_t)n;
+      const uint32_t o1 = (uint32_t)u1 * (uint32_t)n;
       uint32_t a[D + 1];
       if (u1 != r1_u1) {  // R[u_1][u_b] only when the lane's u_1 moved on
         r1_u1 = u1;
         r1_pm = pmU;
 #pragma unroll
         for (int b = 2; b <= D; ++b) {
-          r1[b] = __ldg(rowu1 + u[b]);
+          r1[b] = __ldg(rk + (o1 + (uint32_t)u[b]));
           r1_pm = umax(r1_pm, r1[b]);
         }
       }
       const uint32_t pm_up = r1_pm;
       uint32_t rs = pm_up;
-      a[1] = valid ? __ldg(rowu1 + v0) : VR_RINF;
+      a[1] = valid ? __ldg(rk + (o1 + (uint32_t)v0)) : VR_RINF;
       rs = umax(rs, a[1]);
 #pragma unroll
       for (int q = 2; q <= D; ++q) {
-        a[q] = valid ? __ldg(rowq[q] + v0) : VR_RINF;
+        a[q] = valid ? __ldg(rk + (oq[q] + (uint32_t)v0)) : VR_RINF;
         rs = umax(rs, a[q]);
       }
       const bool surv = valid && rs != VR_RINF;
@@ -593,7 +596,10 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
       surv_c += surv;
       const uint64_t cidx = c0 + il;
       bool cleared = false;
-      if (B.clr && surv) cleared = bit_test(B.clr, cidx);
+      if (clrw && surv) {
+        const uint32_t bo = cb + il;
+        cleared = (__ldg(clrw + (bo >> 5)) >> (bo & 31)) & 1u;
+      }
       clr_c += cleared;
       bool active = surv && !cleared;
       int hitv = -1;
@@ -626,8 +632,8 @@ __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimP
           const int v = n - 1 - j;
           uint32_t m = 0;
 #pragma unroll
-          for (int q = 1; q <= D; ++q) m = umax(m, __ldg((q == 1 ? rowu1 : rowq[q]) + v));
-          if (active && m <= rs && umax(m, __ldg(rowtop - (uint32_t)j * (uint32_t)n + v0)) <= rs) {
+          for (int q = 1; q <= D; ++q) m = umax(m, __ldg(rk + ((q == 1 ? o1 : oq[q]) + (uint32_t)v)));
+          if (active && m <= rs && umax(m, __ldg(rk + ((uint32_t)v * (uint32_t)n + (uint32_t)v0))) <= rs) {
             hitv = v;
             active = false;
           }
