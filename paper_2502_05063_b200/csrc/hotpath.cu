@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(HP_THREADS) k_enumerate(Tables T, DimParams p,
 // row tails, and the per-row setup (prefix maxima, window, cidx base) becomes per-chunk.
 // Per lane the row-dependent parts (R[u_1][u_b], R[u_1][v] in the window) are read for the
 // lane's own u_1 (mostly shared by the warp).  Same tests and outputs as process_row.
-constexpr int FL_CHUNK = 1024;  // largest chunk
+constexpr int FL_CHUNK = 1024;  // largest chunk (VR_FL_CHUNK overrides, for tuning runs)
 
 template <int D>
 __global__ void __launch_bounds__(HP_THREADS, 4) k_enumerate_flat(Tables T, DimParams p, HotBuffers B,
@@ -922,7 +922,9 @@ static const FlatTable* flat_table(int64_t n, int D) {
     const uint64_t total = binom_u64((uint64_t)n, D + 1);
     uint64_t c = total / ((uint64_t)sms * 24);
     c = (c + 31) / 32 * 32;
-    ft.chunk = (int)std::max<uint64_t>(128, std::min<uint64_t>((uint64_t)FL_CHUNK, c));
+    uint64_t cap = FL_CHUNK;
+    if (const char* e = std::getenv("VR_FL_CHUNK")) cap = std::max<uint64_t>(128, (uint64_t)std::atoll(e) / 32 * 32);
+    ft.chunk = (int)std::max<uint64_t>(128, std::min<uint64_t>(cap, c));
   }
   const uint64_t CH = (uint64_t)ft.chunk;
   // walk the (D-1)-subsets in colex order; u_2 = the smallest element
