@@ -40,6 +40,9 @@ import numpy as np  # noqa: E402
 from datagen import clouds as G  # noqa: E402
 
 METRIC = "hot-path simplices/s (VR barcodes, dims 1..max_dim)"
+# the JSON line goes to the process's real stdout; everything else a library may print on
+# fd 1 (e.g. NCCL's version banner at communicator init) is sent to stderr (see main())
+OUT = sys.stdout
 UNIT = "simplices/s"
 
 
@@ -186,7 +189,7 @@ def run_reference(args, rank, world):
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"first {m} points of {cfg.name} per step, max_dim={D}"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=OUT, flush=True)
 
 
 def run_ours(args, rank, world, local_rank):
@@ -288,6 +291,16 @@ def run_ours(args, rank, world, local_rank):
         tm = {"rank_ops_enumerate": 0.0, "rank_ops_resolve": 0.0}
     else:
         tm = plan.timing()
+    # the workload's method-level op count — a property of the workload, not of
+    # the sharding (the shards partition the candidates; every candidate's scan is its own):
+    # from an UNTIMED single-GPU plan of the same input when the timed path is sharded
+    if a_ref is not None:
+        ops_total = tm["rank_ops_enumerate"] + tm["rank_ops_resolve"]
+    else:
+        p1 = vr.Plan(dev_lt, n, D, cfg.threshold, stream=stream)
+        t1 = p1.timing()
+        ops_total = t1["rank_ops_enumerate"] + t1["rank_ops_resolve"]
+        p1.close()
     per = {k: stage[k] / args.steps for k in stage}
     # roofline of the dominant kernel: k_enumerate is ALU-bound —
     # algorithmic work = SURVEY.md 8(d)'s integer-op figure (computed by the library);
@@ -325,6 +338,16 @@ def run_ours(args, rank, world, local_rank):
                            "work = SURVEY.md 8(d) per-unit figures: 2 integer ops per rank read (d per candidate, "
                            "(d+1) per scanned cofacet vertex, C(d+2,2) per tested column) + (d+1)*ceil(log2 n) "
                            "decode compares per tested column"}
+    # step-level roofline at every N: the workload's rank ops over the WHOLE step time (all
+    # kernels, sort and exchanges included) against N GPUs' ALU peak — a lower bound on the
+    # dominant kernel's fraction, and the number that stays defined for the sharded path
+    step_ach = ops_total / (ms_per_step / 1000.0) / 1e12 if ms_per_step > 0 else None
+    roof["step"] = {"achieved": step_ach, "peak": alu_peak * world, "unit": "Tops/s",
+                    "frac": (step_ach / (alu_peak * world)) if step_ach else None, "ops_per_step": ops_total,
+                    "what": "workload rank ops / whole hot-path step time, vs n_gpus x ALU peak"}
+    if a_ref is None:  # sharded: no per-kernel events; the step-level figure is the roofline
+        roof.update({"kernel": "hot path step (sharded)", "achieved": step_ach, "peak": alu_peak * world,
+                     "frac": roof["step"]["frac"], "ops_per_step": ops_total, "ms_per_step": ms_per_step})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -377,11 +400,15 @@ def run_ours(args, rank, world, local_rank):
             line["cpu_ripser"] = ripser_style_run(cfg, D, bc.threshold, bc.pairs)
         except Exception as e:  # pragma: no cover
             line["cpu_ripser"] = {"error": str(e)}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=OUT, flush=True)
 
 
 def main():
+    global OUT
     args = parse()
+    sys.stdout.flush()
+    OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
