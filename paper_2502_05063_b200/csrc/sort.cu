@@ -4,7 +4,10 @@
 // cidx, which gives diam desc, cidx asc. LSD, only the significant bits".  The paper's
 // Alg 18 line 5 calls an unnamed library GPU-sort; this is our own.
 //
-// One pass per 8-bit digit, three launches per pass:
+// Up to 131072 keys (RS_CL_MAX x RS_SMALL_CAP): ONE launch of one thread-block cluster,
+// every pass in distributed shared memory (rs_cluster; rs_small below 8192 keys).  Larger:
+// one cooperative launch (rs_coop) or, past its co-residency limit,
+// one pass per 8-bit digit, three launches per pass:
 //   rs_hist     per-tile digit histogram  (reads 8 B/key)
 //   scan        exclusive scan of the digit-major [256][tiles] histogram
 //   rs_scatter  stable in-tile ranking (warp __match_any_sync multisplit over contiguous
@@ -13,6 +16,7 @@
 // Stability: inside a tile order is (digit, position); across tiles the digit-major scan
 // orders tiles — so each pass is a stable counting sort, as LSD requires.
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <cooperative_groups.h>
@@ -296,6 +300,115 @@ __global__ void __launch_bounds__(RS_THREADS) rs_small(uint64_t* __restrict__ ke
   for (int i = threadIdx.x; i < n; i += RS_THREADS) keys[i] = A[i];
 }
 
+// Whole sort of n <= RS_CL_MAX * RS_SMALL_CAP keys by ONE thread-block cluster (up to 16
+// CTAs of 1024 threads, one per SM): the keys stay in the cluster's distributed shared
+// memory for every pass.  Per pass: each CTA counts the digits of its tile per warp segment
+// and publishes the tile's counts in its own shared memory; cluster barrier; every CTA reads
+// all tiles' counts over DSMEM (digit totals + the counts of lower-ranked CTAs = the stable
+// global start of each of its digits) and ranks its keys (warp multisplit, stable) straight
+// into the owning CTA's next-pass buffer (DSMEM stores); cluster barrier.  No grid-wide
+// barrier and no global-memory round trip between passes.
+constexpr int RS_CL_MAX = 16;
+constexpr int CL_THREADS = 1024;
+constexpr int CL_WARPS = CL_THREADS / 32;
+
+__device__ __forceinline__ uint32_t block_exclusive_scan_1024(uint32_t x, uint32_t* warp_tot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) warp_tot[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t t = warp_tot[lane];
+    uint32_t ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += y;
+    }
+    warp_tot[lane] = ti - t;
+  }
+  __syncthreads();
+  const uint32_t r = warp_tot[w] + inc - x;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(CL_THREADS, 1) rs_cluster(uint64_t* __restrict__ keys, int n, int begin_bit, int end_bit,
+                                                            int tile) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int me = (int)cl.block_rank();
+  const int csize = (int)cl.num_blocks();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  extern __shared__ __align__(16) unsigned char rs_smem[];
+  uint64_t* A = (uint64_t*)rs_smem;            // this pass's input tile
+  uint64_t* Bk = A + RS_SMALL_CAP;             // this pass's output tile (written by every CTA)
+  uint32_t* whist = (uint32_t*)(Bk + RS_SMALL_CAP);  // [CL_WARPS][RS_BINS]
+  uint32_t* hist = whist + CL_WARPS * RS_BINS;  // this tile's digit counts (read by the cluster)
+  uint32_t* gofs = hist + RS_BINS;              // global start of this tile's keys of each digit
+  __shared__ uint32_t warp_tot[CL_WARPS];
+  const int base = me * tile;
+  const int cnt = n - base < tile ? (n - base > 0 ? n - base : 0) : tile;
+  const int seg = ((cnt + CL_WARPS * 32 - 1) / (CL_WARPS * 32)) * 32;  // keys per warp segment
+  const int seg0 = w * seg;
+  for (int i = threadIdx.x; i < cnt; i += CL_THREADS) A[i] = keys[base + i];
+  for (int shift = begin_bit; shift < end_bit; shift += 8) {
+    const uint32_t dmask = end_bit - shift >= 8 ? 0xFFu : ((1u << (end_bit - shift)) - 1u);
+    for (int i = threadIdx.x; i < CL_WARPS * RS_BINS; i += CL_THREADS) whist[i] = 0;
+    __syncthreads();
+    for (int i = seg0 + lane; i < seg0 + seg; i += 32)
+      if (i < cnt) atomicAdd(&whist[w * RS_BINS + ((uint32_t)(A[i] >> shift) & dmask)], 1u);
+    __syncthreads();
+    if (threadIdx.x < RS_BINS) {  // prefix over warp segments (stability) and the tile count
+      const int b = threadIdx.x;
+      uint32_t run = 0;
+      for (int q = 0; q < CL_WARPS; ++q) {
+        const uint32_t t = whist[q * RS_BINS + b];
+        whist[q * RS_BINS + b] = run;
+        run += t;
+      }
+      hist[b] = run;
+    }
+    cl.sync();  // every tile's counts published; the previous pass's scatter is complete
+    uint32_t tot = 0, before = 0;
+    if (threadIdx.x < RS_BINS) {
+      const int b = threadIdx.x;
+      for (int c = 0; c < csize; ++c) {
+        const uint32_t h = cl.map_shared_rank(hist, c)[b];
+        tot += h;
+        before += c < me ? h : 0u;
+      }
+    }
+    const uint32_t dig_start = block_exclusive_scan_1024(threadIdx.x < RS_BINS ? tot : 0u, warp_tot);
+    if (threadIdx.x < RS_BINS) gofs[threadIdx.x] = dig_start + before;
+    __syncthreads();
+    for (int i0 = seg0; i0 < seg0 + seg && i0 < cnt; i0 += 32) {
+      const int i = i0 + lane;
+      const bool valid = i < cnt;
+      const uint64_t k = valid ? A[i] : 0ull;
+      const uint32_t dg = valid ? ((uint32_t)(k >> shift) & dmask) : (RS_BINS + lane);
+      const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+      int pos = 0;
+      if (valid) pos = (int)(gofs[dg] + whist[w * RS_BINS + dg] + __popc(peers & lanemask_lt()));
+      __syncwarp();
+      if (valid && (lane == 31 - __clz(peers))) whist[w * RS_BINS + dg] += __popc(peers);
+      if (valid) {
+        const int dst = pos / tile;
+        cl.map_shared_rank(Bk, dst)[pos - dst * tile] = k;
+      }
+      __syncwarp();
+    }
+    cl.sync();  // the next pass's tiles are complete
+    uint64_t* t = A; A = Bk; Bk = t;
+  }
+  for (int i = threadIdx.x; i < cnt; i += CL_THREADS) keys[base + i] = A[i];
+}
+
 // Scatter for up to RS_FUSED_TILES tiles: the block computes its own digit offsets from
 // the per-tile histogram (no separate scan launch).
 constexpr uint32_t RS_FUSED_TILES = 256;
@@ -406,6 +519,53 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit,
   }
   if (n <= (size_t)RS_SMALL_CAP) {  // one CTA, all passes in shared memory
     rs_small<<<1, RS_THREADS, smem_small, st>>>(keys, (int)n, begin_bit, end_bit);
+    if (launches) *launches += 1;
+    return keys;
+  }
+  // one cluster, all passes in distributed shared memory
+  static int cl_max = -1;
+  const size_t smem_cl = 2 * RS_SMALL_CAP * sizeof(uint64_t) + (CL_WARPS * RS_BINS + 2 * RS_BINS) * sizeof(uint32_t);
+  if (cl_max < 0) {
+    cl_max = 0;
+    if (!std::getenv("VR_NO_CLUSTER_SORT") &&
+        cudaFuncSetAttribute(rs_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cl) == cudaSuccess &&
+        cudaFuncSetAttribute(rs_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+      for (int c = RS_CL_MAX; c >= 2 && cl_max == 0; c /= 2) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)c;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3((unsigned)c);
+        cfg.blockDim = dim3(CL_THREADS);
+        cfg.dynamicSmemBytes = smem_cl;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, (void*)rs_cluster, &cfg) == cudaSuccess && ncl > 0) cl_max = c;
+      }
+    }
+    cudaGetLastError();
+  }
+  if (cl_max > 0 && n <= (size_t)cl_max * RS_SMALL_CAP) {
+    int c = 2;
+    while ((size_t)c * RS_SMALL_CAP < n) c *= 2;
+    int tile = (int)((n + (size_t)c - 1) / (size_t)c);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)c;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)c);
+    cfg.blockDim = dim3(CL_THREADS);
+    cfg.dynamicSmemBytes = smem_cl;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nn = (int)n;
+    cudaLaunchKernelEx(&cfg, rs_cluster, keys, nn, begin_bit, end_bit, tile);
     if (launches) *launches += 1;
     return keys;
   }
