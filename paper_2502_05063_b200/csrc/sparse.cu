@@ -151,6 +151,7 @@ __device__ __forceinline__ void sparse_row(const Tables& T, const DimParams& p, 
     const uint64_t cidx = cbase + (uint64_t)v0;
     bool cleared = false;
     if (B.clr && surv) cleared = bit_test(B.clr, cidx);
+    else if (B.clr_hash && surv) cleared = hash_has(B.clr_hash, B.clr_hash_mask, cidx);
     clr_acc += __popc(__ballot_sync(0xffffffffu, cleared));
     bool active = surv && !cleared;
     int hitv = -1, examined = 0;
@@ -198,9 +199,10 @@ __device__ __forceinline__ void sparse_row(const Tables& T, const DimParams& p, 
       }
     }
     app_acc += __popc(__ballot_sync(0xffffffffu, app));
-    if (app && (B.clr_next || B.app_pairs)) {
+    if (app && (B.clr_next || B.clr_next_hash || B.app_pairs)) {
       const uint64_t tc = cofacet_cidx<D>(T, s, hitv);
       if (B.clr_next) bit_set(B.clr_next, tc);
+      if (B.clr_next_hash) hash_put(B.clr_next_hash, B.clr_next_hash_mask, tc);
       if (B.app_pairs) {
         const unsigned long long slot = atomicAdd(&B.ctr->app_pairs, 1ull);
         if (slot < B.app_cap) {
@@ -210,8 +212,9 @@ __device__ __forceinline__ void sparse_row(const Tables& T, const DimParams& p, 
       }
     }
     const uint64_t key = ((uint64_t)(p.maxr - rs) << p.cbits) | cidx;
-    const bool to_resid = B.clr && hitv >= 0 && !app;
-    const bool to_queue = active || (!B.clr && hitv >= 0 && !app);
+    const bool clrmode = B.clr || B.clr_hash;  // clearing decided above (else in phase 2)
+    const bool to_resid = clrmode && hitv >= 0 && !app;
+    const bool to_queue = active || (!clrmode && hitv >= 0 && !app);
     const unsigned long long rslot = warp_append(to_resid, &B.ctr->residual);
     if (to_resid && rslot < B.rcap) B.resid[rslot] = key;
     const unsigned long long qslot = warp_append(to_queue, &B.ctr->queued);
@@ -313,7 +316,8 @@ __global__ void __launch_bounds__(SP_THREADS) k_resolve_sparse(Tables T, DimPara
           if (j != a && j != b) ex[j] = umax(ex[j], r);
       }
     const int anchor = s[D - 1];  // u_1: the list phase 1 walked
-    const int v = coop_scan_nbr<D + 1>(T, SR, s, anchor, rs, B.clr ? p.steps : 0, scan_acc);
+    const bool clrmode = B.clr || B.clr_hash;
+    const int v = coop_scan_nbr<D + 1>(T, SR, s, anchor, rs, clrmode ? p.steps : 0, scan_acc);
     bool app = false;
     if (v >= 0) {
       bool bad = false;
@@ -335,9 +339,10 @@ __global__ void __launch_bounds__(SP_THREADS) k_resolve_sparse(Tables T, DimPara
     }
     if (app) {
       ++app_acc;
-      if (lane == 0 && (B.clr_next || B.app_pairs)) {
+      if (lane == 0 && (B.clr_next || B.clr_next_hash || B.app_pairs)) {
         const uint64_t tc = cofacet_cidx<D>(T, s, v);
         if (B.clr_next) bit_set(B.clr_next, tc);
+        if (B.clr_next_hash) hash_put(B.clr_next_hash, B.clr_next_hash_mask, tc);
         if (B.app_pairs) {
           const unsigned long long slot = atomicAdd(&B.ctr->app_pairs, 1ull);
           if (slot < B.app_cap) {
@@ -348,7 +353,7 @@ __global__ void __launch_bounds__(SP_THREADS) k_resolve_sparse(Tables T, DimPara
       }
       continue;
     }
-    if (!B.clr) {
+    if (!clrmode) {
       bool cleared = sorted_contains(B.deaths, B.ndeaths, cidx);
       if (D >= 2 && !cleared) {
         int js = -1;
@@ -382,6 +387,11 @@ __global__ void __launch_bounds__(SP_THREADS) k_resolve_sparse(Tables T, DimPara
     if (clr_acc) atomicAdd(&B.ctr->cleared, clr_acc);
     if (scan_acc) atomicAdd(&B.ctr->scanned2, scan_acc);
   }
+}
+
+__global__ void k_hash_put(const uint64_t* __restrict__ list, int64_t m, uint64_t* __restrict__ t, uint64_t mask) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    hash_put(t, mask, __ldg(list + i));
 }
 
 // ------------------------------------------------------------------ launchers
@@ -464,4 +474,13 @@ void launch_resolve_sparse(const DimParams& p, const uint32_t* rank, const uint6
   *launches += 1;
 }
 
+}  // namespace vr
+
+namespace vr {
+void launch_hash_put(const uint64_t* list, int64_t m, uint64_t* table, uint64_t mask, cudaStream_t st, int64_t* launches) {
+  if (m <= 0) return;
+  const int64_t blocks = std::min<int64_t>((m + 255) / 256, 148 * 8);
+  k_hash_put<<<(unsigned)blocks, 256, 0, st>>>(list, m, table, mask);
+  if (launches) *launches += 1;
+}
 }  // namespace vr

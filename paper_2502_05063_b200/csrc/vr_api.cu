@@ -222,6 +222,8 @@ struct DimRun {
   int64_t ndeaths_in = 0;
   DevBuf clr;        // clearing bitmap over the d-simplices (empty: recompute mode)
   size_t clr_words = 0;
+  DevBuf hash;       // sparse mode without a bitmap: hash set of the d-simplex pivots
+  uint64_t hash_mask = 0;  // slots - 1; 0 = no hash set (recompute mode)
   bool active = false;
 };
 
@@ -280,6 +282,28 @@ struct vr_plan {
   }
   uint32_t* clr_of(int d) {
     return (d >= 1 && d <= D && dims[(size_t)d].clr_words) ? dims[(size_t)d].clr.as<uint32_t>() : nullptr;
+  }
+  uint64_t* hash_of(int d) {
+    return (d >= 1 && d <= D && dims[(size_t)d].hash_mask) ? dims[(size_t)d].hash.as<uint64_t>() : nullptr;
+  }
+  uint64_t hash_mask_of(int d) { return hash_of(d) ? dims[(size_t)d].hash_mask : 0; }
+  // the hash-set fields of dimension d's HotBuffers
+  void hash_fields(vr::HotBuffers& B, int d) {
+    B.clr_hash = hash_of(d);
+    B.clr_hash_mask = hash_mask_of(d);
+    B.clr_next_hash = hash_of(d + 1);
+    B.clr_next_hash_mask = hash_mask_of(d + 1);
+  }
+  // (sized by the row bound, 2x rounded up to a power of two: most probes are misses, and a
+  // low load keeps them at one slot — measured: re-sizing to 2x the inserted count made the
+  // dimension-3 enumeration of config 5 12% slower)
+  void hash_reset(int d, cudaStream_t s) {
+    if (uint64_t* h = hash_of(d)) cudaMemsetAsync(h, 0xFF, (dims[(size_t)d].hash_mask + 1) * 8, s);
+  }
+  void hash_deaths(int d, cudaStream_t s) {  // deaths of dimension d-1 (deaths_in of d) into d's set
+    if (uint64_t* h = hash_of(d))
+      vr::launch_hash_put(dims[(size_t)d].deaths_in.as<uint64_t>(), dims[(size_t)d].ndeaths_in, h, dims[(size_t)d].hash_mask, s,
+                          &launches);
   }
   vr::SparseRows sparse_rows(int d, vr::DimCounters* ctr) {
     vr::SparseRows SR{};
@@ -504,9 +528,12 @@ void stage_setup(vr_plan& P) {
   P.dims.clear();
   P.dims.resize((size_t)D + 2);
   CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  // (tests: VR_FORCE_CLEAR_HASH puts sparse dimensions >= 2 on the hash-set path)
+  const bool force_hash = P.sparse && P.world == 1 && std::getenv("VR_FORCE_CLEAR_HASH") != nullptr;
   for (int d = 1; d <= D; ++d) {
     const uint64_t cand = binom_host((uint64_t)n, (uint64_t)d + 1);
     const size_t words = (size_t)((cand + 31) / 32);
+    if (force_hash && d >= 2) continue;
     if (cand && P.m && words * 4 <= kMaxBitmapBytes && words * 4 <= free_b / 16) {
       P.dims[(size_t)d].clr.ensure(words * 4);
       P.dims[(size_t)d].clr_words = words;
@@ -595,6 +622,24 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
       P.rows_cap[(size_t)d] = std::max<uint64_t>(bound, 1);
     }
   }
+  // sparse mode, no bitmap for dimension d+1 (C(n, d+2) bits too many), one GPU: the
+  // pivots of this dimension (apparent cofacets + residual deaths, at most `bound`) go into a
+  // hash set that dimension d+1 probes in phase 1 — instead of queueing every non-apparent
+  // column for the phase-2 recomputation
+  if (P.sparse && P.world == 1 && d < D && !P.clr_of(d + 1) && !std::getenv("VR_NO_CLEAR_HASH")) {
+    DimRun& nx = P.dims[(size_t)d + 1];
+    uint64_t slots = 1024;
+    while (slots < 2 * std::max<uint64_t>(bound, 1) + 1024) slots <<= 1;
+    size_t fb = 0, tb = 0;
+    CUDA_TRY(cudaMemGetInfo(&fb, &tb));
+    if (slots * 8 <= fb / 8) {
+      nx.hash.ensure(slots * 8);
+      nx.hash_mask = slots - 1;
+      P.hash_reset(d + 1, st);
+    } else {
+      nx.hash_mask = 0;
+    }
+  }
   ST.mark("  row bound");
   // queue / residual capacity: every candidate, bounded by a share of free device memory
   size_t free_b = 0, total_b = 0;
@@ -638,6 +683,7 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
     }
     vr::HotBuffers B{P.queue.as<uint64_t>(), P.qvert.as<uint4>(), P.qcap, P.resid.as<uint64_t>(), P.rcap,
                      P.clr_of(d), clr_next, dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, ctr, app_ptr, app_cap};
+    P.hash_fields(B, d);
     vr::SparseRows SR = P.sparse_rows(d, ctr);
     p.row_begin = rb;
     p.row_end = re;
@@ -707,7 +753,10 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
   stt.ms_enumerate = t_enum;
   stt.ms_resolve = t_res;
   stt.ms_sort = t_sort;
-  P.work_candidates += (double)cand;
+  // candidates the kernels actually examine: all C(n, d+1) dense; in sparse mode the
+  // (row, neighbour of u_1 below u_1) pairs, i.e. the row bound
+  const double cand_work = P.sparse ? (double)bound : (double)cand;
+  P.work_candidates += cand_work;
   P.work_scanned += (double)hc.scanned;
   P.work_scanned2 += (double)hc.scanned2;
   // algorithmic integer work, SURVEY.md §8(d) per-unit figures: 2 ops per rank read;
@@ -721,7 +770,7 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
     const double cd2 = (double)(d + 2) * (double)(d + 1) / 2.0;
     double queued = 0;
     for (auto& c : dr.chunks) queued += (double)c.queued;
-    P.work_rank_ops += 2.0 * d * (double)cand + 2.0 * (d + 1) * (double)hc.scanned + 2.0 * cd2 * tested +
+    P.work_rank_ops += 2.0 * d * cand_work + 2.0 * (d + 1) * (double)hc.scanned + 2.0 * cd2 * tested +
                        (double)(d + 1) * lg * tested;
     P.work_rank_ops2 += 2.0 * (d + 1) * (double)hc.scanned2 + (double)(d + 1) * lg * queued;
   }
@@ -764,6 +813,7 @@ void stage_dim_finish(vr_plan& P, int d, const uint64_t* keys, uint64_t nkeys) {
     if (!P.deaths.empty())
       CUDA_TRY(cudaMemcpyAsync(nx.deaths_in.p, P.deaths.data(), P.deaths.size() * 8, cudaMemcpyHostToDevice, st));
     if (P.clr_of(d + 1)) vr::launch_set_bits(nx.deaths_in.as<uint64_t>(), nx.ndeaths_in, P.clr_of(d + 1), st, &P.launches);
+    P.hash_deaths(d + 1, st);
     stt.ms_transfer += ms_since(tx);
   }
   stt.residual_columns = (int64_t)nkeys;
@@ -852,11 +902,13 @@ void replay(vr_plan& P) {
     cudaEventRecord(e1.first, st);
     cudaMemsetAsync(ctr, 0, sizeof(vr::DimCounters), st);
     if (clr_next) cudaMemsetAsync(clr_next, 0, P.dims[(size_t)d + 1].clr_words * 4, st);
+    P.hash_reset(d + 1, st);
     cudaEventRecord(e1.second, st);
     vr::DimParams p = dr.p;
     for (const Chunk& c : dr.chunks) {
       vr::HotBuffers B{P.queue.as<uint64_t>(), P.qvert.as<uint4>(), P.qcap, P.resid.as<uint64_t>(), P.rcap,
                        clr_of(d), clr_next, dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, ctr, nullptr, 0};
+      P.hash_fields(B, d);
       vr::SparseRows SR = P.sparse_rows(d, ctr);
       p.row_begin = c.row_begin;
       p.row_end = c.row_end;
@@ -880,6 +932,7 @@ void replay(vr_plan& P) {
     if (d < P.D && clr_next)
       vr::launch_set_bits(P.dims[(size_t)d + 1].deaths_in.as<uint64_t>(), P.dims[(size_t)d + 1].ndeaths_in, clr_next,
                           st, &P.launches);
+    if (d < P.D) P.hash_deaths(d + 1, st);
     cudaEventRecord(e4.second, st);
   }
   P.used_events[0] = used[0]; P.used_events[1] = used[1]; P.used_events[2] = used[2]; P.used_events[3] = used[3];
@@ -1233,10 +1286,12 @@ int vr_dist_replay_dim(vr_plan* P, int32_t d) {
     uint32_t* clr_next = P->clr_of(d + 1);
     cudaMemsetAsync(ctr, 0, sizeof(vr::DimCounters), st);
     if (clr_next) cudaMemsetAsync(clr_next, 0, P->dims[(size_t)d + 1].clr_words * 4, st);
+    P->hash_reset(d + 1, st);
     vr::DimParams p = dr.p;
     for (const Chunk& c : dr.chunks) {
       vr::HotBuffers B{P->queue.as<uint64_t>(), P->qvert.as<uint4>(), P->qcap, P->resid.as<uint64_t>(), P->rcap,
                        P->clr_of(d), clr_next, dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, ctr, nullptr, 0};
+      P->hash_fields(B, d);
       vr::SparseRows SR = P->sparse_rows(d, ctr);
       p.row_begin = c.row_begin;
       p.row_end = c.row_end;
@@ -1259,6 +1314,7 @@ int vr_dist_replay_deaths(vr_plan* P, int32_t d) {
     if (d < P->D && P->clr_of(d + 1))
       vr::launch_set_bits(P->dims[(size_t)d + 1].deaths_in.as<uint64_t>(), P->dims[(size_t)d + 1].ndeaths_in,
                           P->clr_of(d + 1), P->st, &P->launches);
+    if (d < P->D) P->hash_deaths(d + 1, P->st);
     CUDA_TRY(cudaGetLastError());
   });
 }

@@ -128,6 +128,25 @@ __device__ __forceinline__ bool bit_test(const uint32_t* __restrict__ bm, uint64
   return (__ldg(bm + (i >> 5)) >> (i & 31)) & 1u;
 }
 __device__ __forceinline__ void bit_set(uint32_t* bm, uint64_t i) { atomicOr(bm + (i >> 5), 1u << (i & 31)); }
+// open-addressing set of 64-bit keys (~0 = empty slot, linear probing); the caller sizes the
+// table to at least twice the keys it can receive
+__device__ __forceinline__ uint64_t hash_slot(uint64_t x) {
+  x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull; x ^= x >> 33;
+  return x;
+}
+__device__ __forceinline__ void hash_put(uint64_t* t, uint64_t mask, uint64_t k) {
+  for (uint64_t i = hash_slot(k) & mask;; i = (i + 1) & mask) {
+    const unsigned long long prev = atomicCAS((unsigned long long*)(t + i), ~0ull, (unsigned long long)k);
+    if (prev == ~0ull || prev == k) return;
+  }
+}
+__device__ __forceinline__ bool hash_has(const uint64_t* t, uint64_t mask, uint64_t k) {
+  for (uint64_t i = hash_slot(k) & mask;; i = (i + 1) & mask) {
+    const uint64_t x = __ldcg(t + i);
+    if (x == k) return true;
+    if (x == ~0ull) return false;
+  }
+}
 
 template <int D>
 __device__ __forceinline__ uint4 pack_vertices(const int (&s)[D + 1]) {

@@ -60,7 +60,14 @@ struct HotBuffers {
   DimCounters* ctr;
   uint64_t* app_pairs;   // debug (index-level output): (s, t) per apparent pair, or nullptr
   uint64_t app_cap;
+  // sparse mode where a bitmap over C(n, d+1) cannot exist: the d-simplex pivots of
+  // dimension d-1 as an open-addressing hash set (key ~0 = empty, power-of-two slots)
+  const uint64_t* clr_hash;
+  uint64_t clr_hash_mask;
+  uint64_t* clr_next_hash;  // receives this dimension's apparent cofacets
+  uint64_t clr_next_hash_mask;
 };
+void launch_hash_put(const uint64_t* list, int64_t m, uint64_t* table, uint64_t mask, cudaStream_t st, int64_t* launches);
 void launch_enumerate(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
                       cudaStream_t st, int64_t* launches);
 void launch_resolve(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,

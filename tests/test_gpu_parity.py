@@ -293,6 +293,44 @@ def test_sparse_mode_config_subsample(name, m, D, steps):
     full_check(cfg.lower_tri(m), m, D, thr, sparse_mode=2, apparent_steps=steps)
 
 
+# sparse dimensions >= 2 with the clearing hash set instead of a bitmap (the path taken when
+# C(n, d+1) bits cannot be allocated, e.g. config 5 at dimension 3), forced at small n
+@pytest.mark.parametrize("seed,n,D,kind,thr", [c for c in CASES if c[2] >= 2][::2])
+def test_sparse_clear_hash_index_level(seed, n, D, kind, thr, monkeypatch):
+    monkeypatch.setenv("VR_FORCE_CLEAR_HASH", "1")
+    if kind == "tied":
+        lt = G.random_tied(n, seed, levels=3)
+    elif kind == "tied2":
+        lt = G.random_tied(n, seed, levels=8)
+    else:
+        lt = G.random_cloud(n, seed)
+    t = math.inf if thr == "inf" else (O.enclosing_radius(lt, n) if thr == "R" else float(np.quantile(lt, 0.6)))
+    full_check(lt, n, D, t, sparse_mode=2)
+
+
+@pytest.mark.parametrize("name,m,D", [("c5_o3_4096", 36, 2), ("c5_o3_4096", 22, 3), ("c2_s3_192", 24, 3)])
+@pytest.mark.parametrize("steps", [2, 32])
+def test_sparse_clear_hash_config_subsample(name, m, D, steps, monkeypatch):
+    monkeypatch.setenv("VR_FORCE_CLEAR_HASH", "1")
+    cfg = G.CONFIGS[name]
+    thr = 1.0 if name == "c5_o3_4096" else cfg.threshold
+    full_check(cfg.lower_tri(m), m, D, thr, sparse_mode=2, apparent_steps=steps)
+
+
+def test_config5_dim3_hash_equals_recompute(c5_lower_tri, monkeypatch):
+    # config 5 at max_dim 3 takes the hash set at dimension 3 by itself; the recompute path
+    # (VR_NO_CLEAR_HASH) must give the same barcode and the same counts
+    cfg = G.CONFIGS["c5_o3_4096"]
+    a = vr.barcodes(c5_lower_tri, cfg.n, 3, cfg.threshold)
+    monkeypatch.setenv("VR_NO_CLEAR_HASH", "1")
+    b = vr.barcodes(c5_lower_tri, cfg.n, 3, cfg.threshold)
+    for d in range(4):
+        assert np.array_equal(a.pairs[d], b.pairs[d])
+    for k in ("survivors", "apparent", "cleared", "residual_columns"):
+        assert a.stats[3][k] == b.stats[3][k], k
+    assert a.stats[3]["queued"] < b.stats[3]["queued"]
+
+
 @pytest.fixture(scope="module")
 def c5_lower_tri():
     return G.CONFIGS["c5_o3_4096"].lower_tri()
@@ -504,3 +542,26 @@ def test_sparse_coo_input(seed):
         assert np.array_equal(den.pairs[d], got.pairs[d])
     with pytest.raises(Exception):
         vr.barcodes_coo(n, [0], [0], [1.0], D)
+
+
+# ------------------------------------------------------------------ roofline work counters
+@pytest.mark.parametrize("name,D", [("c2_s3_192", 3), ("c5_o3_4096", 2), ("c4a_sierpinski512", 2)])
+def test_work_counter_rate_below_alu_peak(name, D):
+    # the SURVEY 8(d) op count the bench divides by kernel time must describe work the
+    # kernels really do: ops / measured kernel time can never exceed the ALU peak (148 SMs x
+    # 64 lanes x 2.1 GHz, a bound above any B200 clock) — a dense candidate count on the
+    # sparse path once gave 500x the peak
+    import torch
+    cfg = G.CONFIGS[name]
+    lt = torch.from_numpy(cfg.lower_tri()).cuda()
+    plan = vr.Plan(lt, cfg.n, D, cfg.threshold)
+    for _ in range(3):
+        plan.replay()
+    torch.cuda.synchronize()
+    tm = plan.timing()
+    plan.close()
+    peak = 148 * 64 * 2.1e9
+    assert tm["rank_ops_enumerate"] > 0
+    assert tm["rank_ops_enumerate"] / (tm["ms_enumerate"] / 1e3) < peak
+    if tm["ms_resolve"] > 0:
+        assert tm["rank_ops_resolve"] / (tm["ms_resolve"] / 1e3) < peak

@@ -1,32 +1,25 @@
-"""Hot-path device time vs the phase-1 tuning knobs (diagnostics)."""
-import itertools, json, math, os, sys
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path.insert(0, ROOT)
-import torch
-import paper_2502_05063_b200 as vr
-from datagen import clouds as G
+"""Sweep the phase-1 scan budget (vr_options.apparent_steps) on a config: device ms per stage
+of the hot path (plan replay, median of 10).  Diagnostics: python tools/steps_sweep.py c5_o3_4096 3 16 32 64 128"""
+import os
+import statistics
+import sys
 
-names = [a for a in sys.argv[1:] if not a.startswith("--")]
-combos = [(32, 2), (4, 3), (8, 3), (12, 3), (16, 3), (24, 3), (32, 3)]
-for name in names:
-    cfg = G.CONFIGS[name]
-    lt = torch.from_numpy(cfg.lower_tri()).cuda()
-    ref = None
-    for steps, var in combos:
-        plan = vr.Plan(lt, cfg.n, cfg.max_dim, cfg.threshold, apparent_steps=steps, scan_variant=var)
-        bars = [p.tobytes() for p in plan.result.pairs]
-        if ref is None:
-            ref = bars
-        assert bars == ref, "tuning changed the barcode"
-        for _ in range(3):
-            plan.replay()
-        acc = {"ms_tables": 0, "ms_enumerate": 0, "ms_resolve": 0, "ms_sort": 0}
-        for _ in range(5):
-            plan.replay()
-            t = plan.timing()
-            for k in acc:
-                acc[k] += t[k] / 5
-        q = sum(plan.result.stats[d]["queued"] for d in range(1, cfg.max_dim + 1))
-        print(json.dumps({"config": name, "steps": steps, "variant": var, "queued": q,
-                          **{k: round(v, 3) for k, v in acc.items()}, "total": round(sum(acc.values()), 3)}), flush=True)
-        plan.close()
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2502_05063_b200 as vr  # noqa: E402
+from datagen import clouds as G  # noqa: E402
+
+cfg = G.CONFIGS[sys.argv[1]]
+D = int(sys.argv[2])
+lt = torch.from_numpy(cfg.lower_tri()).cuda()
+for s in [int(x) for x in sys.argv[3:]]:
+    plan = vr.Plan(lt, cfg.n, D, cfg.threshold, apparent_steps=s)
+    rows = []
+    for _ in range(10):
+        plan.replay()
+        rows.append(plan.timing())
+    med = {k: round(statistics.median(r[k] for r in rows), 3) for k in ("ms_tables", "ms_enumerate", "ms_resolve", "ms_sort")}
+    st = plan.result.stats
+    print(s, med, round(sum(med.values()), 3), "queued", [st[d]["queued"] for d in range(1, D + 1)], flush=True)
+    plan.close()
