@@ -226,7 +226,7 @@ __device__ __forceinline__ void sparse_row(const Tables& T, const DimParams& p, 
 }
 
 template <int D>
-__global__ void __launch_bounds__(SP_THREADS) k_enum_sparse(Tables T, DimParams p, HotBuffers B, SparseRows S) {
+__global__ void __launch_bounds__(SP_THREADS, 8) k_enum_sparse(Tables T, DimParams p, HotBuffers B, SparseRows S) {
   const int lane = threadIdx.x & 31;
   unsigned long long surv_acc = 0, app_acc = 0, scan_acc = 0, clr_acc = 0;
   const uint64_t W = (uint64_t)p.shard_world;
