@@ -102,9 +102,11 @@ __device__ __forceinline__ void sparse_row(const Tables& T, const DimParams& p, 
   for (int i = 1; i <= D; ++i) cbase += binom(T, u[i], i + 1);
   const uint16_t* __restrict__ L = S.adj + __ldg(S.adj_off + u1);
   const int deg = (int)(__ldg(S.adj_off + u1 + 1) - __ldg(S.adj_off + u1));
-  // first neighbour below u_1 (L is descending)
+  // first neighbour below u_1 (L is descending): after the deg - deg_below(u_1) above it
   int k0 = 0;
-  {
+  if (S.deg_below) {
+    k0 = deg - (int)__ldg(S.deg_below + u1);
+  } else {
     int lo = 0, hi = deg;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;

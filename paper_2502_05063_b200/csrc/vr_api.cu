@@ -314,6 +314,7 @@ struct vr_plan {
       SR.rows_out = d < D ? rows[(size_t)d].as<uint4>() : nullptr;
       SR.rows_out_cap = d < D ? rows_cap[(size_t)d] : 0;
       SR.rows_out_count = &ctr->rows_out;
+      SR.deg_below = deg_below.as<uint32_t>();
     }
     return SR;
   }

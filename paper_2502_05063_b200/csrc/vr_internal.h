@@ -82,6 +82,8 @@ struct SparseRows {
   uint4* rows_out;                // survivors of dimension d (rows of d+1), or nullptr
   uint64_t rows_out_cap;
   unsigned long long* rows_out_count;
+  const uint32_t* deg_below;      // neighbours w < v per vertex (list position of the first one
+                                  // below v = deg(v) - deg_below(v)), or nullptr
 };
 void launch_adjacency(const uint32_t* rank, int n, uint32_t* deg, uint32_t* deg_below, uint32_t* off, uint16_t* adj,
                       void* scan_tmp, cudaStream_t st, int64_t* launches);
