@@ -549,8 +549,15 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit,
     cudaGetLastError();
   }
   if (cl_max > 0 && n <= (size_t)cl_max * RS_SMALL_CAP) {
+    // the smallest power-of-two cluster whose CTAs hold at most `per` keys each (capped at the
+    // largest cluster; VR_CL_TILE overrides `per`)
+    static const size_t per = []() {
+      const char* e = std::getenv("VR_CL_TILE");
+      const long long v = e ? std::atoll(e) : 0;
+      return (size_t)(v >= 256 && v <= RS_SMALL_CAP ? v : 2048);  // 2048: measured best (c2 edge sort 16 CTAs)
+    }();
     int c = 2;
-    while ((size_t)c * RS_SMALL_CAP < n) c *= 2;
+    while ((size_t)c * per < n && c < cl_max) c *= 2;
     int tile = (int)((n + (size_t)c - 1) / (size_t)c);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
