@@ -920,7 +920,9 @@ static const FlatTable* flat_table(int64_t n, int D) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t total = binom_u64((uint64_t)n, D + 1);
-    uint64_t c = total / ((uint64_t)sms * 24);
+    uint64_t wps = 24;  // target warps per SM (VR_FL_WARPS overrides, for tuning runs)
+    if (const char* e = std::getenv("VR_FL_WARPS")) wps = std::max<uint64_t>(1, (uint64_t)std::atoll(e));
+    uint64_t c = total / ((uint64_t)sms * wps);
     c = (c + 31) / 32 * 32;
     uint64_t cap = FL_CHUNK;
     if (const char* e = std::getenv("VR_FL_CHUNK")) cap = std::max<uint64_t>(128, (uint64_t)std::atoll(e) / 32 * 32);
