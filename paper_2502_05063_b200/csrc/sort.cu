@@ -517,11 +517,6 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit,
     cudaFuncSetAttribute(rs_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_small);
     g_rs_attr_done = true;
   }
-  if (n <= (size_t)RS_SMALL_CAP) {  // one CTA, all passes in shared memory
-    rs_small<<<1, RS_THREADS, smem_small, st>>>(keys, (int)n, begin_bit, end_bit);
-    if (launches) *launches += 1;
-    return keys;
-  }
   // one cluster, all passes in distributed shared memory
   static int cl_max = -1;
   const size_t smem_cl = 2 * RS_SMALL_CAP * sizeof(uint64_t) + (CL_WARPS * RS_BINS + 2 * RS_BINS) * sizeof(uint32_t);
@@ -547,6 +542,19 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit,
       }
     }
     cudaGetLastError();
+  }
+  // one CTA, all passes in shared memory: up to RS_SMALL_CAP keys without clusters, else
+  // up to VR_SMALL_SORT_MAX (default 2048) keys — above that a cluster of 2-4 CTAs of 1024
+  // threads sorts faster than one 256-thread CTA
+  static const size_t small_max = []() {
+    const char* e = std::getenv("VR_SMALL_SORT_MAX");
+    const long long v = e ? std::atoll(e) : 2048;
+    return (size_t)(v >= 0 && v <= RS_SMALL_CAP ? v : 2048);
+  }();
+  if (n <= (size_t)RS_SMALL_CAP && (cl_max == 0 || n <= small_max)) {
+    rs_small<<<1, RS_THREADS, smem_small, st>>>(keys, (int)n, begin_bit, end_bit);
+    if (launches) *launches += 1;
+    return keys;
   }
   if (cl_max > 0 && n <= (size_t)cl_max * RS_SMALL_CAP) {
     // the smallest power-of-two cluster whose CTAs hold at most `per` keys each (capped at the

@@ -255,7 +255,7 @@ def test_betti_circle_and_s3():
 
 
 # ------------------------------------------------------------------ a4 alone: the radix sort
-@pytest.mark.parametrize("n", [0, 1, 2, 100, 4096, 4097, 8192, 8193, 16385, 30000, 65537, 70000, 130122, 131072, 131073,
+@pytest.mark.parametrize("n", [0, 1, 2, 100, 2048, 2049, 3001, 4096, 4097, 8192, 8193, 16385, 30000, 65537, 70000, 130122, 131072, 131073,
                                1_200_000])
 @pytest.mark.parametrize("bits", [(0, 64), (0, 41), (8, 40)])
 def test_radix_sort_matches_numpy(n, bits):
