@@ -562,7 +562,7 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit,
     static const size_t per = []() {
       const char* e = std::getenv("VR_CL_TILE");
       const long long v = e ? std::atoll(e) : 0;
-      return (size_t)(v >= 256 && v <= RS_SMALL_CAP ? v : 2048);  // 2048: measured best (c2 edge sort 16 CTAs)
+      return (size_t)(v >= 256 && v <= RS_SMALL_CAP ? v : 1024);  // 1024: measured best (tools/ab_sort_sweep.sh)
     }();
     int c = 2;
     while ((size_t)c * per < n && c < cl_max) c *= 2;
