@@ -974,9 +974,11 @@ static void enumerate_d(const DimParams& p, const Tables& T, const HotBuffers& B
   } else {
     q.win = 0;
   }
-  // flattened chunks from d = 2 on (measured: equal on c2, -8% on c4a); dimension 1 has
-  // one super-row of n long rows and stays on the row kernel (VR_FLAT_MIN_D overrides)
-  static const int flat_min_d = std::getenv("VR_FLAT_MIN_D") ? std::atoi(std::getenv("VR_FLAT_MIN_D")) : 2;
+  // flattened chunks from d = 2 on (measured: equal on c2, -8% on c4a), and from d = 1 when
+  // n >= 128 (one super-row of n long rows: -3.5% on c4a, -0.3% on c2; +2.5% on c1, n = 64,
+  // where the row kernel stays); VR_FLAT_MIN_D overrides
+  static const int flat_min_env = std::getenv("VR_FLAT_MIN_D") ? std::atoi(std::getenv("VR_FLAT_MIN_D")) : -1;
+  const int flat_min_d = flat_min_env >= 0 ? flat_min_env : (q.n >= 128 ? 1 : 2);
   if (D >= flat_min_d && q.win && q.variant == 1 && q.row_begin == 0 &&
       q.row_end == binom_u64((uint64_t)q.n, D) && !getenv_flag("VR_NO_FLAT")) {
     const FlatTable* ft = flat_table(q.n, D);
