@@ -68,7 +68,10 @@ typedef struct {
 typedef struct {
   int32_t include_zero;  /* 0 (default): report birth < death only; 1: also zero-length pairs */
   int32_t index_pairs;   /* 1: also keep the index-level pairing (every pair, apparent ones
-                            included; intended for tests on small inputs) */
+                            included; intended for tests on small inputs); k > 1: the same,
+                            but at most k apparent pairs per dimension (an arbitrary subset —
+                            for sampled checks of full-size inputs).  The apparent pairs come
+                            first, then one entry per residual column */
   int32_t residual_mode; /* 0: reduction-matrix (V) mode (§5.2.9, default); 1: oblivious (Alg 12) */
   int32_t apparent_steps;/* cofacets tested per column in the first (lane-per-column) phase of
                             the apparent test before a column moves to the warp-cooperative
@@ -104,7 +107,12 @@ typedef struct {
   double ms_sort;          /* GPU: radix sort of the columns into coboundary order */
   double ms_residual;      /* host: residual reduction (dim 0: union-find) */
   double ms_transfer;      /* host<->device copies of this dimension's columns / pairs */
+  int64_t kernels;         /* VR_KERNEL_* flags of the enumeration kernels this dimension ran */
 } vr_stats;
+#define VR_KERNEL_ROW 1          /* k_enumerate: one warp per prefix row (dense) */
+#define VR_KERNEL_FLAT 2         /* k_enumerate_flat: flattened (u_1, v_0) chunks (dense) */
+#define VR_KERNEL_SPARSE 4       /* output-sensitive kernels (threshold-graph bitmap rows) */
+#define VR_KERNEL_SMEM_WINDOW 8  /* dense: the 32-vertex scan window staged in shared memory */
 
 typedef struct vr_result vr_result;
 

@@ -55,7 +55,12 @@ _STAT_TIMES = ["ms_enumerate", "ms_resolve", "ms_sort", "ms_residual", "ms_trans
 
 
 class _Stats(ctypes.Structure):
-    _fields_ = [(f, ctypes.c_int64) for f in _STAT_FIELDS] + [(f, ctypes.c_double) for f in _STAT_TIMES]
+    _fields_ = [(f, ctypes.c_int64) for f in _STAT_FIELDS] + [(f, ctypes.c_double) for f in _STAT_TIMES] + \
+               [("kernels", ctypes.c_int64)]
+
+
+# vr_stats.kernels flags (include/vr.h)
+KERNEL_ROW, KERNEL_FLAT, KERNEL_SPARSE, KERNEL_SMEM_WINDOW = 1, 2, 4, 8
 
 
 _lib = None
@@ -162,7 +167,7 @@ def _collect(h) -> Barcode:
         bc.index_pairs.append(ip)
         s = _Stats()
         _check(lib.vr_stats_get(h, d, ctypes.byref(s)))
-        bc.stats.append({f: getattr(s, f) for f in _STAT_FIELDS + _STAT_TIMES})
+        bc.stats.append({f: getattr(s, f) for f in _STAT_FIELDS + _STAT_TIMES + ["kernels"]})
     return bc
 
 

@@ -954,7 +954,7 @@ static const FlatTable* flat_table(int64_t n, int D) {
 }
 
 template <int D>
-static void enumerate_d(const DimParams& p, const Tables& T, const HotBuffers& B, cudaStream_t st) {
+static int enumerate_d(const DimParams& p, const Tables& T, const HotBuffers& B, cudaStream_t st) {
   const uint64_t rows = p.row_end - p.row_begin;
   const uint64_t warps_needed = (rows + (uint64_t)p.grab - 1) / (uint64_t)p.grab;
   uint64_t blocks = (warps_needed * 32 + HP_THREADS - 1) / HP_THREADS;
@@ -994,10 +994,11 @@ static void enumerate_d(const DimParams& p, const Tables& T, const HotBuffers& B
       if (fb > cap) fb = cap;
       if (fb < 1) fb = 1;
       k_enumerate_flat<D><<<(unsigned)fb, HP_THREADS, smem, st>>>(T, q, B, ft->d_start, ft->nsuper, ft->nchunks, ft->chunk);
-      return;
+      return VR_KERNEL_FLAT | VR_KERNEL_SMEM_WINDOW;
     }
   }
   k_enumerate<D><<<(unsigned)blocks, HP_THREADS, smem, st>>>(T, q, B);
+  return VR_KERNEL_ROW | (q.win ? VR_KERNEL_SMEM_WINDOW : 0);
 }
 
 template <int D>
@@ -1009,19 +1010,21 @@ static void resolve_d(const DimParams& p, const Tables& T, const HotBuffers& B, 
   k_resolve<D><<<(unsigned)blocks, HP_THREADS, 0, st>>>(T, p, B, qn);
 }
 
-void launch_enumerate(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
-                      cudaStream_t st, int64_t* launches) {
+int launch_enumerate(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
+                     cudaStream_t st, int64_t* launches) {
   Tables T{rank, binom, (int32_t)p.n, kmax};
+  int k = 0;
   switch (p.d) {
-    case 1: enumerate_d<1>(p, T, B, st); break;
-    case 2: enumerate_d<2>(p, T, B, st); break;
-    case 3: enumerate_d<3>(p, T, B, st); break;
-    case 4: enumerate_d<4>(p, T, B, st); break;
-    case 5: enumerate_d<5>(p, T, B, st); break;
-    case 6: enumerate_d<6>(p, T, B, st); break;
-    default: return;
+    case 1: k = enumerate_d<1>(p, T, B, st); break;
+    case 2: k = enumerate_d<2>(p, T, B, st); break;
+    case 3: k = enumerate_d<3>(p, T, B, st); break;
+    case 4: k = enumerate_d<4>(p, T, B, st); break;
+    case 5: k = enumerate_d<5>(p, T, B, st); break;
+    case 6: k = enumerate_d<6>(p, T, B, st); break;
+    default: return 0;
   }
   *launches += 1;
+  return k;
 }
 
 void launch_resolve(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,

@@ -261,7 +261,8 @@ struct vr_plan {
   std::vector<DimRun> dims;  // index d (1..D), dims[0] unused
   // output-sensitive mode: threshold-graph CSR and per-dimension survivor lists
   bool sparse = false;
-  DevBuf adj_off, adj, deg, deg_below, scan_tmp2, bound;
+  DevBuf bm, deg, deg_below, bound;  // threshold-graph bitmap (n x nw words), degrees
+  int32_t nw = 0;
   std::vector<DevBuf> rows;           // rows[d] = packed d-simplex survivors (rows of d+1)
   std::vector<uint64_t> rows_count;   // survivors written per dimension
   std::vector<uint64_t> rows_cap;
@@ -308,13 +309,12 @@ struct vr_plan {
   vr::SparseRows sparse_rows(int d, vr::DimCounters* ctr) {
     vr::SparseRows SR{};
     if (sparse) {
-      SR.adj_off = adj_off.as<uint32_t>();
-      SR.adj = adj.as<uint16_t>();
+      SR.bm = bm.as<uint32_t>();
+      SR.nw = nw;
       SR.rows_in = d == 1 ? nullptr : rows[(size_t)d - 1].as<uint4>();
       SR.rows_out = d < D ? rows[(size_t)d].as<uint4>() : nullptr;
       SR.rows_out_cap = d < D ? rows_cap[(size_t)d] : 0;
       SR.rows_out_count = &ctr->rows_out;
-      SR.deg_below = deg_below.as<uint32_t>();
     }
     return SR;
   }
@@ -324,6 +324,7 @@ namespace {
 
 const int kDefaultSteps = 32;
 const size_t kMaxBitmapBytes = (size_t)4 << 30;
+const size_t kSparseBitmapBytes = (size_t)64 << 20;
 
 uint64_t binom_host(uint64_t n, uint64_t k) {
   if (k > n) return 0;
@@ -499,27 +500,39 @@ void stage_setup(vr_plan& P) {
     if (mode == 2) sp = true;
     P.sparse = sp && D >= 1 && P.m > 0;
     if (P.sparse) {
+      P.nw = (int32_t)((n + 31) / 32);
       P.deg.ensure(((size_t)n + 1) * 4);
       P.deg_below.ensure(((size_t)n + 1) * 4);
-      P.adj_off.ensure(((size_t)n + 1) * 4);
-      P.adj.ensure(std::max<size_t>(2 * (size_t)P.m, 1) * 2);
-      P.scan_tmp2.ensure(vr::scan_temp_bytes((size_t)n + 1));
+      P.bm.ensure((size_t)n * (size_t)P.nw * 4);
       P.bound.ensure(8);
-      CUDA_TRY(cudaMemsetAsync(P.deg.p, 0, ((size_t)n + 1) * 4, st));
-      vr::launch_adjacency(P.rank.as<uint32_t>(), (int)n, P.deg.as<uint32_t>(), P.deg_below.as<uint32_t>(),
-                           P.adj_off.as<uint32_t>(), P.adj.as<uint16_t>(), P.scan_tmp2.p, st, &P.launches);
+      vr::launch_threshold_bitmap(P.rank.as<uint32_t>(), (int)n, P.bm.as<uint32_t>(), P.deg.as<uint32_t>(),
+                                  P.deg_below.as<uint32_t>(), st, &P.launches);
       CUDA_TRY(cudaGetLastError());
       P.rows.clear();
       P.rows.resize((size_t)D + 2);
       P.rows_count.assign((size_t)D + 2, 0);
       P.rows_cap.assign((size_t)D + 2, 0);
-      // the host residual walks the same threshold-graph adjacency
+      // the host residual walks the same threshold graph: neighbour lists (descending)
+      // from the bitmap
       auto ta = std::chrono::steady_clock::now();
-      M.adj_off.resize((size_t)n + 1);
-      CUDA_TRY(cudaMemcpyAsync(M.adj_off.data(), P.adj_off.p, ((size_t)n + 1) * 4, cudaMemcpyDeviceToHost, st));
+      std::vector<uint32_t> hbm((size_t)n * (size_t)P.nw);
+      CUDA_TRY(cudaMemcpyAsync(hbm.data(), P.bm.p, hbm.size() * 4, cudaMemcpyDeviceToHost, st));
       CUDA_TRY(cudaStreamSynchronize(st));
-      M.adj.resize((size_t)M.adj_off[(size_t)n]);
-      if (!M.adj.empty()) CUDA_TRY(cudaMemcpy(M.adj.data(), P.adj.p, M.adj.size() * 2, cudaMemcpyDeviceToHost));
+      M.adj_off.assign((size_t)n + 1, 0);
+      M.adj.clear();
+      M.adj.reserve(2 * (size_t)P.m);
+      for (int64_t v = 0; v < n; ++v) {
+        const uint32_t* row = hbm.data() + (size_t)v * (size_t)P.nw;
+        for (int k = P.nw - 1; k >= 0; --k) {
+          uint32_t x = row[k];
+          while (x) {
+            const int b = 31 - __builtin_clz(x);
+            M.adj.push_back((uint16_t)(32 * k + b));
+            x &= ~(1u << b);
+          }
+        }
+        M.adj_off[(size_t)v + 1] = (uint32_t)M.adj.size();
+      }
       R->stats[0].ms_transfer += ms_since(ta);
     }
   }
@@ -535,6 +548,10 @@ void stage_setup(vr_plan& P) {
     const uint64_t cand = binom_host((uint64_t)n, (uint64_t)d + 1);
     const size_t words = (size_t)((cand + 31) / 32);
     if (force_hash && d >= 2) continue;
+    // output-sensitive mode on one GPU: a bitmap only while it stays small (its bits are
+    // probed at random); beyond that the hash set of the pivots is smaller and L2-friendlier
+    // (config 5: 1 MiB at dimension 1; 1.4 GiB at dimension 2 -> hash set)
+    if (P.sparse && P.world == 1 && d >= 2 && words * 4 > kSparseBitmapBytes) continue;
     if (cand && P.m && words * 4 <= kMaxBitmapBytes && words * 4 <= free_b / 16) {
       P.dims[(size_t)d].clr.ensure(words * 4);
       P.dims[(size_t)d].clr_words = words;
@@ -659,7 +676,10 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
   uint64_t app_cap = 0;
   uint64_t* app_ptr = nullptr;
   if (P.opt.index_pairs) {
+    // index_pairs = 1: every apparent pair; k > 1: at most k of them (an arbitrary subset,
+    // for sampled checks at full size)
     app_cap = std::max<uint64_t>(bound, 1);
+    if (P.opt.index_pairs > 1) app_cap = std::min<uint64_t>(app_cap, (uint64_t)P.opt.index_pairs);
     P.app_pairs.ensure((size_t)app_cap * 16);
     app_ptr = P.app_pairs.as<uint64_t>();
   }
@@ -667,6 +687,7 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
   vr::DimCounters* ctr = P.ctrs.as<vr::DimCounters>() + d;
   CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(vr::DimCounters), st));
   float t_enum = 0, t_res = 0;
+  int64_t kernels = 0;
   uint64_t resid_count = 0;
   for (uint64_t rb = 0; rb < rows_total; rb += rows_per_chunk) {
     const uint64_t re = std::min(rows_total, rb + rows_per_chunk);
@@ -691,8 +712,12 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
     CUDA_TRY(cudaMemsetAsync(&ctr->row_next, 0, 8, st));
     CUDA_TRY(cudaMemsetAsync(&ctr->queued, 0, 8, st));
     CUDA_TRY(cudaEventRecord(P.ev[2], st));
-    if (P.sparse) vr::launch_enumerate_sparse(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, SR, st, &P.launches);
-    else vr::launch_enumerate(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, st, &P.launches);
+    if (P.sparse) {
+      vr::launch_enumerate_sparse(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, SR, st, &P.launches);
+      kernels |= VR_KERNEL_SPARSE;
+    } else {
+      kernels |= vr::launch_enumerate(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, st, &P.launches);
+    }
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(P.ev[3], st));
     unsigned long long q = 0;
@@ -754,6 +779,7 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
   stt.ms_enumerate = t_enum;
   stt.ms_resolve = t_res;
   stt.ms_sort = t_sort;
+  stt.kernels = kernels;
   // candidates the kernels actually examine: all C(n, d+1) dense; in sparse mode the
   // (row, neighbour of u_1 below u_1) pairs, i.e. the row bound
   const double cand_work = P.sparse ? (double)bound : (double)cand;
@@ -883,11 +909,9 @@ void replay(vr_plan& P) {
     cudaEventRecord(e.first, st);
     vr::launch_tables(P.d_lt, P.n, P.threshold, P.keys.as<uint64_t>(), P.alt.as<uint64_t>(), P.rowmax.as<uint32_t>(),
                       P.sort_tmp.p, P.rank.as<uint32_t>(), P.tout.as<vr::TablesOut>(), &sorted, st, &P.launches);
-    if (P.sparse) {
-      cudaMemsetAsync(P.deg.p, 0, ((size_t)P.n + 1) * 4, st);
-      vr::launch_adjacency(P.rank.as<uint32_t>(), (int)P.n, P.deg.as<uint32_t>(), P.deg_below.as<uint32_t>(),
-                           P.adj_off.as<uint32_t>(), P.adj.as<uint16_t>(), P.scan_tmp2.p, st, &P.launches);
-    }
+    if (P.sparse)
+      vr::launch_threshold_bitmap(P.rank.as<uint32_t>(), (int)P.n, P.bm.as<uint32_t>(), P.deg.as<uint32_t>(),
+                                  P.deg_below.as<uint32_t>(), st, &P.launches);
     if (P.D >= 1 && clr_of(1)) {
       cudaMemsetAsync(clr_of(1), 0, P.dims[1].clr_words * 4, st);
       vr::launch_set_bits(P.dims[1].deaths_in.as<uint64_t>(), P.dims[1].ndeaths_in, clr_of(1), st, &P.launches);
@@ -1264,11 +1288,9 @@ int vr_dist_replay_tables(vr_plan* P) {
     vr::launch_tables(P->d_lt, P->n, P->threshold, P->keys.as<uint64_t>(), P->alt.as<uint64_t>(),
                       P->rowmax.as<uint32_t>(), P->sort_tmp.p, P->rank.as<uint32_t>(), P->tout.as<vr::TablesOut>(),
                       &sorted, P->st, &P->launches);
-    if (P->sparse) {
-      cudaMemsetAsync(P->deg.p, 0, ((size_t)P->n + 1) * 4, P->st);
-      vr::launch_adjacency(P->rank.as<uint32_t>(), (int)P->n, P->deg.as<uint32_t>(), P->deg_below.as<uint32_t>(),
-                           P->adj_off.as<uint32_t>(), P->adj.as<uint16_t>(), P->scan_tmp2.p, P->st, &P->launches);
-    }
+    if (P->sparse)
+      vr::launch_threshold_bitmap(P->rank.as<uint32_t>(), (int)P->n, P->bm.as<uint32_t>(), P->deg.as<uint32_t>(),
+                                  P->deg_below.as<uint32_t>(), P->st, &P->launches);
     if (P->D >= 1 && P->clr_of(1)) {
       cudaMemsetAsync(P->clr_of(1), 0, P->dims[1].clr_words * 4, P->st);
       vr::launch_set_bits(P->dims[1].deaths_in.as<uint64_t>(), P->dims[1].ndeaths_in, P->clr_of(1), P->st, &P->launches);

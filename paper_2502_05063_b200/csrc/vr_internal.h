@@ -68,25 +68,25 @@ struct HotBuffers {
   uint64_t clr_next_hash_mask;
 };
 void launch_hash_put(const uint64_t* list, int64_t m, uint64_t* table, uint64_t mask, cudaStream_t st, int64_t* launches);
-void launch_enumerate(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
-                      cudaStream_t st, int64_t* launches);
+// returns the VR_KERNEL_* flags of the kernel launched (vr_stats.kernels)
+int launch_enumerate(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
+                     cudaStream_t st, int64_t* launches);
 void launch_resolve(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
                     uint64_t qn, cudaStream_t st, int64_t* launches);
 void launch_set_bits(const uint64_t* list, int64_t m, uint32_t* bm, cudaStream_t st, int64_t* launches);
 
 // ---------------------------------------------------------------- sparse.cu (output-sensitive mode)
 struct SparseRows {
-  const uint32_t* adj_off;        // CSR offsets of the threshold graph, n+1
-  const uint16_t* adj;            // neighbours, each list descending
+  const uint32_t* bm;             // threshold-graph bitmap, n rows of nw words (bit w of row v: d(v,w) <= t, v != w)
+  int32_t nw;                     // words per bitmap row, ceil(n / 32)
   const uint4* rows_in;           // packed (d-1)-simplex survivors = prefix rows; nullptr for d = 1
   uint4* rows_out;                // survivors of dimension d (rows of d+1), or nullptr
   uint64_t rows_out_cap;
   unsigned long long* rows_out_count;
-  const uint32_t* deg_below;      // neighbours w < v per vertex (list position of the first one
-                                  // below v = deg(v) - deg_below(v)), or nullptr
 };
-void launch_adjacency(const uint32_t* rank, int n, uint32_t* deg, uint32_t* deg_below, uint32_t* off, uint16_t* adj,
-                      void* scan_tmp, cudaStream_t st, int64_t* launches);
+// bitmap + deg(v) + deg_below(v) = #{w < v adjacent to v} from the rank matrix
+void launch_threshold_bitmap(const uint32_t* rank, int n, uint32_t* bm, uint32_t* deg, uint32_t* deg_below, cudaStream_t st,
+                             int64_t* launches);
 void launch_row_bound(const uint4* rows, uint64_t nrows, int dprev, const uint32_t* deg_below, unsigned long long* out,
                       cudaStream_t st, int64_t* launches);
 void launch_enumerate_sparse(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,

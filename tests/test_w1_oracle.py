@@ -96,3 +96,33 @@ def test_generators_above_the_diagonal():
     for P in (PD.gaussian(1000, 1), PD.clustered(1000, 2), PD.uniform(100, 3)):
         assert P.dtype == np.float32 and np.all(P[:, 1] > P[:, 0])
     assert len(np.unique(PD.clustered(2000, 4), axis=0)) < 2000  # coinciding points exist
+
+
+def test_rwmd_exact_values():
+    """Alg 20 by hand: L_A = Σ_{u∈Â} σ(u)·min(min_v ||u−v||, d_Δ(u)), L_B
+    likewise, RWMD = max(L_A, L_B).  Dropping the multiplicity σ, taking min(L_A, L_B)
+    instead of the max, using d_Δ = |d−b| (no √2) or skipping the diagonal option each
+    changes one of these values."""
+    # multiplicities: three copies of (0, 4) against one (0, 3).  Â = {(0,4)} with σ = 3:
+    # nearest is (0,3) at 1 < d_Δ = 4/√2, so L_A = 3·1 = 3; L_B = min(1, 3/√2) = 1
+    A = np.array([[0.0, 4.0]] * 3)
+    B = np.array([[0.0, 3.0]])
+    assert W.rwmd(A, B) == pytest.approx(3.0, rel=1e-12)
+    assert W.rwmd(B, A) == pytest.approx(3.0, rel=1e-12)
+    # asymmetric: L_A = d_Δ((0,1)) = 1/√2 (the diagonal beats both B points);
+    # L_B = min(9, 10/√2) + min(√386, 15/√2) = 10/√2 + 15/√2 = 25/√2 > L_A
+    A = np.array([[0.0, 1.0]])
+    B = np.array([[0.0, 10.0], [5.0, 20.0]])
+    assert W.rwmd(A, B) == pytest.approx(25.0 / R2, rel=1e-12)
+    # nearest neighbour beats the diagonal on both sides: L_A = L_B = 0.5
+    assert W.rwmd(np.array([[1.0, 5.0]]), np.array([[1.5, 5.0]])) == pytest.approx(0.5, rel=1e-12)
+    # σ(v) on the B side: two copies of (2, 2.5) (d_Δ = 0.5/√2) against (2, 9):
+    # L_A = 2·0.5/√2 (diagonal), L_B = min(6.5, 7/√2) = 7/√2 = 4.95 > L_A
+    A = np.array([[2.0, 2.5], [2.0, 2.5]])
+    B = np.array([[2.0, 9.0]])
+    assert W.rwmd(A, B) == pytest.approx(7.0 / R2, rel=1e-12)
+    assert W.rwmd(B, A) == pytest.approx(7.0 / R2, rel=1e-12)
+    # σ decides: four copies of (0, 2) against one (0.5, 2): L_A = 4·0.5 = 2 > L_B = 0.5
+    A = np.array([[0.0, 2.0]] * 4)
+    B = np.array([[0.5, 2.0]])
+    assert W.rwmd(A, B) == pytest.approx(2.0, rel=1e-12)
