@@ -11,7 +11,7 @@ LIB = os.path.join(HERE, "libvr.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["vr_api.cu", "tables.cu", "sort.cu", "hotpath.cu", "sparse.cu", "hypha.cu", "hypha_host.cpp", "netsimplex.cpp", "w1.cu", "host.cpp"]
-HEADERS = ["vr_common.cuh", "vr_internal.h"]
+HEADERS = ["vr_common.cuh", "vr_internal.h", "vr_types.h"]
 
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -38,7 +38,7 @@ namespace vr {
 
 constexpr int SP_THREADS = 256;
 constexpr int SP_WARPS = SP_THREADS / 32;
-constexpr int SP_LCAP = 128;  // C(σ) entries listed per warp at a time (longer lists: segments)
+constexpr int SP_LCAP = 256;  // C(σ) entries listed per warp at a time (longer lists: segments)
 
 // ------------------------------------------------------------------ threshold-graph bitmap
 // one warp per vertex v: word k of row v from the 32 coalesced ranks R[v][32k .. 32k+31];
@@ -71,40 +71,39 @@ __global__ void k_bitmap(const uint32_t* __restrict__ rank, int n, int nw, uint3
   }
 }
 
-// sum over rows of deg_below(u_1): a bound on the d-simplices the rows can produce
-__global__ void k_row_bound(const uint4* __restrict__ rows, uint64_t nrows, int dprev, const uint32_t* __restrict__ deg_below,
-                            unsigned long long* __restrict__ out) {
-  unsigned long long acc = 0;
-  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (uint64_t)gridDim.x * blockDim.x) {
-    const uint4 p = rows[r];
-    const uint32_t w[4] = {p.x, p.y, p.z, p.w};
-    const int u1 = (int)((w[dprev >> 1] >> ((dprev & 1) * 16)) & 0xFFFFu);  // smallest vertex s[dprev]
-    acc += deg_below[u1];
-  }
-  acc = __reduce_add_sync(0xffffffffu, (unsigned)acc);  // per-warp partial fits 32 bits
-  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
-}
-
 // ------------------------------------------------------------------ bitmap lists
-// The set bits of AND_{i<K} bm[x_i] (words k <= word, descending vertex order, the top word
-// masked by top_mask) appended to list[0..cap): 32 words per round, one per lane (lane l
-// takes word `word - l`), a warp prefix sum of the popcounts places each lane's bits.  Stops
-// before the first word that does not fit.  Returns the entries written; *word = the next
-// word to list (-1 when done), *top_mask = the mask for that word (all ones).
+// The set bits of AND_{i<K} bm[x_i] over the words k <= *word, in descending vertex order,
+// appended to list[0..cap) (the word *word itself masked by *top_mask).  Rows are padded to
+// a multiple of 4 words, so a round reads one 16-byte quad of words per lane and row
+// (lane l takes quad `(*word >> 2) - l`: 128 words = 4096 vertices per round, coalesced),
+// and a warp prefix sum of the popcounts places each lane's bits.  Stops before the first
+// quad that does not fit (cap >= 128 keeps one quad always fitting).  Returns the entries
+// written; *word = the next word to list (-1 when done), *top_mask = its mask (all ones).
+// *above (if given) counts the entries >= `split` (the survivors are the entries < split).
 template <int K>
 __device__ __forceinline__ int bm_list(const SparseRows& S, const int (&x)[K], int& word, uint32_t& top_mask,
-                                       uint16_t* __restrict__ list, int cap) {
+                                       uint16_t* __restrict__ list, int cap, int split, int* above) {
   const int lane = threadIdx.x & 31;
-  int fill = 0;
+  int fill = 0, nab = 0;
   while (word >= 0) {
-    const int k = word - lane;
-    uint32_t bits = 0;
-    if (k >= 0) {
-      bits = lane == 0 ? top_mask : 0xffffffffu;
+    const int q = (word >> 2) - lane;
+    uint32_t wv[4] = {0, 0, 0, 0};  // words 4q .. 4q+3
+    if (q >= 0) {
+      wv[0] = wv[1] = wv[2] = wv[3] = 0xffffffffu;
 #pragma unroll
-      for (int i = 0; i < K; ++i) bits &= __ldg(S.bm + (size_t)x[i] * (size_t)S.nw + (size_t)k);
+      for (int i = 0; i < K; ++i) {
+        const uint4 t = __ldg(reinterpret_cast<const uint4*>(S.bm + (size_t)x[i] * (size_t)S.nw) + q);
+        wv[0] &= t.x; wv[1] &= t.y; wv[2] &= t.z; wv[3] &= t.w;
+      }
+      if (lane == 0) {  // the first quad: drop the words above `word`, mask `word`
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = 4 * q + j;
+          wv[j] = k > word ? 0u : (k == word ? (wv[j] & top_mask) : wv[j]);
+        }
+      }
     }
-    const int c = __popc(bits);
+    const int c = __popc(wv[0]) + __popc(wv[1]) + __popc(wv[2]) + __popc(wv[3]);
     int incl = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -112,224 +111,495 @@ __device__ __forceinline__ int bm_list(const SparseRows& S, const int (&x)[K], i
       if (lane >= o) incl += y;
     }
     const bool fits = fill + incl <= cap;  // monotone in the lane: a prefix of the lanes fits
-    const uint32_t fm = __ballot_sync(0xffffffffu, fits);
-    const int nfit = __popc(fm);
-    if (fits) {
+    const int nfit = __popc(__ballot_sync(0xffffffffu, fits));
+    int ab = 0;
+    if (fits && c) {
       int pos = fill + incl - c;
-      while (bits) {
-        const int b = 31 - __clz(bits);
-        list[pos++] = (uint16_t)(32 * k + b);
-        bits &= ~(1u << b);
+#pragma unroll
+      for (int j = 3; j >= 0; --j) {
+        uint32_t bits = wv[j];
+        const int base = 32 * (4 * q + j);
+        if (above) {
+          const int r = split - base;  // bits >= r are >= split
+          ab += r <= 0 ? __popc(bits) : (r >= 32 ? 0 : __popc(bits >> r));
+        }
+        while (bits) {
+          const int b = 31 - __clz(bits);
+          list[pos++] = (uint16_t)(base + b);
+          bits &= ~(1u << b);
+        }
       }
     }
+    if (above) nab += __reduce_add_sync(0xffffffffu, (unsigned)ab);
     const int added = nfit ? __shfl_sync(0xffffffffu, incl, nfit - 1) : 0;
     fill += added;
-    word -= nfit;
-    top_mask = nfit ? 0xffffffffu : top_mask;
+    if (nfit) {
+      word = 4 * ((word >> 2) - nfit) + 3;  // the top word of the first quad left (< 0: done)
+      top_mask = 0xffffffffu;
+    }
     if (nfit < 32) break;
   }
   __syncwarp();
+  if (above) *above = nab;
   return fill;
 }
 
 // ------------------------------------------------------------------ phase 1 (+ decision)
+struct Acc {
+  unsigned long long surv = 0, app = 0, scan = 0, clr = 0, next_bound = 0;
+};
+
+// Lemma 5.3.6 condition 1 over one list segment: the first v of cv[0..fill) (descending)
+// with v != w and max(m(v), R[w][v]) <= rs; all lanes step together (broadcast shared
+// loads), a rank is gathered only where m(v) <= rs.  Clears `active` on a hit.
+__device__ __forceinline__ int scan_list(const Tables& T, const uint16_t* cv, const uint32_t* cm, int fill, int w,
+                                         uint32_t rs, bool& active, int& examined) {
+  int hitv = -1;
+  for (int k = 0; k < fill; k += 2) {
+    {
+      const int v = cv[k];
+      const uint32_t m = cm[k];
+      examined += active;
+      if (active && v != w && m <= rs && rank_at(T, w, v) <= rs) {
+        hitv = v;
+        active = false;
+      }
+    }
+    if (k + 1 < fill) {
+      const int v = cv[k + 1];
+      const uint32_t m = cm[k + 1];
+      examined += active;
+      if (active && v != w && m <= rs && rank_at(T, w, v) <= rs) {
+        hitv = v;
+        active = false;
+      }
+    }
+    if (!__any_sync(0xffffffffu, active)) break;
+  }
+  return hitv;
+}
+
+// Entry of a batch of survivors s = σ ∪ {w} (one per valid lane): the survivor count, the
+// row of a later dimension (rows_out), the next dimension's bound term deg_below(w), and the
+// clearing test (the dimension-(d-1) pivots, Lemma 4.2.3).  Returns `cleared`.
+template <int D>
+__device__ __forceinline__ bool survivor_head(const HotBuffers& B, const SparseRows& S, const int (&s)[D + 1], bool valid,
+                                              int nb, uint64_t cidx, Acc& acc) {
+  acc.surv += (unsigned long long)nb;
+  if (S.rows_out) {
+    const unsigned long long slot = warp_append(valid, S.rows_out_count);
+    if (valid && slot < S.rows_out_cap) S.rows_out[slot] = pack_vertices<D>(s);
+  }
+  if (valid) acc.next_bound += __ldg(S.deg_below + s[D]);
+  bool cleared = false;
+  if (valid) {
+    if (B.clr) cleared = bit_test(B.clr, cidx);
+    else if (B.clr_set.table) cleared = set_has(B.clr_set, cidx);
+  }
+  acc.clr += __popc(__ballot_sync(0xffffffffu, cleared));
+  return cleared;
+}
+
+// Exit of a batch: Lemma 5.3.6 condition 2 for the lanes with a hit (no facet of
+// t = s ∪ {hitv} lex-smaller than s — one without a vertex x > hitv — has diam(t) = diam(s)),
+// then the outputs: apparent -> counted + its cofacet into the next dimension's clearing
+// set; non-apparent -> residual list (or the recompute queue).
+template <int D>
+__device__ __forceinline__ void survivor_tail(const Tables& T, const DimParams& p, const HotBuffers& B, const int (&u)[D + 1],
+                                              uint32_t pm_up, const uint32_t (&pm_ex)[D + 1], const int (&s)[D + 1], int w,
+                                              uint32_t rs, uint64_t cidx, bool valid, bool cleared, int hitv, int examined,
+                                              Acc& acc) {
+  acc.scan += (unsigned long long)__reduce_add_sync(0xffffffffu, (unsigned)examined);
+  bool app = false;
+  if (hitv >= 0) {
+    app = true;
+    uint32_t a[D + 1], b[D + 1];
+    uint32_t bup = 0;
+#pragma unroll
+    for (int i = 1; i <= D; ++i) {
+      a[i] = rank_at(T, u[i], w);
+      b[i] = rank_at(T, hitv, u[i]);
+      bup = umax(bup, b[i]);
+    }
+    const uint32_t b0 = rank_at(T, hitv, w);
+    if (w > hitv && umax(pm_up, bup) == rs) app = false;
+#pragma unroll
+    for (int j = 1; j <= D; ++j) {
+      if (u[j] > hitv) {
+        uint32_t m = umax(pm_ex[j], b0);
+#pragma unroll
+        for (int i = 1; i <= D; ++i)
+          if (i != j) m = umax(m, umax(a[i], b[i]));
+        if (m == rs) app = false;
+      }
+    }
+  }
+  acc.app += __popc(__ballot_sync(0xffffffffu, app));
+  if (app && (B.clr_next || B.clr_next_set.table || B.app_pairs)) {
+    const uint64_t tc = cofacet_cidx<D>(T, s, hitv);
+    if (B.clr_next) bit_set(B.clr_next, tc);
+    if (B.clr_next_set.table) set_put(B.clr_next_set, tc);
+    if (B.app_pairs) {
+      const unsigned long long slot = atomicAdd(&B.ctr->app_pairs, 1ull);
+      if (slot < B.app_cap) {
+        B.app_pairs[2 * slot] = cidx;
+        B.app_pairs[2 * slot + 1] = tc;
+      }
+    }
+  }
+  const bool clrmode = B.clr || B.clr_set.table;  // clearing decided here (else in k_resolve_sparse)
+  const bool nonapp = valid && !cleared && !app;
+  const bool to_resid = clrmode && nonapp;
+  const bool to_queue = !clrmode && nonapp;
+  const uint64_t key = ((uint64_t)(p.maxr - rs) << p.cbits) | cidx;
+  const unsigned long long rslot = warp_append(to_resid, &B.ctr->residual);
+  if (to_resid && rslot < B.rcap) B.resid[rslot] = key;
+  const unsigned long long qslot = warp_append(to_queue, &B.ctr->queued);
+  if (to_queue && qslot < B.qcap) {
+    B.qkey[qslot] = key;
+    B.qvert[qslot] = pack_vertices<D>(s);
+  }
+}
+
+// The survivors of a row σ = (u_D > ... > u_1) whose C(σ) list is complete in cv/cm (m(v) =
+// max_i R[u_i][v]): they are its tail cv[first_w..fill) (the entries < u_1), 32 per batch.
+template <int D>
+__device__ __forceinline__ void row_from_list(const Tables& T, const DimParams& p, const HotBuffers& B, const SparseRows& S,
+                                              const int (&u)[D + 1], uint32_t pm_up, const uint32_t (&pm_ex)[D + 1],
+                                              uint64_t cbase, const uint16_t* cv, const uint32_t* cm, int fill, int first_w,
+                                              Acc& acc) {
+  const int lane = threadIdx.x & 31;
+  for (int s0 = first_w; s0 < fill; s0 += 32) {
+    const int nb = fill - s0 < 32 ? fill - s0 : 32;
+    const bool valid = lane < nb;
+    const int w = valid ? (int)cv[s0 + lane] : 0;
+    const uint32_t rs = valid ? umax(pm_up, cm[s0 + lane]) : 0;
+    int s[D + 1];  // s[0] > ... > s[D] = w
+#pragma unroll
+    for (int i = 0; i < D; ++i) s[i] = u[D - i];
+    s[D] = w;
+    const uint64_t cidx = cbase + (uint64_t)w;
+    const bool cleared = survivor_head<D>(B, S, s, valid, nb, cidx, acc);
+    bool active = valid && !cleared;
+    int examined = 0;
+    const int hitv = __any_sync(0xffffffffu, active) ? scan_list(T, cv, cm, fill, w, rs, active, examined) : -1;
+    survivor_tail<D>(T, p, B, u, pm_up, pm_ex, s, w, rs, cidx, valid, cleared, hitv, examined, acc);
+  }
+}
+
+// prefix pair maxima of σ: pm_up over all pairs, pm_ex[j] over the pairs avoiding u_j
+template <int D>
+__device__ __forceinline__ void pair_maxima(const Tables& T, const int (&u)[D + 1], int from, uint32_t& pm_up,
+                                            uint32_t (&pm_ex)[D + 1]) {
+  pm_up = 0;
+#pragma unroll
+  for (int j = 0; j <= D; ++j) pm_ex[j] = 0;
+#pragma unroll
+  for (int a = 1; a <= D; ++a)
+#pragma unroll
+    for (int b = a + 1; b <= D; ++b) {
+      if (a < from) continue;
+      const uint32_t rr = rank_at(T, u[a], u[b]);
+      pm_up = umax(pm_up, rr);
+#pragma unroll
+      for (int j = 1; j <= D; ++j)
+        if (j != a && j != b) pm_ex[j] = umax(pm_ex[j], rr);
+    }
+}
+
+// m(v) = max_{i >= from} R[u_i][v] for the list entries, into cm
+template <int D>
+__device__ __forceinline__ void list_maxima(const Tables& T, const int (&u)[D + 1], int from, const uint16_t* cv,
+                                            uint32_t* cm, int fill) {
+  const int lane = threadIdx.x & 31;
+  for (int j = lane; j < fill; j += 32) {
+    const int v = cv[j];
+    uint32_t m = 0;
+#pragma unroll
+    for (int i = 1; i <= D; ++i)
+      if (i >= from) m = umax(m, rank_at(T, u[i], v));
+    cm[j] = m;
+  }
+  __syncwarp();
+}
+
+// One row σ = (u_D > ... > u_1), any list length: C(σ) in segments of SP_LCAP entries from
+// the top (the buffer keeps the segment it holds across survivor batches), the survivors
+// listed from the bitmap words below u_1 in batches.  Buffers: cv/cm (SP_LCAP), sw (128).
+template <int D>
+__device__ void row_general(const Tables& T, const DimParams& p, const HotBuffers& B, const SparseRows& S, const int (&u)[D + 1],
+                            uint16_t* cv, uint32_t* cm, uint16_t* sw, Acc& acc) {
+  const int lane = threadIdx.x & 31;
+  const int u1 = u[1];
+  if (u1 == 0) return;
+  int x[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) x[i] = u[i + 1];
+  uint32_t pm_up;
+  uint32_t pm_ex[D + 1];
+  pair_maxima<D>(T, u, 1, pm_up, pm_ex);
+  uint64_t cbase = 0;
+#pragma unroll
+  for (int i = 1; i <= D; ++i) cbase += binom(T, u[i], i + 1);
+  const int top_word = (T.n - 1) >> 5;
+  const uint32_t top_word_mask = (T.n & 31) ? ((1u << (T.n & 31)) - 1) : 0xffffffffu;
+  int c_word = top_word;
+  uint32_t c_mask = top_word_mask;
+  int nabove = 0;
+  int c_fill = bm_list<D>(S, x, c_word, c_mask, cv, SP_LCAP, u1, &nabove);
+  list_maxima<D>(T, u, 1, cv, cm, c_fill);
+  if (c_word < 0) {  // the whole list fits: the survivors are its tail
+    row_from_list<D>(T, p, B, S, u, pm_up, pm_ex, cbase, cv, cm, c_fill, nabove, acc);
+    return;
+  }
+  int c_seg = 0;  // the segment held in cv/cm; c_word / c_mask continue after it
+  int s_word = (u1 - 1) >> 5;
+  uint32_t s_mask = (u1 & 31) ? ((1u << (u1 & 31)) - 1) : 0xffffffffu;
+  int s_fill = 0, s_pos = 0;
+  while (true) {
+    if (s_pos == s_fill) {
+      if (s_word < 0) break;
+      s_fill = bm_list<D>(S, x, s_word, s_mask, sw, 128, 0, nullptr);
+      s_pos = 0;
+      if (s_fill == 0) break;
+    }
+    const int nb = s_fill - s_pos < 32 ? s_fill - s_pos : 32;
+    const bool valid = lane < nb;
+    int w = 0;
+    uint32_t rs = 0;
+    if (valid) {
+      w = sw[s_pos + lane];
+      uint32_t m = 0;
+#pragma unroll
+      for (int i = 1; i <= D; ++i) m = umax(m, rank_at(T, u[i], w));
+      rs = umax(pm_up, m);
+    }
+    s_pos += nb;
+    int s[D + 1];
+#pragma unroll
+    for (int i = 0; i < D; ++i) s[i] = u[D - i];
+    s[D] = w;
+    const uint64_t cidx = cbase + (uint64_t)w;
+    const bool cleared = survivor_head<D>(B, S, s, valid, nb, cidx, acc);
+    bool active = valid && !cleared;
+    int hitv = -1, examined = 0;
+    int seg = 0;
+    while (__any_sync(0xffffffffu, active)) {
+      if (c_seg != seg) {  // (re)build segment `seg`
+        if (seg == 0) {
+          c_word = top_word;
+          c_mask = top_word_mask;
+        }
+        c_fill = bm_list<D>(S, x, c_word, c_mask, cv, SP_LCAP, 0, nullptr);
+        list_maxima<D>(T, u, 1, cv, cm, c_fill);
+        c_seg = seg;
+      }
+      const int h = scan_list(T, cv, cm, c_fill, w, rs, active, examined);
+      if (h >= 0) hitv = h;
+      if (c_word < 0) break;  // this was the last segment
+      ++seg;
+    }
+    survivor_tail<D>(T, p, B, u, pm_up, pm_ex, s, w, rs, cidx, valid, cleared, hitv, examined, acc);
+  }
+}
+
+// rows handed out by a shared counter, `grab` per atomic; the shard's rows are every
+// shard_world-th row
+__device__ __forceinline__ bool next_rows(const DimParams& p, const HotBuffers& B, uint64_t nrows, uint64_t& g0,
+                                          uint64_t& gend) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long g = 0;
+  if (lane == 0) g = atomicAdd(&B.ctr->row_next, (unsigned long long)p.grab);
+  g = __shfl_sync(0xffffffffu, g, 0);
+  if (g >= nrows) return false;
+  g0 = g;
+  gend = g + (uint64_t)p.grab < nrows ? g + (uint64_t)p.grab : nrows;
+  return true;
+}
+
+template <int K>
+__device__ __forceinline__ void unpack_row(const uint4* rows, uint64_t r, int (&t)[K]) {
+  const uint4 pk = rows[r];
+  const uint32_t w4[4] = {pk.x, pk.y, pk.z, pk.w};
+#pragma unroll
+  for (int i = 0; i < K; ++i) t[i] = (int)((w4[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu);
+}
+
+__device__ __forceinline__ void flush_acc(const HotBuffers& B, Acc& acc) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    if (acc.surv) atomicAdd(&B.ctr->survivors, acc.surv);
+    if (acc.app) atomicAdd(&B.ctr->apparent1, acc.app);
+    if (acc.scan) atomicAdd(&B.ctr->scanned, acc.scan);
+    if (acc.clr) atomicAdd(&B.ctr->cleared, acc.clr);
+  }
+  unsigned long long nbsum = acc.next_bound;  // per lane
+#pragma unroll
+  for (int o = 16; o; o >>= 1) nbsum += __shfl_xor_sync(0xffffffffu, nbsum, o);
+  if (lane == 0 && nbsum) atomicAdd(&B.ctr->next_bound, nbsum);
+}
+
+// Single level: a row is a (D-1)-simplex σ (a survivor of dimension D-1; the vertices for
+// D = 1), extended by w ∈ C(σ), w < u_1.
 template <int D>
 __global__ void __launch_bounds__(SP_THREADS, 4) k_enum_sparse(Tables T, DimParams p, HotBuffers B, SparseRows S) {
-  __shared__ uint16_t s_cv[SP_WARPS][SP_LCAP];  // C(σ), descending (one segment)
-  __shared__ uint32_t s_cm[SP_WARPS][SP_LCAP];  // m(v) = max_i R[u_i][v]
-  __shared__ uint16_t s_w[SP_WARPS][32];        // a batch of survivors w < u_1
-  const int lane = threadIdx.x & 31;
+  __shared__ uint16_t s_cv[SP_WARPS][SP_LCAP];
+  __shared__ uint32_t s_cm[SP_WARPS][SP_LCAP];
+  __shared__ uint16_t s_w[SP_WARPS][128];
   const int wi = threadIdx.x >> 5;
-  uint16_t* cv = s_cv[wi];
-  uint32_t* cm = s_cm[wi];
-  uint16_t* sw = s_w[wi];
-  unsigned long long surv_acc = 0, app_acc = 0, scan_acc = 0, clr_acc = 0;
-  const bool clrmode = B.clr || B.clr_hash;  // clearing decided here (else in k_resolve_sparse)
+  Acc acc;
   const uint64_t W = (uint64_t)p.shard_world;
   const uint64_t all = p.row_end - p.row_begin;
-  const uint64_t nrows = all > (uint64_t)p.shard_rank ? (all - (uint64_t)p.shard_rank + W - 1) / W : 0;  // this shard's rows
-  while (true) {
-    unsigned long long g = 0;
-    if (lane == 0) g = atomicAdd(&B.ctr->row_next, 1ull);
-    g = __shfl_sync(0xffffffffu, g, 0);
-    if (g >= nrows) break;
-    const uint64_t r = p.row_begin + g * W + (uint64_t)p.shard_rank;
-    int u[D + 1];  // u[1] < ... < u[D] (u[0] unused)
-    if (S.rows_in == nullptr) {  // dimension 1: the rows are the vertices
-      u[1] = (int)r;
-    } else {                    // the (D-1)-simplex t[0] > ... > t[D-1]: u_i = t[D-i]
-      int t[D];
-      const uint4 pk = S.rows_in[r];
-      const uint32_t w4[4] = {pk.x, pk.y, pk.z, pk.w};
+  const uint64_t nrows = all > (uint64_t)p.shard_rank ? (all - (uint64_t)p.shard_rank + W - 1) / W : 0;
+  uint64_t g0, gend;
+  while (next_rows(p, B, nrows, g0, gend)) {
+    for (uint64_t g = g0; g < gend; ++g) {
+      const uint64_t r = p.row_begin + g * W + (uint64_t)p.shard_rank;
+      int u[D + 1];  // u[1] < ... < u[D] (u[0] unused)
+      u[0] = 0;
+      if (S.rows_in == nullptr) {
+        u[1] = (int)r;
+      } else {
+        int t[D];
+        unpack_row<D>(S.rows_in, r, t);
 #pragma unroll
-      for (int i = 0; i < D; ++i) t[i] = (int)((w4[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu);
-#pragma unroll
-      for (int i = 1; i <= D; ++i) u[i] = t[D - i];
+        for (int i = 1; i <= D; ++i) u[i] = t[D - i];
+      }
+      row_general<D>(T, p, B, S, u, s_cv[wi], s_cm[wi], s_w[wi], acc);
     }
-    u[0] = 0;
-    const int u1 = u[1];
-    if (u1 == 0) continue;
-    int x[D];  // the row's vertices (bitmap rows to AND)
+  }
+  flush_acc(B, acc);
+}
+
+// Two levels (D >= 2): a row is a (D-2)-simplex τ = (u_D > ... > u_2) (a survivor of
+// dimension D-2; the vertices for D = 2).  C(τ) is listed once, with m_τ(v) = max_{i>=2}
+// R[u_i][v]; each x ∈ C(τ), x < u_2 — a (D-1)-simplex σ = τ ∪ {x} — then gets its own
+// C(σ) = { v ∈ C(τ) : R[x][v] != RINF } with m_σ(v) = max(m_τ(v), R[x][v]): ONE rank gather
+// per list entry instead of the AND of D bitmap rows and D gathers.  τ lists longer than
+// SP_LCAP fall back to row_general per σ.
+template <int D>
+__global__ void __launch_bounds__(SP_THREADS, 4) k_enum_sparse2(Tables T, DimParams p, HotBuffers B, SparseRows S) {
+  __shared__ uint16_t s_tv[SP_WARPS][SP_LCAP];  // C(τ)
+  __shared__ uint32_t s_tm[SP_WARPS][SP_LCAP];  // m_τ
+  __shared__ uint16_t s_cv[SP_WARPS][SP_LCAP];  // C(σ)
+  __shared__ uint32_t s_cm[SP_WARPS][SP_LCAP];  // m_σ
+  __shared__ uint16_t s_w[SP_WARPS][128];
+  const int lane = threadIdx.x & 31;
+  const int wi = threadIdx.x >> 5;
+  uint16_t* tv = s_tv[wi];
+  uint32_t* tm = s_tm[wi];
+  uint16_t* cv = s_cv[wi];
+  uint32_t* cm = s_cm[wi];
+  Acc acc;
+  const uint64_t W = (uint64_t)p.shard_world;
+  const uint64_t all = p.row_end - p.row_begin;
+  const uint64_t nrows = all > (uint64_t)p.shard_rank ? (all - (uint64_t)p.shard_rank + W - 1) / W : 0;
+  const int top_word = (T.n - 1) >> 5;
+  const uint32_t top_word_mask = (T.n & 31) ? ((1u << (T.n & 31)) - 1) : 0xffffffffu;
+  // work item g = (row g / slices, slice g % slices): slice k takes every slices-th x
+  // (few rows with long lists, e.g. D = 2 with vertex rows, are split over warps)
+  const uint64_t NS = (uint64_t)p.slices;
+  uint64_t g0, gend;
+  while (next_rows(p, B, nrows * NS, g0, gend)) {
+    for (uint64_t gi = g0; gi < gend; ++gi) {
+      const uint64_t g = gi / NS;
+      const int slice = (int)(gi - g * NS);
+      const uint64_t r = p.row_begin + g * W + (uint64_t)p.shard_rank;
+      int u[D + 1];
+      u[0] = u[1] = 0;
+      if (S.rows_in == nullptr) {  // D = 2: τ is a vertex
+        u[2] = (int)r;
+      } else {
+        int t[D - 1];
+        unpack_row<D - 1>(S.rows_in, r, t);
 #pragma unroll
-    for (int i = 0; i < D; ++i) x[i] = u[i + 1];
-    // prefix pair maxima: pm_up over all pairs of σ, pm_ex[j] over the pairs avoiding u_j
-    uint32_t pm_up = 0;
-    uint32_t pm_ex[D + 1];
-#pragma unroll
-    for (int j = 0; j <= D; ++j) pm_ex[j] = 0;
-#pragma unroll
-    for (int a = 1; a <= D; ++a)
-#pragma unroll
-      for (int b = a + 1; b <= D; ++b) {
-        const uint32_t rr = rank_at(T, u[a], u[b]);
-        pm_up = umax(pm_up, rr);
-#pragma unroll
-        for (int j = 1; j <= D; ++j)
-          if (j != a && j != b) pm_ex[j] = umax(pm_ex[j], rr);
+        for (int i = 2; i <= D; ++i) u[i] = t[D - i];
       }
-    uint64_t cbase = 0;
+      const int u2 = u[2];
+      if (u2 < 2) continue;  // no x < u_2 with a w < x
+      int xt[D - 1];
 #pragma unroll
-    for (int i = 1; i <= D; ++i) cbase += binom(T, u[i], i + 1);
-    // C(σ) in segments of SP_LCAP entries from the top; the buffer keeps the segment it
-    // holds (c_seg) across survivor batches, and c_word / c_mask continue after it
-    int c_word = 0, c_fill = 0, c_seg = -1;
-    uint32_t c_mask = 0;
-    // survivors w < u_1 in batches of 32
-    int s_word = (u1 - 1) >> 5;
-    uint32_t s_mask = (u1 & 31) ? ((1u << (u1 & 31)) - 1) : 0xffffffffu;
-    while (s_word >= 0) {
-      const int nb = bm_list<D>(S, x, s_word, s_mask, sw, 32);
-      if (nb == 0) break;
-      const bool valid = lane < nb;
-      const int w = valid ? (int)sw[lane] : 0;
-      uint32_t a[D + 1];
-      uint32_t rs = pm_up;
-#pragma unroll
-      for (int i = 1; i <= D; ++i) {
-        a[i] = valid ? rank_at(T, u[i], w) : 0;
-        rs = umax(rs, a[i]);
-      }
-      surv_acc += (unsigned long long)nb;
-      int s[D + 1];  // s[0] > ... > s[D] = w
-#pragma unroll
-      for (int i = 0; i < D; ++i) s[i] = u[D - i];
-      s[D] = w;
-      if (S.rows_out) {  // every survivor is a prefix row of dimension d+1
-        const unsigned long long slot = warp_append(valid, S.rows_out_count);
-        if (valid && slot < S.rows_out_cap) S.rows_out[slot] = pack_vertices<D>(s);
-      }
-      const uint64_t cidx = cbase + (uint64_t)w;
-      bool cleared = false;
-      if (valid) {
-        if (B.clr) cleared = bit_test(B.clr, cidx);
-        else if (B.clr_hash) cleared = hash_has(B.clr_hash, B.clr_hash_mask, cidx);
-      }
-      clr_acc += __popc(__ballot_sync(0xffffffffu, cleared));
-      bool active = valid && !cleared;
-      int hitv = -1, examined = 0;
-      // Lemma 5.3.6 condition 1: the first v of C(σ) (descending) with v != w and
-      // max(m(v), R[w][v]) <= diam(s)
-      int seg = 0;
-      while (__any_sync(0xffffffffu, active)) {
-        if (c_seg != seg) {  // (re)build segment `seg` of C(σ)
-          if (seg == 0) {
-            c_word = S.nw - 1;
-            c_mask = (T.n & 31) ? ((1u << (T.n & 31)) - 1) : 0xffffffffu;
+      for (int i = 0; i < D - 1; ++i) xt[i] = u[i + 2];
+      int word = top_word;
+      uint32_t mask = top_word_mask;
+      int nab = 0;
+      const int tfill = bm_list<D - 1>(S, xt, word, mask, tv, SP_LCAP, u2, &nab);
+      if (word >= 0) {  // C(τ) longer than the list: every σ on the general path
+        int s_word = (u2 - 1) >> 5;
+        uint32_t s_mask = (u2 & 31) ? ((1u << (u2 & 31)) - 1) : 0xffffffffu;
+        int base = 0;  // list index of tv[0] among the x's
+        while (s_word >= 0) {
+          const int nx = bm_list<D - 1>(S, xt, s_word, s_mask, tv, SP_LCAP, 0, nullptr);
+          for (int ix = 0; ix < nx; ++ix) {
+            if ((base + ix) % (int)p.slices != slice) continue;
+            u[1] = tv[ix];
+            row_general<D>(T, p, B, S, u, cv, cm, s_w[wi], acc);
           }
-          c_fill = bm_list<D>(S, x, c_word, c_mask, cv, SP_LCAP);
-          for (int j = lane; j < c_fill; j += 32) {
-            const int v = cv[j];
-            uint32_t m = 0;
-#pragma unroll
-            for (int i = 1; i <= D; ++i) m = umax(m, rank_at(T, u[i], v));
-            cm[j] = m;
-          }
+          base += nx;
           __syncwarp();
-          c_seg = seg;
         }
-        for (int k = 0; k < c_fill; k += 2) {
-          {
-            const int v = cv[k];
-            const uint32_t m = cm[k];
-            examined += active;
-            if (active && v != w && m <= rs && rank_at(T, w, v) <= rs) {
-              hitv = v;
-              active = false;
-            }
-          }
-          if (k + 1 < c_fill) {
-            const int v = cv[k + 1];
-            const uint32_t m = cm[k + 1];
-            examined += active;
-            if (active && v != w && m <= rs && rank_at(T, w, v) <= rs) {
-              hitv = v;
-              active = false;
-            }
-          }
-          if (!__any_sync(0xffffffffu, active)) break;
-        }
-        if (c_word < 0) break;  // this was the last segment
-        ++seg;
+        continue;
       }
-      active = false;
-      scan_acc += (unsigned long long)__reduce_add_sync(0xffffffffu, (unsigned)examined);
-      // condition 2: no facet of t = s ∪ {hitv} lex-smaller than s (one without a vertex
-      // x > hitv) has diam(t) = diam(s)
-      bool app = false;
-      if (hitv >= 0) {
-        app = true;
-        uint32_t b[D + 1];
-        uint32_t bup = 0;
+      list_maxima<D>(T, u, 2, tv, tm, tfill);
+      // τ's pair maxima and cidx part
+      uint32_t pt_up;
+      uint32_t pt_ex[D + 1];
+      pair_maxima<D>(T, u, 2, pt_up, pt_ex);
+      uint64_t cb_t = 0;
 #pragma unroll
-        for (int i = 1; i <= D; ++i) {
-          b[i] = rank_at(T, hitv, u[i]);
-          bup = umax(bup, b[i]);
-        }
-        const uint32_t b0 = rank_at(T, hitv, w);
-        if (w > hitv && umax(pm_up, bup) == rs) app = false;
+      for (int i = 2; i <= D; ++i) cb_t += binom(T, u[i], i + 1);
+      for (int ix = nab + slice; ix < tfill; ix += (int)p.slices) {  // σ = τ ∪ {x}, x descending
+        const int x = tv[ix];
+        if (x == 0) continue;
+        u[1] = x;
+        // σ's pair maxima from τ's and the D-1 new edges (x, u_i)
+        uint32_t ax[D + 1];
+        uint32_t pm_up = pt_up;
 #pragma unroll
-        for (int j = 1; j <= D; ++j) {
-          if (u[j] > hitv) {
-            uint32_t m = umax(pm_ex[j], b0);
+        for (int i = 2; i <= D; ++i) {
+          ax[i] = rank_at(T, x, u[i]);
+          pm_up = umax(pm_up, ax[i]);
+        }
+        uint32_t pm_ex[D + 1];
+        pm_ex[0] = 0;
+        pm_ex[1] = pt_up;
 #pragma unroll
-            for (int i = 1; i <= D; ++i)
-              if (i != j) m = umax(m, umax(a[i], b[i]));
-            if (m == rs) app = false;
-          }
+        for (int j = 2; j <= D; ++j) {
+          uint32_t m = pt_ex[j];
+#pragma unroll
+          for (int i = 2; i <= D; ++i)
+            if (i != j) m = umax(m, ax[i]);
+          pm_ex[j] = m;
         }
-      }
-      app_acc += __popc(__ballot_sync(0xffffffffu, app));
-      if (app && (B.clr_next || B.clr_next_hash || B.app_pairs)) {
-        const uint64_t tc = cofacet_cidx<D>(T, s, hitv);
-        if (B.clr_next) bit_set(B.clr_next, tc);
-        if (B.clr_next_hash) hash_put(B.clr_next_hash, B.clr_next_hash_mask, tc);
-        if (B.app_pairs) {
-          const unsigned long long slot = atomicAdd(&B.ctr->app_pairs, 1ull);
-          if (slot < B.app_cap) {
-            B.app_pairs[2 * slot] = cidx;
-            B.app_pairs[2 * slot + 1] = tc;
+        // C(σ): the entries of C(τ) adjacent to x, order kept (ballot compaction)
+        int fill = 0, first_w = 0;
+        for (int j0 = 0; j0 < tfill; j0 += 32) {
+          const int j = j0 + lane;
+          int v = 0;
+          uint32_t rx = VR_RINF;
+          if (j < tfill) {
+            v = tv[j];
+            rx = rank_at(T, x, v);  // RINF: not adjacent (or v = x)
           }
+          const bool keep = rx != VR_RINF;
+          const uint32_t km = __ballot_sync(0xffffffffu, keep);
+          if (keep) {
+            const int pos = fill + __popc(km & lanemask_lt());
+            cv[pos] = (uint16_t)v;
+            cm[pos] = umax(tm[j], rx);
+          }
+          first_w += __popc(__ballot_sync(0xffffffffu, keep && v > x));
+          fill += __popc(km);
         }
+        __syncwarp();
+        const uint64_t cbase = cb_t + binom(T, x, 2);
+        row_from_list<D>(T, p, B, S, u, pm_up, pm_ex, cbase, cv, cm, fill, first_w, acc);
+        __syncwarp();
       }
-      const bool nonapp = valid && !cleared && !app;
-      const bool to_resid = clrmode && nonapp;
-      const bool to_queue = !clrmode && nonapp;  // clearing decided by k_resolve_sparse
-      const uint64_t key = ((uint64_t)(p.maxr - rs) << p.cbits) | cidx;
-      const unsigned long long rslot = warp_append(to_resid, &B.ctr->residual);
-      if (to_resid && rslot < B.rcap) B.resid[rslot] = key;
-      const unsigned long long qslot = warp_append(to_queue, &B.ctr->queued);
-      if (to_queue && qslot < B.qcap) {
-        B.qkey[qslot] = key;
-        B.qvert[qslot] = pack_vertices<D>(s);
-      }
+      __syncwarp();
     }
   }
-  if (lane == 0) {
-    if (surv_acc) atomicAdd(&B.ctr->survivors, surv_acc);
-    if (app_acc) atomicAdd(&B.ctr->apparent1, app_acc);
-    if (scan_acc) atomicAdd(&B.ctr->scanned, scan_acc);
-    if (clr_acc) atomicAdd(&B.ctr->cleared, clr_acc);
-  }
+  flush_acc(B, acc);
 }
 
 // ------------------------------------------------------------------ phase 2 (recompute mode)
@@ -430,9 +700,9 @@ __global__ void __launch_bounds__(SP_THREADS) k_resolve_sparse(Tables T, DimPara
   }
 }
 
-__global__ void k_hash_put(const uint64_t* __restrict__ list, int64_t m, uint64_t* __restrict__ t, uint64_t mask) {
+__global__ void k_set_put(const uint64_t* __restrict__ list, int64_t m, ClearSet c) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-    hash_put(t, mask, __ldg(list + i));
+    set_put(c, __ldg(list + i));
 }
 
 // ------------------------------------------------------------------ launchers
@@ -443,30 +713,39 @@ static int sp_sms() {
   return s > 0 ? s : 148;
 }
 
-void launch_threshold_bitmap(const uint32_t* rank, int n, uint32_t* bm, uint32_t* deg, uint32_t* deg_below, cudaStream_t st,
-                             int64_t* launches) {
-  const int nw = (n + 31) / 32;
+void launch_threshold_bitmap(const uint32_t* rank, int n, int nw, uint32_t* bm, uint32_t* deg, uint32_t* deg_below,
+                             cudaStream_t st, int64_t* launches) {
   const unsigned blocks = (unsigned)(((uint64_t)n * 32 + SP_THREADS - 1) / SP_THREADS);
   k_bitmap<<<blocks, SP_THREADS, 0, st>>>(rank, n, nw, bm, deg, deg_below);
   *launches += 1;
 }
 
-void launch_row_bound(const uint4* rows, uint64_t nrows, int dprev, const uint32_t* deg_below, unsigned long long* out,
-                      cudaStream_t st, int64_t* launches) {
-  if (!nrows) return;
-  const uint64_t blocks = std::min<uint64_t>((nrows + 255) / 256, (uint64_t)sp_sms() * 8);
-  k_row_bound<<<(unsigned)blocks, 256, 0, st>>>(rows, nrows, dprev, deg_below, out);
-  *launches += 1;
-}
-
 template <int D>
-static void enum_sparse_d(const DimParams& p, const Tables& T, const HotBuffers& B, const SparseRows& S, cudaStream_t st) {
+static void enum_sparse_d(const DimParams& p, const Tables& T, const HotBuffers& B, const SparseRows& S, bool two,
+                          cudaStream_t st) {
   const uint64_t rows = p.row_end - p.row_begin;
+  const uint64_t cap = (uint64_t)sp_sms() * 4;  // 4 CTAs of 8 warps per SM
   uint64_t blocks = (rows * 32 + SP_THREADS - 1) / SP_THREADS;
-  const uint64_t cap = (uint64_t)sp_sms() * 4;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  k_enum_sparse<D><<<(unsigned)blocks, SP_THREADS, 0, st>>>(T, p, B, S);
+  DimParams q = p;
+  // rows per atomic grab: 4 when every warp gets dozens of rows (one shared counter), else 1
+  q.grab = rows >= cap * SP_WARPS * 64 ? 4 : 1;
+  if constexpr (D >= 2) {
+    if (two) {
+      // slices per row so that there are >= 8 work items per resident warp
+      const uint64_t slots = cap * SP_WARPS;
+      uint64_t sl = rows ? (8 * slots + rows - 1) / rows : 1;
+      q.slices = (int)(sl < 1 ? 1 : (sl > 16 ? 16 : sl));
+      blocks = (rows * (uint64_t)q.slices * 32 + SP_THREADS - 1) / SP_THREADS;
+      if (blocks > cap) blocks = cap;
+      if (blocks < 1) blocks = 1;
+      q.grab = rows * (uint64_t)q.slices >= cap * SP_WARPS * 64 ? 4 : 1;
+      k_enum_sparse2<D><<<(unsigned)blocks, SP_THREADS, 0, st>>>(T, q, B, S);
+      return;
+    }
+  }
+  k_enum_sparse<D><<<(unsigned)blocks, SP_THREADS, 0, st>>>(T, q, B, S);
 }
 
 template <int D>
@@ -480,15 +759,15 @@ static void resolve_sparse_d(const DimParams& p, const Tables& T, const HotBuffe
 }
 
 void launch_enumerate_sparse(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
-                             const SparseRows& S, cudaStream_t st, int64_t* launches) {
+                             const SparseRows& S, bool two_level, cudaStream_t st, int64_t* launches) {
   Tables T{rank, binom, (int32_t)p.n, kmax};
   switch (p.d) {
-    case 1: enum_sparse_d<1>(p, T, B, S, st); break;
-    case 2: enum_sparse_d<2>(p, T, B, S, st); break;
-    case 3: enum_sparse_d<3>(p, T, B, S, st); break;
-    case 4: enum_sparse_d<4>(p, T, B, S, st); break;
-    case 5: enum_sparse_d<5>(p, T, B, S, st); break;
-    case 6: enum_sparse_d<6>(p, T, B, S, st); break;
+    case 1: enum_sparse_d<1>(p, T, B, S, false, st); break;
+    case 2: enum_sparse_d<2>(p, T, B, S, two_level, st); break;
+    case 3: enum_sparse_d<3>(p, T, B, S, two_level, st); break;
+    case 4: enum_sparse_d<4>(p, T, B, S, two_level, st); break;
+    case 5: enum_sparse_d<5>(p, T, B, S, two_level, st); break;
+    case 6: enum_sparse_d<6>(p, T, B, S, two_level, st); break;
     default: return;
   }
   *launches += 1;
@@ -510,10 +789,10 @@ void launch_resolve_sparse(const DimParams& p, const uint32_t* rank, const uint6
   *launches += 1;
 }
 
-void launch_hash_put(const uint64_t* list, int64_t m, uint64_t* table, uint64_t mask, cudaStream_t st, int64_t* launches) {
-  if (m <= 0) return;
+void launch_set_put(const uint64_t* list, int64_t m, const ClearSet& c, cudaStream_t st, int64_t* launches) {
+  if (m <= 0 || !c.table) return;
   const int64_t blocks = std::min<int64_t>((m + 255) / 256, (int64_t)sp_sms() * 8);
-  k_hash_put<<<(unsigned)blocks, 256, 0, st>>>(list, m, table, mask);
+  k_set_put<<<(unsigned)blocks, 256, 0, st>>>(list, m, c);
   if (launches) *launches += 1;
 }
 

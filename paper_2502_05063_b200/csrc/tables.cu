@@ -1,14 +1,18 @@
 // tables.cu — step a0: the device tables every later kernel reads.
 //
-//   1. tb_edge_keys : validate the fp32 lower-distance input (VR_EINPUT on NaN / negative)
-//                     and write one 64-bit key per edge, (fp32 bits << kbits) | (N-1-k),
-//                     k = lower-distance index = edge cidx (Eq 5.6: C(i,2) + j).
-//   2. tb_rowmax    : row maxima of the symmetric matrix (enclosing radius, §5.2.12).
-//   3. radix sort of the edge keys — ascending = diameter ascending, cidx DEscending:
-//                     exactly the §5.1.4 filtration order of the edges (dimension 0 walks
-//                     it for union-find) and the sorted distance list the ranks index.
-//   4. tb_finalize  : R = min_i rowmax_i, t = threshold or R when threshold is
-//                     +inf (Prop 5.2.13), m = #edges with d <= t (inclusive, Eq 5.3).
+//   1. tb_rowmax    : row maxima of the symmetric matrix (enclosing radius, §5.2.12).
+//   2. tb_threshold : R = min_i rowmax_i, t = threshold or R when threshold is
+//                     +inf (Prop 5.2.13).
+//   3. tb_edge_count / scan / tb_edge_compact : validate the fp32 lower-distance input
+//                     (VR_EINPUT on NaN / negative) and write one 64-bit key per edge with
+//                     d <= t (inclusive, Eq 5.3), (fp32 bits << kbits) | (N-1-k), k = lower-
+//                     distance index = edge cidx (Eq 5.6: C(i,2) + j), in DEscending k order; m = their
+//                     number.  (A sparse threshold keeps few edges: config 5 sorts 234K keys
+//                     instead of 8.4M.)
+//   4. radix sort of the m keys on the 31 distance bits (stable) — ascending = diameter
+//                     ascending, cidx DEscending: exactly the §5.1.4 filtration order of the
+//                     edges (dimension 0 walks it for union-find) and the sorted distance
+//                     list the ranks index.
 //   5. tb_rank      : rank[i][j] = index of the first sorted edge with the value d(i,j)
 //                     (a lower_bound), or RINF when d(i,j) > t or i = j.  Equal distances get equal
 //                     ranks and the order is kept, so rank comparisons are the paper's
@@ -32,17 +36,6 @@ __device__ __forceinline__ uint32_t dist_bits(float x) {
   return x == 0.0f ? 0u : __float_as_uint(x);
 }
 
-__global__ void tb_edge_keys(const float* __restrict__ lt, uint64_t N, int kbits, uint64_t* __restrict__ keys,
-                             TablesOut* __restrict__ out) {
-  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += (uint64_t)gridDim.x * blockDim.x) {
-    float x = __ldg(lt + k);
-    if (!(x >= 0.0f)) atomicOr(&out->err, 1u);  // NaN or negative
-    // stored at N-1-k: the array is then ordered by ~cidx, and a STABLE sort on the 31
-    // distance bits alone yields (distance, ~cidx) order — 4 radix passes instead of 6
-    keys[N - 1 - k] = ((uint64_t)dist_bits(x) << kbits) | (N - 1 - k);
-  }
-}
-
 __global__ void tb_rowmax(const float* __restrict__ lt, int64_t n, uint32_t* __restrict__ rowmax) {
   __shared__ uint32_t red[32];
   const int64_t i = blockIdx.x;
@@ -62,8 +55,7 @@ __global__ void tb_rowmax(const float* __restrict__ lt, int64_t n, uint32_t* __r
   }
 }
 
-__global__ void tb_finalize(const uint32_t* __restrict__ rowmax, int64_t n, float threshold, const uint64_t* __restrict__ sorted,
-                            uint64_t N, int kbits, TablesOut* __restrict__ out) {
+__global__ void tb_threshold(const uint32_t* __restrict__ rowmax, int64_t n, float threshold, TablesOut* __restrict__ out) {
   __shared__ uint32_t red[32];
   uint32_t m = 0xFFFFFFFFu;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = rowmax[i] < m ? rowmax[i] : m;
@@ -78,15 +70,66 @@ __global__ void tb_finalize(const uint32_t* __restrict__ rowmax, int64_t n, floa
     // +inf entries are absent edges (a sparse input): never in the complex.  With such
     // entries R is +inf as well, and then every finite edge is kept (no enclosing-radius cut)
     const uint32_t tb0 = isinf(threshold) ? R : dist_bits(threshold);
-    const uint32_t tb = tb0 < 0x7F800000u ? tb0 : 0x7F7FFFFFu;
-    // m = number of sorted keys whose fp32 bits are <= tb (upper bound)
-    uint64_t lo = 0, hi = N;
-    while (lo < hi) {
-      uint64_t mid = (lo + hi) >> 1;
-      if ((sorted[mid] >> kbits) <= (uint64_t)tb) lo = mid + 1; else hi = mid;
+    out->tbits = tb0 < 0x7F800000u ? tb0 : 0x7F7FFFFFu;
+  }
+}
+
+// edges in DEscending index order k = N-1-j, j = TB_TILE * block + ...: a block counts the
+// edges with d <= t of its tile (and validates the input)
+constexpr int TB_THREADS = 256;
+constexpr int TB_TILE = 2048;
+__global__ void tb_edge_count(const float* __restrict__ lt, uint64_t N, TablesOut* __restrict__ out,
+                              uint32_t* __restrict__ blk_count) {
+  __shared__ uint32_t red[TB_THREADS / 32];
+  const uint32_t tb = out->tbits;
+  const uint64_t j0 = (uint64_t)blockIdx.x * TB_TILE;
+  uint32_t c = 0;
+  for (int i = threadIdx.x; i < TB_TILE; i += TB_THREADS) {
+    const uint64_t j = j0 + (uint64_t)i;
+    if (j >= N) break;
+    const float x = __ldg(lt + (N - 1 - j));
+    if (!(x >= 0.0f)) atomicOr(&out->err, 1u);  // NaN or negative
+    c += dist_bits(x) <= tb;
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < TB_THREADS / 32; ++w) t += red[w];
+    blk_count[blockIdx.x] = t;
+  }
+}
+
+// the keys of the edges with d <= t, order kept (descending k), at the block's offset
+__global__ void tb_edge_compact(const float* __restrict__ lt, uint64_t N, int kbits, TablesOut* __restrict__ out,
+                                const uint32_t* __restrict__ blk_off, uint32_t nblk, uint64_t* __restrict__ keys) {
+  __shared__ uint32_t wsum[TB_THREADS / 32];
+  const uint32_t tb = out->tbits;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t j0 = (uint64_t)blockIdx.x * TB_TILE;
+  uint32_t base = blk_off[blockIdx.x];
+  if (blockIdx.x == 0 && threadIdx.x == 0) out->m_le_t = blk_off[nblk];
+  for (int i0 = 0; i0 < TB_TILE; i0 += TB_THREADS) {
+    const uint64_t j = j0 + (uint64_t)(i0 + threadIdx.x);
+    uint32_t b = 0;
+    bool keep = false;
+    if (j < N) {
+      b = dist_bits(__ldg(lt + (N - 1 - j)));
+      keep = b <= tb;
     }
-    out->tbits = tb;
-    out->m_le_t = lo;
+    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wsum[wid] = __popc(bal);
+    __syncthreads();
+    uint32_t before = 0, total = 0;
+    for (int w = 0; w < TB_THREADS / 32; ++w) {
+      const uint32_t x = wsum[w];
+      before += w < wid ? x : 0;
+      total += x;
+    }
+    if (keep) keys[base + before + __popc(bal & lanemask_lt())] = ((uint64_t)b << kbits) | j;  // j = N-1-k
+    base += total;
+    __syncthreads();
   }
 }
 
@@ -147,24 +190,45 @@ static int bits_for(uint64_t x) {  // number of bits to represent values 0..x
   return b ? b : 1;
 }
 
+size_t tables_temp_bytes(int64_t n) {
+  const uint64_t N = (uint64_t)n * (uint64_t)(n - 1) / 2;
+  const size_t nblk = (size_t)((N + TB_TILE - 1) / TB_TILE);
+  return 2 * (((nblk + 1) * 4 + 255) / 256 * 256) + scan_temp_bytes(nblk + 1);
+}
+
 void launch_tables(const float* d_lt, int64_t n, float threshold, uint64_t* keys64, uint64_t* alt64, uint32_t* rowmax,
-                   void* sort_temp, uint32_t* rank, TablesOut* d_out, uint64_t** sorted_out, cudaStream_t st,
-                   int64_t* launches) {
+                   void* sort_temp, void* tb_temp, uint32_t* rank, TablesOut* d_out, int64_t m_known, uint64_t** sorted_out,
+                   cudaStream_t st, int64_t* launches) {
   const uint64_t N = (uint64_t)n * (uint64_t)(n - 1) / 2;
   const int kbits = bits_for(N ? N - 1 : 0);
   cudaMemsetAsync(d_out, 0, sizeof(TablesOut), st);
+  tb_rowmax<<<(unsigned)n, 256, 0, st>>>(d_lt, n, rowmax);
+  tb_threshold<<<1, 1024, 0, st>>>(rowmax, n, threshold, d_out);
+  *launches += 2;
   uint64_t* sorted = keys64;
   if (N) {
-    unsigned g = (unsigned)((N + 255) / 256 < 148u * 16u ? (N + 255) / 256 : 148u * 16u);
-    tb_edge_keys<<<g, 256, 0, st>>>(d_lt, N, kbits, keys64, d_out);
-    sorted = radix_sort_u64(keys64, alt64, N, kbits, 31 + kbits, sort_temp, st, launches);
-    *launches += 1;
+    const uint32_t nblk = (uint32_t)((N + TB_TILE - 1) / TB_TILE);
+    const size_t cb = (((size_t)nblk + 1) * 4 + 255) / 256 * 256;
+    uint32_t* blk_count = (uint32_t*)tb_temp;
+    uint32_t* blk_off = (uint32_t*)((char*)tb_temp + cb);
+    void* scan_tmp = (char*)tb_temp + 2 * cb;
+    cudaMemsetAsync(blk_count + nblk, 0, 4, st);
+    tb_edge_count<<<nblk, TB_THREADS, 0, st>>>(d_lt, N, d_out, blk_count);
+    exclusive_scan_u32(blk_count, blk_off, (size_t)nblk + 1, scan_tmp, st, launches);
+    tb_edge_compact<<<nblk, TB_THREADS, 0, st>>>(d_lt, N, kbits, d_out, blk_off, nblk, keys64);
+    *launches += 2;
+    uint64_t m = (uint64_t)m_known;
+    if (m_known < 0) {  // first run: the count decides the sort size
+      TablesOut h{};
+      cudaMemcpyAsync(&h, d_out, sizeof h, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      m = h.m_le_t;
+    }
+    sorted = radix_sort_u64(keys64, alt64, (size_t)m, kbits, 31 + kbits, sort_temp, st, launches);
   }
-  tb_rowmax<<<(unsigned)n, 256, 0, st>>>(d_lt, n, rowmax);
-  tb_finalize<<<1, 1024, 0, st>>>(rowmax, n, threshold, sorted, N, kbits, d_out);
   dim3 grid((unsigned)((n + 255) / 256), (unsigned)n);
   tb_rank<<<grid, 256, 0, st>>>(d_lt, n, sorted, kbits, d_out, rank);
-  *launches += 3;
+  *launches += 1;
   *sorted_out = sorted;
 }
 

@@ -222,8 +222,10 @@ struct DimRun {
   int64_t ndeaths_in = 0;
   DevBuf clr;        // clearing bitmap over the d-simplices (empty: recompute mode)
   size_t clr_words = 0;
-  DevBuf hash;       // sparse mode without a bitmap: hash set of the d-simplex pivots
-  uint64_t hash_mask = 0;  // slots - 1; 0 = no hash set (recompute mode)
+  DevBuf hash, bloom;  // sparse mode without a bitmap: the clearing set (ClearSet) of d
+  uint64_t hash_mask = 0;  // slots - 1; 0 = no set (recompute mode)
+  uint32_t bloom_words = 0;
+  bool two_level = false;  // sparse: k_enum_sparse2 (rows = survivors of d-2)
   bool active = false;
 };
 
@@ -254,7 +256,7 @@ struct vr_plan {
   const float* d_lt = nullptr;
   uint64_t N = 0;
   int kbits = 1, kmax = 0;
-  DevBuf rank, binom, keys, alt, rowmax, sort_tmp, tout, ctrs, queue, qvert, resid, resid_alt, app_pairs, lt_copy;
+  DevBuf rank, binom, keys, alt, rowmax, sort_tmp, tb_tmp, tout, ctrs, queue, qvert, resid, resid_alt, app_pairs, lt_copy;
   uint64_t qcap = 0, rcap = 0, app_cap = 0;
   uint32_t maxr = 0;
   uint64_t m = 0;
@@ -266,6 +268,7 @@ struct vr_plan {
   std::vector<DevBuf> rows;           // rows[d] = packed d-simplex survivors (rows of d+1)
   std::vector<uint64_t> rows_count;   // survivors written per dimension
   std::vector<uint64_t> rows_cap;
+  std::vector<uint64_t> next_bound;   // per dimension: sum over its survivors s of deg_below(min s)
   int64_t survivors_total = 0;
   int64_t apparent_total = 0, residual_total = 0;
   int64_t launches = 0;
@@ -284,37 +287,53 @@ struct vr_plan {
   uint32_t* clr_of(int d) {
     return (d >= 1 && d <= D && dims[(size_t)d].clr_words) ? dims[(size_t)d].clr.as<uint32_t>() : nullptr;
   }
-  uint64_t* hash_of(int d) {
-    return (d >= 1 && d <= D && dims[(size_t)d].hash_mask) ? dims[(size_t)d].hash.as<uint64_t>() : nullptr;
+  vr::ClearSet set_of(int d) {
+    vr::ClearSet c{nullptr, 0, nullptr, 1};
+    if (d >= 1 && d <= D && dims[(size_t)d].hash_mask) {
+      c.table = dims[(size_t)d].hash.as<uint64_t>();
+      c.mask = dims[(size_t)d].hash_mask;
+      c.bloom = dims[(size_t)d].bloom.as<uint32_t>();
+      c.bloom_words = dims[(size_t)d].bloom_words;
+    }
+    return c;
   }
-  uint64_t hash_mask_of(int d) { return hash_of(d) ? dims[(size_t)d].hash_mask : 0; }
-  // the hash-set fields of dimension d's HotBuffers
+  // the clearing-set fields of dimension d's HotBuffers
   void hash_fields(vr::HotBuffers& B, int d) {
-    B.clr_hash = hash_of(d);
-    B.clr_hash_mask = hash_mask_of(d);
-    B.clr_next_hash = hash_of(d + 1);
-    B.clr_next_hash_mask = hash_mask_of(d + 1);
+    B.clr_set = set_of(d);
+    B.clr_next_set = set_of(d + 1);
   }
-  // (sized by the row bound, 2x rounded up to a power of two: most probes are misses, and a
-  // low load keeps them at one slot — measured: re-sizing to 2x the inserted count made the
-  // dimension-3 enumeration of config 5 12% slower)
+  // (the table is sized by the row bound, 2x rounded up to a power of two: most probes are
+  // misses, and a low load keeps the few that reach it at one slot)
   void hash_reset(int d, cudaStream_t s) {
-    if (uint64_t* h = hash_of(d)) cudaMemsetAsync(h, 0xFF, (dims[(size_t)d].hash_mask + 1) * 8, s);
+    const vr::ClearSet c = set_of(d);
+    if (!c.table) return;
+    cudaMemsetAsync(c.table, 0xFF, (c.mask + 1) * 8, s);
+    cudaMemsetAsync(c.bloom, 0, (size_t)c.bloom_words * 4, s);
   }
   void hash_deaths(int d, cudaStream_t s) {  // deaths of dimension d-1 (deaths_in of d) into d's set
-    if (uint64_t* h = hash_of(d))
-      vr::launch_hash_put(dims[(size_t)d].deaths_in.as<uint64_t>(), dims[(size_t)d].ndeaths_in, h, dims[(size_t)d].hash_mask, s,
-                          &launches);
+    const vr::ClearSet c = set_of(d);
+    if (c.table) vr::launch_set_put(dims[(size_t)d].deaths_in.as<uint64_t>(), dims[(size_t)d].ndeaths_in, c, s, &launches);
+  }
+  // rows of dimension d: single level — the survivors of d-1 (vertices for d = 1); two
+  // levels — the survivors of d-2 (vertices for d = 2).  Dimension d keeps its survivors
+  // when a later dimension reads them as rows (rows_needed).
+  bool rows_needed(int d) const {
+    for (int k = d + 1; k <= D && k <= d + 2; ++k)
+      if ((dims[(size_t)k].two_level ? k - 2 : k - 1) == d) return true;
+    return false;
   }
   vr::SparseRows sparse_rows(int d, vr::DimCounters* ctr) {
     vr::SparseRows SR{};
     if (sparse) {
       SR.bm = bm.as<uint32_t>();
       SR.nw = nw;
-      SR.rows_in = d == 1 ? nullptr : rows[(size_t)d - 1].as<uint4>();
-      SR.rows_out = d < D ? rows[(size_t)d].as<uint4>() : nullptr;
-      SR.rows_out_cap = d < D ? rows_cap[(size_t)d] : 0;
+      const int src = dims[(size_t)d].two_level ? d - 2 : d - 1;
+      SR.rows_in = src <= 0 ? nullptr : rows[(size_t)src].as<uint4>();
+      const bool keep = rows_needed(d);
+      SR.rows_out = keep ? rows[(size_t)d].as<uint4>() : nullptr;
+      SR.rows_out_cap = keep ? rows_cap[(size_t)d] : 0;
       SR.rows_out_count = &ctr->rows_out;
+      SR.deg_below = deg_below.as<uint32_t>();
     }
     return SR;
   }
@@ -423,6 +442,7 @@ void stage_setup(vr_plan& P) {
   P.tout.ensure(sizeof(vr::TablesOut));
   P.ctrs.ensure(sizeof(vr::DimCounters) * (size_t)(D + 1));
   P.sort_tmp.ensure(vr::radix_sort_temp_bytes(std::max<size_t>(P.N, 1)));
+  P.tb_tmp.ensure(vr::tables_temp_bytes(n));
   CUDA_TRY(cudaMemcpyAsync(P.binom.p, hb.data(), hb.size() * 8, cudaMemcpyHostToDevice, st));
   for (auto& e : P.ev)
     if (!e) CUDA_TRY(cudaEventCreate(&e));
@@ -432,7 +452,8 @@ void stage_setup(vr_plan& P) {
   uint64_t* sorted = nullptr;
   CUDA_TRY(cudaEventRecord(P.ev[0], st));
   vr::launch_tables(P.d_lt, n, P.threshold, P.keys.as<uint64_t>(), P.alt.as<uint64_t>(), P.rowmax.as<uint32_t>(),
-                    P.sort_tmp.p, P.rank.as<uint32_t>(), P.tout.as<vr::TablesOut>(), &sorted, st, &P.launches);
+                    P.sort_tmp.p, P.tb_tmp.p, P.rank.as<uint32_t>(), P.tout.as<vr::TablesOut>(), -1, &sorted, st,
+                    &P.launches);
   CUDA_TRY(cudaGetLastError());
   vr::TablesOut to{};
   CUDA_TRY(cudaMemcpyAsync(&to, P.tout.p, sizeof to, cudaMemcpyDeviceToHost, st));
@@ -500,18 +521,18 @@ void stage_setup(vr_plan& P) {
     if (mode == 2) sp = true;
     P.sparse = sp && D >= 1 && P.m > 0;
     if (P.sparse) {
-      P.nw = (int32_t)((n + 31) / 32);
+      P.nw = (int32_t)(((n + 31) / 32 + 3) / 4 * 4);  // words per row, padded to 16-byte quads
       P.deg.ensure(((size_t)n + 1) * 4);
       P.deg_below.ensure(((size_t)n + 1) * 4);
       P.bm.ensure((size_t)n * (size_t)P.nw * 4);
-      P.bound.ensure(8);
-      vr::launch_threshold_bitmap(P.rank.as<uint32_t>(), (int)n, P.bm.as<uint32_t>(), P.deg.as<uint32_t>(),
+      vr::launch_threshold_bitmap(P.rank.as<uint32_t>(), (int)n, P.nw, P.bm.as<uint32_t>(), P.deg.as<uint32_t>(),
                                   P.deg_below.as<uint32_t>(), st, &P.launches);
       CUDA_TRY(cudaGetLastError());
       P.rows.clear();
       P.rows.resize((size_t)D + 2);
       P.rows_count.assign((size_t)D + 2, 0);
       P.rows_cap.assign((size_t)D + 2, 0);
+      P.next_bound.assign((size_t)D + 2, 0);
       // the host residual walks the same threshold graph: neighbour lists (descending)
       // from the bitmap
       auto ta = std::chrono::steady_clock::now();
@@ -541,6 +562,9 @@ void stage_setup(vr_plan& P) {
   // ---------------- clearing bitmaps (one bit per d-simplex index) where they fit
   P.dims.clear();
   P.dims.resize((size_t)D + 2);
+  // output-sensitive dimensions >= 2 extend the survivors of d-2 by two vertices
+  // (k_enum_sparse2); VR_SPARSE_1LEVEL keeps the single-level kernel (A/B, tests)
+  for (int d = 2; d <= D; ++d) P.dims[(size_t)d].two_level = P.sparse && !std::getenv("VR_SPARSE_1LEVEL");
   CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
   // (tests: VR_FORCE_CLEAR_HASH puts sparse dimensions >= 2 on the hash-set path)
   const bool force_hash = P.sparse && P.world == 1 && std::getenv("VR_FORCE_CLEAR_HASH") != nullptr;
@@ -605,10 +629,10 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
                        : (P.opt.rows_per_grab > 0 ? P.opt.rows_per_grab
                                                   : ((n < 384 && binom_host((uint64_t)n, (uint64_t)d) >= 8192) ? 4 : 1));
   p.variant = P.opt.scan_variant > 0 ? P.opt.scan_variant - 1 : 1;
-  // shards: dense rows (and the vertex rows of sparse dimension 1) are interleaved over
-  // the ranks; sparse rows of d >= 2 are this rank's own survivors of d-1, which already
-  // partition the d-simplices (each has exactly one prefix (d-1)-simplex)
-  const bool interleave = P.world > 1 && (!P.sparse || d == 1);
+  // shards: dense rows (and sparse vertex rows: dimension 1, or 2 with two levels) are
+  // interleaved over the ranks; other sparse rows are this rank's own survivors of a lower
+  // dimension, which already partition the d-simplices (each has exactly one prefix)
+  const bool interleave = P.world > 1 && (!P.sparse || d == (dr.two_level ? 2 : 1));
   p.shard_rank = interleave ? P.rank_id : 0;
   p.shard_world = interleave ? P.world : 1;
   const uint64_t rows = binom_host((uint64_t)n, (uint64_t)d);
@@ -617,25 +641,16 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
   uint32_t* clr_next = P.clr_of(d + 1);
   if (clr_next) CUDA_TRY(cudaMemsetAsync(clr_next, 0, P.dims[(size_t)d + 1].clr_words * 4, st));
 
-  // sparse mode: the rows are the survivors of dimension d-1 (vertices for d = 1) and
-  // sum over rows of deg_below(u_1) bounds the d-simplices they can produce
+  // sparse mode: the rows are the survivors of d-1 (single level; vertices for d = 1) or of
+  // d-2 (two levels; vertices for d = 2).  The d-simplices number at most the bound the
+  // dimension-(d-1) kernel accumulated, sum over its survivors s of deg_below(min s)
   uint64_t bound = cand;
   uint64_t nrows_sp = 0;
   if (P.sparse) {
-    if (d == 1) {
-      nrows_sp = (uint64_t)n;
-      bound = P.m;
-    } else {
-      nrows_sp = P.rows_count[(size_t)d - 1];
-      CUDA_TRY(cudaMemsetAsync(P.bound.p, 0, 8, st));
-      vr::launch_row_bound(P.rows[(size_t)d - 1].as<uint4>(), nrows_sp, d - 1, P.deg_below.as<uint32_t>(),
-                           P.bound.as<unsigned long long>(), st, &P.launches);
-      unsigned long long b = 0;
-      CUDA_TRY(cudaMemcpyAsync(&b, P.bound.p, 8, cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaStreamSynchronize(st));
-      bound = std::min<uint64_t>(cand, b);
-    }
-    if (d < D) {
+    const int src = dr.two_level ? d - 2 : d - 1;
+    nrows_sp = src <= 0 ? (uint64_t)n : P.rows_count[(size_t)src];
+    bound = d == 1 ? P.m : std::min<uint64_t>(cand, P.next_bound[(size_t)d - 1]);
+    if (P.rows_needed(d)) {
       P.rows[(size_t)d].ensure(std::max<uint64_t>(bound, 1) * 16);
       P.rows_cap[(size_t)d] = std::max<uint64_t>(bound, 1);
     }
@@ -650,9 +665,14 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
     while (slots < 2 * std::max<uint64_t>(bound, 1) + 1024) slots <<= 1;
     size_t fb = 0, tb = 0;
     CUDA_TRY(cudaMemGetInfo(&fb, &tb));
-    if (slots * 8 <= fb / 8) {
+    // Bloom filter: 16 bits per bounding key (3 bits set per key: ~0.1% false positives at
+    // the pivots actually inserted)
+    const uint64_t bw = std::min<uint64_t>(std::max<uint64_t>(bound / 2, 1024), (uint64_t)UINT32_MAX);
+    if (slots * 8 + bw * 4 <= fb / 8) {
       nx.hash.ensure(slots * 8);
       nx.hash_mask = slots - 1;
+      nx.bloom.ensure(bw * 4);
+      nx.bloom_words = (uint32_t)bw;
       P.hash_reset(d + 1, st);
     } else {
       nx.hash_mask = 0;
@@ -663,8 +683,12 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
   size_t free_b = 0, total_b = 0;
   CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
   const uint64_t qmax = std::max<uint64_t>((uint64_t)(free_b / 4 / 40), 1024);
-  const uint64_t qwant = std::min<uint64_t>(std::max<uint64_t>(bound, 1), qmax);
-  if (P.sparse && bound > qmax) throw VrError(VR_ECAPACITY, "output-sensitive mode: column bound exceeds device memory");
+  // (sparse mode with a clearing bitmap or set decides every column in the enumeration
+  // kernel: no queue)
+  const bool sp_decided = P.sparse && (P.clr_of(d) || P.set_of(d).table);
+  const uint64_t qwant = sp_decided ? 1024 : std::min<uint64_t>(std::max<uint64_t>(bound, 1), qmax);
+  if (P.sparse && !sp_decided && bound > qmax)
+    throw VrError(VR_ECAPACITY, "output-sensitive mode: column bound exceeds device memory");
   if (P.qcap < qwant) {
     P.queue.ensure((size_t)qwant * 8);
     P.qvert.ensure((size_t)qwant * 16);
@@ -713,7 +737,8 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
     CUDA_TRY(cudaMemsetAsync(&ctr->queued, 0, 8, st));
     CUDA_TRY(cudaEventRecord(P.ev[2], st));
     if (P.sparse) {
-      vr::launch_enumerate_sparse(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, SR, st, &P.launches);
+      vr::launch_enumerate_sparse(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, SR, dr.two_level, st,
+                                  &P.launches);
       kernels |= VR_KERNEL_SPARSE;
     } else {
       kernels |= vr::launch_enumerate(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, st, &P.launches);
@@ -741,12 +766,13 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
     resid_count = rc;
     dr.chunks.push_back(Chunk{rb, re, q});
   }
-  if (P.sparse && d < D) {
-    unsigned long long ro = 0;
-    CUDA_TRY(cudaMemcpyAsync(&ro, &ctr->rows_out, 8, cudaMemcpyDeviceToHost, st));
+  if (P.sparse) {
+    vr::DimCounters c{};
+    CUDA_TRY(cudaMemcpyAsync(&c, ctr, sizeof c, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    if (ro > P.rows_cap[(size_t)d]) throw VrError(VR_ECAPACITY, "survivor list overflow");
-    P.rows_count[(size_t)d] = ro;
+    if (P.rows_needed(d) && c.rows_out > P.rows_cap[(size_t)d]) throw VrError(VR_ECAPACITY, "survivor list overflow");
+    P.rows_count[(size_t)d] = P.rows_needed(d) ? c.rows_out : 0;
+    P.next_bound[(size_t)d] = c.next_bound;
   }
   dr.residual = resid_count;
   ST.mark("  enumerate + resolve");
@@ -908,9 +934,10 @@ void replay(vr_plan& P) {
     auto& e = ev(0);
     cudaEventRecord(e.first, st);
     vr::launch_tables(P.d_lt, P.n, P.threshold, P.keys.as<uint64_t>(), P.alt.as<uint64_t>(), P.rowmax.as<uint32_t>(),
-                      P.sort_tmp.p, P.rank.as<uint32_t>(), P.tout.as<vr::TablesOut>(), &sorted, st, &P.launches);
+                      P.sort_tmp.p, P.tb_tmp.p, P.rank.as<uint32_t>(), P.tout.as<vr::TablesOut>(), (int64_t)P.m, &sorted, st,
+                      &P.launches);
     if (P.sparse)
-      vr::launch_threshold_bitmap(P.rank.as<uint32_t>(), (int)P.n, P.bm.as<uint32_t>(), P.deg.as<uint32_t>(),
+      vr::launch_threshold_bitmap(P.rank.as<uint32_t>(), (int)P.n, P.nw, P.bm.as<uint32_t>(), P.deg.as<uint32_t>(),
                                   P.deg_below.as<uint32_t>(), st, &P.launches);
     if (P.D >= 1 && clr_of(1)) {
       cudaMemsetAsync(clr_of(1), 0, P.dims[1].clr_words * 4, st);
@@ -941,7 +968,9 @@ void replay(vr_plan& P) {
       cudaEventRecord(e2.first, st);
       cudaMemsetAsync(&ctr->row_next, 0, 8, st);
       cudaMemsetAsync(&ctr->queued, 0, 8, st);
-      if (P.sparse) vr::launch_enumerate_sparse(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, SR, st, &P.launches);
+      if (P.sparse)
+        vr::launch_enumerate_sparse(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, SR, dr.two_level, st,
+                                    &P.launches);
       else vr::launch_enumerate(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, st, &P.launches);
       cudaEventRecord(e2.second, st);
       auto& e3 = ev(2);
@@ -1286,10 +1315,11 @@ int vr_dist_replay_tables(vr_plan* P) {
     if (!P) throw VrError(VR_EINVAL, "plan is NULL");
     uint64_t* sorted = nullptr;
     vr::launch_tables(P->d_lt, P->n, P->threshold, P->keys.as<uint64_t>(), P->alt.as<uint64_t>(),
-                      P->rowmax.as<uint32_t>(), P->sort_tmp.p, P->rank.as<uint32_t>(), P->tout.as<vr::TablesOut>(),
+                      P->rowmax.as<uint32_t>(), P->sort_tmp.p, P->tb_tmp.p, P->rank.as<uint32_t>(), P->tout.as<vr::TablesOut>(),
+                      (int64_t)P->m,
                       &sorted, P->st, &P->launches);
     if (P->sparse)
-      vr::launch_threshold_bitmap(P->rank.as<uint32_t>(), (int)P->n, P->bm.as<uint32_t>(), P->deg.as<uint32_t>(),
+      vr::launch_threshold_bitmap(P->rank.as<uint32_t>(), (int)P->n, P->nw, P->bm.as<uint32_t>(), P->deg.as<uint32_t>(),
                                   P->deg_below.as<uint32_t>(), P->st, &P->launches);
     if (P->D >= 1 && P->clr_of(1)) {
       cudaMemsetAsync(P->clr_of(1), 0, P->dims[1].clr_words * 4, P->st);
@@ -1320,7 +1350,9 @@ int vr_dist_replay_dim(vr_plan* P, int32_t d) {
       p.row_end = c.row_end;
       cudaMemsetAsync(&ctr->row_next, 0, 8, st);
       cudaMemsetAsync(&ctr->queued, 0, 8, st);
-      if (P->sparse) vr::launch_enumerate_sparse(p, P->rank.as<uint32_t>(), P->binom.as<uint64_t>(), P->kmax, B, SR, st, &P->launches);
+      if (P->sparse)
+        vr::launch_enumerate_sparse(p, P->rank.as<uint32_t>(), P->binom.as<uint64_t>(), P->kmax, B, SR, dr.two_level, P->st,
+                                    &P->launches);
       else vr::launch_enumerate(p, P->rank.as<uint32_t>(), P->binom.as<uint64_t>(), P->kmax, B, st, &P->launches);
       if (P->sparse) vr::launch_resolve_sparse(p, P->rank.as<uint32_t>(), P->binom.as<uint64_t>(), P->kmax, B, SR, c.queued, st, &P->launches);
       else vr::launch_resolve(p, P->rank.as<uint32_t>(), P->binom.as<uint64_t>(), P->kmax, B, c.queued, st, &P->launches);

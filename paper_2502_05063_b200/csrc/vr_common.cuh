@@ -15,6 +15,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "vr_types.h"
+
 #define VR_RINF 0xFFFFFFFFu
 
 namespace vr {
@@ -146,6 +148,27 @@ __device__ __forceinline__ bool hash_has(const uint64_t* t, uint64_t mask, uint6
     if (x == k) return true;
     if (x == ~0ull) return false;
   }
+}
+
+// The clearing set of a dimension (output-sensitive mode): the cidx of its columns that are
+// pivots (deaths) of the dimension below, in the open-addressing table above, fronted by a
+// blocked Bloom filter — one 32-bit word per key with 3 bits set — that answers most of the
+// (mostly negative) membership probes from a few MB that stay in L2.
+__device__ __forceinline__ void bloom_of(const ClearSet& c, uint64_t h, uint32_t& word, uint32_t& bits) {
+  word = (uint32_t)(((uint64_t)(uint32_t)(h >> 32) * (uint64_t)c.bloom_words) >> 32);
+  bits = (1u << (h & 31)) | (1u << ((h >> 5) & 31)) | (1u << ((h >> 10) & 31));
+}
+__device__ __forceinline__ void set_put(const ClearSet& c, uint64_t k) {
+  uint32_t w, b;
+  bloom_of(c, hash_slot(k), w, b);
+  atomicOr(c.bloom + w, b);
+  hash_put(c.table, c.mask, k);
+}
+__device__ __forceinline__ bool set_has(const ClearSet& c, uint64_t k) {
+  uint32_t w, b;
+  bloom_of(c, hash_slot(k), w, b);
+  if ((__ldcg(c.bloom + w) & b) != b) return false;
+  return hash_has(c.table, c.mask, k);
 }
 
 template <int D>

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/vr.h"
+#include "vr_types.h"
 
 namespace vr {
 
@@ -24,10 +25,13 @@ struct TablesOut {
   uint64_t m_le_t;     // number of edges with d <= t
   uint32_t rbits_pad;
 };
-// keys64 (n(n-1)/2) and alt64 ping-pong buffers, rowmax (n), rank (n*n), out (device)
+// keys64 (n(n-1)/2) and alt64 ping-pong buffers, rowmax (n), rank (n*n), out (device),
+// tb_temp (tables_temp_bytes(n)); m_known = the edge count under t when known (replays), or
+// -1 (the first run: read back after the compaction, one stream synchronisation)
+size_t tables_temp_bytes(int64_t n);
 void launch_tables(const float* d_lt, int64_t n, float threshold, uint64_t* keys64, uint64_t* alt64, uint32_t* rowmax,
-                   void* sort_temp, uint32_t* rank, TablesOut* d_out, uint64_t** sorted_out, cudaStream_t st,
-                   int64_t* launches);
+                   void* sort_temp, void* tb_temp, uint32_t* rank, TablesOut* d_out, int64_t m_known, uint64_t** sorted_out,
+                   cudaStream_t st, int64_t* launches);
 void launch_build_binom(uint64_t* binom, int64_t n, int kmax, cudaStream_t st, int64_t* launches);
 
 // ---------------------------------------------------------------- hot path kernels
@@ -43,9 +47,11 @@ struct DimParams {
   int shard_world = 1;
   uint64_t row_begin, row_end;  // prefix rows [row_begin, row_end) of the d-simplices
   int win = 0;         // 1: k_enumerate stages the 32-vertex scan window in shared memory
+  int slices = 1;      // k_enum_sparse2: work items per row (each takes every slices-th x)
 };
 struct DimCounters {   // device counters (unsigned long long each)
   unsigned long long survivors, apparent1, apparent2, cleared, queued, residual, row_next, app_pairs, scanned, scanned2, rows_out;
+  unsigned long long next_bound;  // sparse: sum over survivors s of deg_below(min s) (bounds the next dimension)
 };
 struct HotBuffers {
   uint64_t* qkey;        // phase-2 queue: column keys
@@ -60,14 +66,12 @@ struct HotBuffers {
   DimCounters* ctr;
   uint64_t* app_pairs;   // debug (index-level output): (s, t) per apparent pair, or nullptr
   uint64_t app_cap;
-  // sparse mode where a bitmap over C(n, d+1) cannot exist: the d-simplex pivots of
-  // dimension d-1 as an open-addressing hash set (key ~0 = empty, power-of-two slots)
-  const uint64_t* clr_hash;
-  uint64_t clr_hash_mask;
-  uint64_t* clr_next_hash;  // receives this dimension's apparent cofacets
-  uint64_t clr_next_hash_mask;
+  // sparse mode where no bitmap over C(n, d+1) is kept: the d-simplex pivots of dimension
+  // d-1 as a hash set with a Bloom filter in front (vr_common.cuh ClearSet)
+  ClearSet clr_set;       // table == nullptr: none
+  ClearSet clr_next_set;  // receives this dimension's apparent cofacets
 };
-void launch_hash_put(const uint64_t* list, int64_t m, uint64_t* table, uint64_t mask, cudaStream_t st, int64_t* launches);
+void launch_set_put(const uint64_t* list, int64_t m, const ClearSet& c, cudaStream_t st, int64_t* launches);
 // returns the VR_KERNEL_* flags of the kernel launched (vr_stats.kernels)
 int launch_enumerate(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
                      cudaStream_t st, int64_t* launches);
@@ -78,19 +82,21 @@ void launch_set_bits(const uint64_t* list, int64_t m, uint32_t* bm, cudaStream_t
 // ---------------------------------------------------------------- sparse.cu (output-sensitive mode)
 struct SparseRows {
   const uint32_t* bm;             // threshold-graph bitmap, n rows of nw words (bit w of row v: d(v,w) <= t, v != w)
-  int32_t nw;                     // words per bitmap row, ceil(n / 32)
-  const uint4* rows_in;           // packed (d-1)-simplex survivors = prefix rows; nullptr for d = 1
-  uint4* rows_out;                // survivors of dimension d (rows of d+1), or nullptr
+  int32_t nw;                     // words per bitmap row: ceil(n / 32) rounded up to a multiple of 4 (zero padding)
+  const uint4* rows_in;           // packed row simplices (single level: survivors of d-1; two levels: of d-2),
+                                  // nullptr = the vertices
+  uint4* rows_out;                // survivors of dimension d (rows of a later dimension), or nullptr
   uint64_t rows_out_cap;
   unsigned long long* rows_out_count;
+  const uint32_t* deg_below;      // #{w < v adjacent to v} per vertex (DimCounters.next_bound)
 };
 // bitmap + deg(v) + deg_below(v) = #{w < v adjacent to v} from the rank matrix
-void launch_threshold_bitmap(const uint32_t* rank, int n, uint32_t* bm, uint32_t* deg, uint32_t* deg_below, cudaStream_t st,
-                             int64_t* launches);
-void launch_row_bound(const uint4* rows, uint64_t nrows, int dprev, const uint32_t* deg_below, unsigned long long* out,
-                      cudaStream_t st, int64_t* launches);
+// (nw: words per row, >= ceil(n/32); the words past the last vertex are written as zeros)
+void launch_threshold_bitmap(const uint32_t* rank, int n, int nw, uint32_t* bm, uint32_t* deg, uint32_t* deg_below,
+                             cudaStream_t st, int64_t* launches);
+// two_level (d >= 2): rows are (d-2)-simplices extended by two vertices (k_enum_sparse2)
 void launch_enumerate_sparse(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
-                             const SparseRows& S, cudaStream_t st, int64_t* launches);
+                             const SparseRows& S, bool two_level, cudaStream_t st, int64_t* launches);
 void launch_resolve_sparse(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
                            const SparseRows& S, uint64_t qn, cudaStream_t st, int64_t* launches);
 

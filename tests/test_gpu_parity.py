@@ -158,7 +158,7 @@ def test_row_scheduling_invariance(grab, D):
     # rows_per_grab: rows per atomic grab; the scan window in shared memory is used at
     # n <= 544 and the global path above — both must agree
     for n in (70, 600):
-        if n == 600 and D == 3:
+        if n == 600 and (D == 3 or (D == 2 and grab != 3)):  # (n = 600, D = 2: 30 s of host residual each)
             continue
         lt = G.random_cloud(n, 5)
         a = vr.barcodes(lt, n, D, rows_per_grab=grab, index_pairs=True)

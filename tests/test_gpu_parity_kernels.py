@@ -97,16 +97,42 @@ def test_row_kernel_window_dim1_vs_oracle(n, kind, thr):
     _check(lt, n, 1, _threshold(lt, n, thr), vr.KERNEL_ROW | vr.KERNEL_SMEM_WINDOW, dims=(1,), sparse_mode=1)
 
 
-# k_enum_sparse: the bitmap rows over several words (n > 32, ragged n % 32) at every
-# dimension, tied and untied, with and without the clearing hash set
+# k_enum_sparse / k_enum_sparse2: the bitmap rows over several words (n > 32, ragged n % 32)
+# at every dimension, tied and untied, with and without the clearing set (hash + Bloom)
 @pytest.mark.parametrize("n,D,kind,thr", [(45, 3, "tied3", "q50"), (45, 3, "cloud", "q60"), (70, 2, "tied5", "q35"),
                                           (70, 2, "cloud", "R"), (150, 1, "tied8", "q20"), (97, 2, "tied3", "q25")])
 @pytest.mark.parametrize("hashset", [False, True])
-def test_sparse_kernel_vs_oracle(n, D, kind, thr, hashset, monkeypatch):
+@pytest.mark.parametrize("levels", [1, 2])
+def test_sparse_kernel_vs_oracle(n, D, kind, thr, hashset, levels, monkeypatch):
+    # levels = 2: dimensions >= 2 on k_enum_sparse2 (rows = survivors of d-2, two vertices
+    # added); 1: every dimension on k_enum_sparse (rows = survivors of d-1)
     if hashset:
         monkeypatch.setenv("VR_FORCE_CLEAR_HASH", "1")
+    if levels == 1:
+        monkeypatch.setenv("VR_SPARSE_1LEVEL", "1")
     lt = _input(kind, n, 500 + n + D)
     _check(lt, n, D, _threshold(lt, n, thr), vr.KERNEL_SPARSE, dims=range(1, D + 1), sparse_mode=2)
+
+
+# the output-sensitive kernels on rows whose C(σ) lists pass SP_LCAP = 256 entries (the
+# segmented path, dense graphs) against the dense kernels (pinned to the oracle above) —
+# the oracle itself is not feasible at these sizes
+@pytest.mark.parametrize("n,D,kind,thr", [(300, 1, "cloud", "R"), (300, 2, "quant16", "q95"), (400, 3, "cloud", "q12")])
+@pytest.mark.parametrize("levels", [1, 2])
+def test_sparse_long_lists_equal_dense(n, D, kind, thr, levels, monkeypatch):
+    lt = _input(kind, n, 700 + n + D)
+    t = _threshold(lt, n, thr)
+    a = vr.barcodes(lt, n, D, t, index_pairs=True, sparse_mode=1)
+    if levels == 1:
+        monkeypatch.setenv("VR_SPARSE_1LEVEL", "1")
+    b = vr.barcodes(lt, n, D, t, index_pairs=True, sparse_mode=2)
+    for d in range(1, D + 1):
+        assert b.stats[d]["kernels"] & vr.KERNEL_SPARSE, d
+    for d in range(D + 1):
+        assert np.array_equal(a.pairs[d], b.pairs[d])
+        assert {tuple(x) for x in a.index_pairs[d].tolist()} == {tuple(x) for x in b.index_pairs[d].tolist()}
+        for k in ("survivors", "apparent", "cleared", "residual_columns", "pairs_all", "essential"):
+            assert a.stats[d][k] == b.stats[d][k], (d, k)
 
 
 # ADVICE (round 1): ties through the window kernels at the sizes where they run, flat

@@ -22,7 +22,11 @@ for r in rows:
         continue
     if cur is None or kern not in cur or hdr is None or not r[0].isdigit():
         continue
-    f = lambda k: float(r[hdr.index(k)]) if r[hdr.index(k)] not in ("", "-") else 0.0
+    def f(k):
+        try:
+            return float(r[hdr.index(k)])
+        except (ValueError, IndexError):
+            return 0.0
     d = lines.setdefault(int(r[0]), [r[1][:90], 0.0, 0.0, 0.0])
     d[1] += f("Instructions Executed")
     d[2] += f("Warp Stall Sampling (All Samples)")
