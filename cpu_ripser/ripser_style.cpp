@@ -129,6 +129,11 @@ struct Ripser {
   int max_dim;
   float thr;
   std::vector<float> D;  // full n x n, diagonal 0
+  // sparse mode (thresholds keeping <= 1/4 of the edges, as Ripser's sparse distance
+  // matrices): each vertex's neighbours under the threshold, descending — a cofacet vertex
+  // must be a neighbour of every vertex of the simplex
+  bool sparse = false;
+  std::vector<std::vector<int>> nbr;
   Binom B;
   std::vector<Pairs> out;
   std::vector<int64_t> n_columns, n_emergent, n_reduced, n_simplices;
@@ -140,6 +145,16 @@ struct Ripser {
         ms_dim(md + 1, 0.0) {
     for (int64_t i = 1; i < n; ++i)
       for (int64_t j = 0; j < i; ++j) D[(size_t)i * n + j] = D[(size_t)j * n + i] = lt[i * (i - 1) / 2 + j];
+    int64_t kept = 0;
+    for (int64_t i = 1; i < n; ++i)
+      for (int64_t j = 0; j < i; ++j) kept += D[(size_t)i * n + j] <= thr;
+    if (n > 64 && 4 * kept <= n * (n - 1) / 2) {
+      sparse = true;
+      nbr.assign((size_t)n, {});
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t w = n - 1; w >= 0; --w)
+          if (w != i && D[(size_t)i * n + w] <= thr) nbr[(size_t)i].push_back((int)w);
+    }
   }
   float dist(int64_t i, int64_t j) const { return D[(size_t)i * n + j]; }
 
@@ -170,6 +185,10 @@ struct Ripser {
   // f(Entry) returns false to stop.
   template <class F>
   void cofacets(const Entry& s, const int* v, int d, F&& f) const {
+    if (sparse) {
+      cofacets_sparse(s, v, d, f);
+      return;
+    }
     uint64_t above = 0, below = s.cidx;  // index parts of the vertices above / below w
     int j = d;                           // v[0..j] are below w
     for (int64_t w = n - 1; w >= 0; --w) {
@@ -185,6 +204,27 @@ struct Ripser {
         --j;
         continue;
       }
+      float dm = s.diam;
+      const float* row = &D[(size_t)w * n];
+      for (int a = 0; a <= d; ++a) dm = std::max(dm, row[v[a]]);
+      if (dm > thr) continue;
+      Entry c{dm, above + B.at(w, j + 2) + below};
+      if (!f(c)) return;
+    }
+  }
+
+  // the same, w running over the neighbours of v[0] (descending) only
+  template <class F>
+  void cofacets_sparse(const Entry& s, const int* v, int d, F&& f) const {
+    uint64_t above = 0, below = s.cidx;
+    int j = d;
+    for (int w : nbr[(size_t)v[0]]) {
+      while (j >= 0 && v[j] > w) {  // vertices of s above w move to the upper part
+        below -= B.at(v[j], j + 1);
+        above += B.at(v[j], j + 2);
+        --j;
+      }
+      if (j >= 0 && v[j] == w) continue;  // w is a vertex of s (it moves up at the next w)
       float dm = s.diam;
       const float* row = &D[(size_t)w * n];
       for (int a = 0; a <= d; ++a) dm = std::max(dm, row[v[a]]);
@@ -355,9 +395,17 @@ struct Ripser {
                 std::vector<Entry>* cols, bool keep_next) {
     int v[16];
     int64_t count = 0;
+    std::vector<int> ws;
     for (const Entry& s : simp) {
       vertices(s.cidx, d, v);
-      for (int64_t w = v[d] + 1; w < n; ++w) {
+      ws.clear();
+      if (sparse) {
+        for (int w : nbr[(size_t)v[d]])
+          if (w > v[d]) ws.push_back(w);
+      } else {
+        for (int64_t w = v[d] + 1; w < n; ++w) ws.push_back((int)w);
+      }
+      for (int w : ws) {
         float dm = s.diam;
         const float* row = &D[(size_t)w * n];
         for (int a = 0; a <= d; ++a) dm = std::max(dm, row[v[a]]);

@@ -202,6 +202,16 @@ class Config:
         generator stream (a subsample usable by the oracle)."""
         return lower_tri_from_points(self.points(n))
 
+    def patch(self, m: int, center: int = 0) -> np.ndarray:
+        """fp32 lower-distance vector of the m points of the full cloud nearest to point
+        `center` (itself included; ties by index), in index order: a local patch with the
+        full cloud's density — for thresholded configs (config 5) the first-m subsample is
+        nearly empty at the config's threshold, a patch is not."""
+        x = self.points()
+        d = np.sqrt(((x - x[center]) ** 2).sum(1))
+        idx = np.sort(np.argsort(d, kind="stable")[:m])
+        return lower_tri_from_points(x[idx])
+
 
 INF = float("inf")
 

@@ -171,14 +171,26 @@ int64_t vr_plan_survivors(const vr_plan* plan);
  * plan's stream), to verify that a replay did the work. */
 int vr_plan_check(vr_plan* plan, int64_t* apparent_total, int64_t* residual_total);
 /* Device time (ms, CUDA events on the plan's stream) of the last replay's stages, summed
- * over dimensions: [0] tables (a0), [1] enumerate + apparent phase 1, [2] apparent
- * phase 2 + clearing + compaction, [3] radix sort.  Synchronizes the plan's stream.
- * Also the algorithmic work counters of the plan's first run: [4] candidates,
- * [5] survivors, [6] cofacet vertices scanned (both phases), [7] rank comparisons of
- * the enumerate kernel, sum over d of (d+1)*(candidates_d + phase-1 scanned_d), [8] rank
- * comparisons of the resolve kernel, sum over d of (d+1)*(phase-2 scanned_d)
- * (DESIGN.md "Roofline"). */
+ * over dimensions: [0] tables (a0), [1] enumerate + apparent phase 1 (with each
+ * dimension's setup), [2] apparent phase 2 + clearing + compaction, [3] radix sort.
+ * Synchronizes the plan's stream.  Also the algorithmic work of the plan's first run,
+ * summed over d: [4] candidates examined, [5] survivors, [6] cofacet vertices scanned (both
+ * phases), [7] integer ops of the enumeration kernels = 2 per rank read (vr_plan_dim_timing
+ * [5] + [6]) + the decode compares, [8] the same for the phase-2 kernels (DESIGN.md
+ * "Roofline"). */
 int vr_plan_timing(vr_plan* plan, double out[9]);
+/* Per dimension d (1..max_dim) of the last replay (synchronizes the plan's stream):
+ * [0] device ms of the enumeration kernel(s) (a1 + a2 + a5 phase 1 + a3), [1] phase-2
+ * kernel(s) (a5 phase 2 + a2 + a6), [2] the radix sort of the residual columns (a4, + the
+ * next dimension's death bits / clearing-set inserts), [3] the dimension's setup (counter
+ * reset, next clearing bitmap / set reset); and the algorithmic work of the plan's first
+ * run: [4] survivors, [5] rank reads of the
+ * enumeration (d per candidate examined: every C(n, d+1) index dense, the survivors in the
+ * output-sensitive mode), [6] rank reads of the apparent test in the enumeration kernel
+ * ((d+1) per scanned cofacet vertex + C(d+2, 2) per tested column), [7] rank reads of the
+ * phase-2 kernel, [8] decode compares ((d+1)·⌈log2 n⌉ per tested column — credited work the
+ * fused kernels do not execute), [9] the VR_KERNEL_* flags. */
+int vr_plan_dim_timing(vr_plan* plan, int32_t d, double out[10]);
 void vr_plan_free(vr_plan* plan);
 
 /* ----------------------------------------------------------------------------------
@@ -340,6 +352,14 @@ void vr_w1_net_free(vr_w1_net* net);
  * order), using the current device.  Returns VR_OK or an error code.
  * ---------------------------------------------------------------------------------- */
 int vr_radix_sort_u64(uint64_t* keys, int64_t n, int32_t begin_bit, int32_t end_bit);
+
+/* ----------------------------------------------------------------------------------
+ * Diagnostics (bench.py): measured on-chip peaks of `device` — the integer-ALU throughput
+ * (IMNMX/LOP3 chains, ops/s) and the L2 read bandwidth (a 48 MiB L2-resident buffer,
+ * bytes/s) — the roofline denominators of the hot kernels.  Synchronous;
+ * allocates 48 MiB on the device for the call.
+ * ---------------------------------------------------------------------------------- */
+int vr_probe_peaks(int32_t device, double* alu_ops_per_s, double* l2_bytes_per_s);
 
 #ifdef __cplusplus
 }

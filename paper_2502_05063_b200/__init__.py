@@ -95,6 +95,7 @@ def load() -> ctypes.CDLL:
         "vr_plan_check": (ctypes.c_int, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
         "vr_plan_timing": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double)]),
         "vr_plan_free": (None, [vp]),
+        "vr_plan_dim_timing": (ctypes.c_int, [vp, i32, ctypes.POINTER(ctypes.c_double)]),
         "vr_radix_sort_u64": (ctypes.c_int, [vp, i64, i32, i32]),
         "vr_hypha_pivots": (ctypes.c_int, [vp, vp, i64, vp, i32, vp, vp]),
         "vr_min_cost_flow": (ctypes.c_int, [i64, vp, i64, vp, vp, vp, i64, vp, vp]),
@@ -116,6 +117,7 @@ def load() -> ctypes.CDLL:
         "vr_dist_replay_deaths": (ctypes.c_int, [vp, i32]),
         "vr_dist_copy_keys_async": (ctypes.c_int, [vp, i32, vp]),
         "vr_plan_launches": (i64, [vp]),
+        "vr_probe_peaks": (ctypes.c_int, [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
         "vr_host_residual": (ctypes.c_int, [vp, vp, i64, i64, i32, ctypes.c_uint32, i32, vp, i64, i32, vp, vp, vp, vp,
                                             ctypes.POINTER(i64)]),
     }
@@ -407,6 +409,14 @@ class Plan:
         _check(load().vr_plan_timing(self._h, out))
         keys = ["ms_tables", "ms_enumerate", "ms_resolve", "ms_sort", "candidates", "survivors", "scanned",
                 "rank_ops_enumerate", "rank_ops_resolve"]
+        return dict(zip(keys, list(out)))
+
+    def dim_timing(self, d: int) -> dict:
+        """Per-dimension device ms of the last replay + the first run's work (vr_plan_dim_timing)."""
+        out = (ctypes.c_double * 10)()
+        _check(load().vr_plan_dim_timing(self._h, d, out))
+        keys = ["ms_enumerate", "ms_resolve", "ms_sort", "ms_setup", "survivors", "reads_a1", "reads_a5",
+                "reads_a5_phase2", "decode", "kernels"]
         return dict(zip(keys, list(out)))
 
     def close(self):

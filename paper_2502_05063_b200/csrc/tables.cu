@@ -1,6 +1,7 @@
 // tables.cu — step a0: the device tables every later kernel reads.
 //
-//   1. tb_rowmax    : row maxima of the symmetric matrix (enclosing radius, §5.2.12).
+//   1. tb_rowmax    : row maxima of the symmetric matrix (enclosing radius, §5.2.12), by
+//                     32 x 32 tiles of the lower triangle (row and column maxima).
 //   2. tb_threshold : R = min_i rowmax_i, t = threshold or R when threshold is
 //                     +inf (Prop 5.2.13).
 //   3. tb_edge_count / scan / tb_edge_compact : validate the fp32 lower-distance input
@@ -13,7 +14,8 @@
 //                     ascending, cidx DEscending: exactly the §5.1.4 filtration order of the
 //                     edges (dimension 0 walks it for union-find) and the sorted distance
 //                     list the ranks index.
-//   5. tb_rank      : rank[i][j] = index of the first sorted edge with the value d(i,j)
+//   5. tb_rank      : (by tiles, written to (i, j) and (j, i) through shared memory)
+//                     rank[i][j] = index of the first sorted edge with the value d(i,j)
 //                     (a lower_bound), or RINF when d(i,j) > t or i = j.  Equal distances get equal
 //                     ranks and the order is kept, so rank comparisons are the paper's
 //                     diameter comparisons, exactly (reading A11: no arithmetic on values).
@@ -36,22 +38,43 @@ __device__ __forceinline__ uint32_t dist_bits(float x) {
   return x == 0.0f ? 0u : __float_as_uint(x);
 }
 
+// The symmetric matrix in 32 x 32 tiles (I, J), I >= J, of the lower triangle: a tile's rows
+// i = 32I + a are contiguous runs of the lower-distance vector (coalesced reads); its column
+// maxima are row maxima of the transposed tile (symmetry), and its ranks are written to
+// both (i, j) and (j, i) through a transpose in shared memory (coalesced writes).
+__device__ __forceinline__ void tile_of(uint32_t b, int& I, int& J) {
+  int t = (int)((sqrtf(8.0f * (float)b + 1.0f) - 1.0f) * 0.5f);
+  while ((uint64_t)(t + 1) * (uint64_t)(t + 2) / 2 <= b) ++t;
+  while ((uint64_t)t * (uint64_t)(t + 1) / 2 > b) --t;
+  I = t;
+  J = (int)(b - (uint32_t)((uint64_t)t * (uint64_t)(t + 1) / 2));
+}
+
+// rowmax[] must be zero on entry (atomicMax of the non-negative fp32 bit patterns)
 __global__ void tb_rowmax(const float* __restrict__ lt, int64_t n, uint32_t* __restrict__ rowmax) {
-  __shared__ uint32_t red[32];
-  const int64_t i = blockIdx.x;
-  uint32_t m = 0;
-  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-    uint32_t b = dist_bits(lt_at(lt, i, j));
-    m = b > m ? b : m;
-  }
+  __shared__ uint32_t cmax[8][32];
+  int I, J;
+  tile_of(blockIdx.x, I, J);
+  const int bx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads, 4 rows each
+  const int64_t j = 32 * (int64_t)J + bx;
+  uint32_t cm = 0;
+  for (int a = ty; a < 32; a += 8) {
+    const int64_t i = 32 * (int64_t)I + a;
+    uint32_t x = 0;
+    if (i < n && j < i) x = dist_bits(__ldg(lt + i * (i - 1) / 2 + j));
+    cm = x > cm ? x : cm;
+    uint32_t rm = x;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) { uint32_t y = __shfl_xor_sync(0xffffffffu, m, o); m = y > m ? y : m; }
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    for (int o = 16; o; o >>= 1) { const uint32_t y = __shfl_xor_sync(0xffffffffu, rm, o); rm = y > rm ? y : rm; }
+    if (bx == 0 && i < n && rm) atomicMax(rowmax + i, rm);
+  }
+  cmax[ty][bx] = cm;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t r = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = red[w] > r ? red[w] : r;
-    rowmax[i] = r;
+  if (ty == 0) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m = cmax[k][bx] > m ? cmax[k][bx] : m;
+    if (j < n && m) atomicMax(rowmax + j, m);
   }
 }
 
@@ -135,28 +158,37 @@ __global__ void tb_edge_compact(const float* __restrict__ lt, uint64_t N, int kb
 
 __global__ void tb_rank(const float* __restrict__ lt, int64_t n, const uint64_t* __restrict__ sorted, int kbits,
                         const TablesOut* __restrict__ tout, uint32_t* __restrict__ rank) {
+  __shared__ uint32_t tile[32][33];
   const uint32_t tb = tout->tbits;
   const uint64_t m = tout->m_le_t;
-  const int64_t i = blockIdx.y;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t r;
-    if (i == j) {
-      r = VR_RINF;  // no self-pairs: a scan over cofacet vertices v needs no v != s_i test
-    } else {
-      const uint32_t b = dist_bits(lt_at(lt, i, j));
-      if (b > tb) {
-        r = VR_RINF;
-      } else {
+  int I, J;
+  tile_of(blockIdx.x, I, J);
+  const int bx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t j = 32 * (int64_t)J + bx;
+  for (int a = ty; a < 32; a += 8) {
+    const int64_t i = 32 * (int64_t)I + a;
+    uint32_t r = VR_RINF;  // i = j: no self-pairs (a scan over cofacet vertices needs no v != s_i test)
+    if (i < n && j < i) {
+      const uint32_t b = dist_bits(__ldg(lt + i * (i - 1) / 2 + j));
+      if (b <= tb) {
         const uint64_t x = (uint64_t)b << kbits;
         uint64_t lo = 0, hi = m;
         while (lo < hi) {
-          uint64_t mid = (lo + hi) >> 1;
+          const uint64_t mid = (lo + hi) >> 1;
           if (__ldg(sorted + mid) < x) lo = mid + 1; else hi = mid;
         }
         r = (uint32_t)lo;
       }
     }
-    rank[(size_t)i * (size_t)n + (size_t)j] = r;
+    tile[a][bx] = r;
+    if (i < n && j <= i) rank[(size_t)i * (size_t)n + (size_t)j] = r;
+  }
+  __syncthreads();
+  // the transpose: (j', i') = (32J + a, 32I + bx) with i' > j'
+  for (int a = ty; a < 32; a += 8) {
+    const int64_t jj = 32 * (int64_t)J + a;
+    const int64_t ii = 32 * (int64_t)I + bx;
+    if (ii < n && jj < ii) rank[(size_t)jj * (size_t)n + (size_t)ii] = tile[bx][a];
   }
 }
 
@@ -202,7 +234,10 @@ void launch_tables(const float* d_lt, int64_t n, float threshold, uint64_t* keys
   const uint64_t N = (uint64_t)n * (uint64_t)(n - 1) / 2;
   const int kbits = bits_for(N ? N - 1 : 0);
   cudaMemsetAsync(d_out, 0, sizeof(TablesOut), st);
-  tb_rowmax<<<(unsigned)n, 256, 0, st>>>(d_lt, n, rowmax);
+  const int T = (int)((n + 31) / 32);
+  const unsigned tiles = (unsigned)((int64_t)T * (T + 1) / 2);
+  cudaMemsetAsync(rowmax, 0, (size_t)n * 4, st);
+  tb_rowmax<<<tiles, 256, 0, st>>>(d_lt, n, rowmax);
   tb_threshold<<<1, 1024, 0, st>>>(rowmax, n, threshold, d_out);
   *launches += 2;
   uint64_t* sorted = keys64;
@@ -226,8 +261,7 @@ void launch_tables(const float* d_lt, int64_t n, float threshold, uint64_t* keys
     }
     sorted = radix_sort_u64(keys64, alt64, (size_t)m, kbits, 31 + kbits, sort_temp, st, launches);
   }
-  dim3 grid((unsigned)((n + 255) / 256), (unsigned)n);
-  tb_rank<<<grid, 256, 0, st>>>(d_lt, n, sorted, kbits, d_out, rank);
+  tb_rank<<<tiles, 256, 0, st>>>(d_lt, n, sorted, kbits, d_out, rank);
   *launches += 1;
   *sorted_out = sorted;
 }

@@ -226,6 +226,10 @@ struct DimRun {
   uint64_t hash_mask = 0;  // slots - 1; 0 = no set (recompute mode)
   uint32_t bloom_words = 0;
   bool two_level = false;  // sparse: k_enum_sparse2 (rows = survivors of d-2)
+  // algorithmic work of the first run: rank reads of
+  // the enumeration (a1) and of the apparent test (a5, both phases), decode compares
+  double reads_a1 = 0, reads_a5 = 0, reads_a5_phase2 = 0, decode = 0, decode_phase2 = 0;
+  int64_t kernels = 0;
   bool active = false;
 };
 
@@ -276,6 +280,7 @@ struct vr_plan {
   double work_candidates = 0, work_scanned = 0, work_rank_ops = 0, work_scanned2 = 0, work_rank_ops2 = 0;
   // replay timing: event pairs per stage (0 tables, 1 enumerate, 2 resolve, 3 sort)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> stage_ev[4];
+  std::vector<int> stage_dim[4];  // dimension of each event pair (0: tables; -d: per-dimension setup)
   int used_events[4] = {0, 0, 0, 0};
   ~vr_plan() {
     if (st) cudaStreamSynchronize(st);  // the device buffers go back to DevCache
@@ -806,9 +811,9 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
   stt.ms_resolve = t_res;
   stt.ms_sort = t_sort;
   stt.kernels = kernels;
-  // candidates the kernels actually examine: all C(n, d+1) dense; in sparse mode the
-  // (row, neighbour of u_1 below u_1) pairs, i.e. the row bound
-  const double cand_work = P.sparse ? (double)bound : (double)cand;
+  // candidates the kernels examine: all C(n, d+1) dense; in the output-sensitive mode the
+  // bitmap AND yields the survivors only
+  const double cand_work = P.sparse ? (double)hc.survivors : (double)cand;
   P.work_candidates += cand_work;
   P.work_scanned += (double)hc.scanned;
   P.work_scanned2 += (double)hc.scanned2;
@@ -826,6 +831,12 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
     P.work_rank_ops += 2.0 * d * cand_work + 2.0 * (d + 1) * (double)hc.scanned + 2.0 * cd2 * tested +
                        (double)(d + 1) * lg * tested;
     P.work_rank_ops2 += 2.0 * (d + 1) * (double)hc.scanned2 + (double)(d + 1) * lg * queued;
+    dr.reads_a1 = (double)d * cand_work;
+    dr.reads_a5 = (double)(d + 1) * (double)hc.scanned + cd2 * tested;
+    dr.reads_a5_phase2 = (double)(d + 1) * (double)hc.scanned2;
+    dr.decode = (double)(d + 1) * lg * tested;
+    dr.decode_phase2 = (double)(d + 1) * lg * queued;
+    dr.kernels = kernels;
   }
   P.survivors_total += stt.survivors;
   P.apparent_total += stt.apparent;
@@ -918,6 +929,7 @@ void run_full(vr_plan& P) {
 void replay(vr_plan& P) {
   cudaStream_t st = P.st;
   int used[4] = {0, 0, 0, 0};
+  int cur_dim = 0;
   auto ev = [&](int stage) -> std::pair<cudaEvent_t, cudaEvent_t>& {
     auto& v = P.stage_ev[stage];
     if ((int)v.size() <= used[stage]) {
@@ -925,7 +937,9 @@ void replay(vr_plan& P) {
       CUDA_TRY(cudaEventCreate(&e.first));
       CUDA_TRY(cudaEventCreate(&e.second));
       v.push_back(e);
+      P.stage_dim[stage].push_back(0);
     }
+    P.stage_dim[stage][(size_t)used[stage]] = cur_dim;
     return v[(size_t)used[stage]++];
   };
   auto clr_of = [&](int d) -> uint32_t* { return P.clr_of(d); };
@@ -950,7 +964,9 @@ void replay(vr_plan& P) {
     if (dr.chunks.empty()) continue;
     vr::DimCounters* ctr = P.ctrs.as<vr::DimCounters>() + d;
     uint32_t* clr_next = clr_of(d + 1);
+    cur_dim = -d;  // the dimension's setup: counters, next clearing bitmap / set reset
     auto& e1 = ev(1);
+    cur_dim = d;
     cudaEventRecord(e1.first, st);
     cudaMemsetAsync(ctr, 0, sizeof(vr::DimCounters), st);
     if (clr_next) cudaMemsetAsync(clr_next, 0, P.dims[(size_t)d + 1].clr_words * 4, st);
@@ -1200,6 +1216,33 @@ int vr_plan_timing(vr_plan* P, double out[9]) {
     out[6] = P->work_scanned + P->work_scanned2;
     out[7] = P->work_rank_ops;
     out[8] = P->work_rank_ops2;
+  });
+}
+
+int vr_plan_dim_timing(vr_plan* P, int32_t d, double out[10]) {
+  return guarded([&] {
+    if (!P || !out || d < 1 || d > P->D) throw VrError(VR_EINVAL, "bad plan / dimension");
+    CUDA_TRY(cudaStreamSynchronize(P->st));
+    double t[4] = {0, 0, 0, 0};
+    for (int k = 0; k < 4; ++k)
+      for (int i = 0; i < P->used_events[k]; ++i) {
+        const int dd = P->stage_dim[k][(size_t)i];
+        if (dd != d && !(k == 1 && dd == -d)) continue;
+        float x = 0;
+        CUDA_TRY(cudaEventElapsedTime(&x, P->stage_ev[k][(size_t)i].first, P->stage_ev[k][(size_t)i].second));
+        t[dd == -d ? 0 : k] += x;
+      }
+    const DimRun& dr = P->dims[(size_t)d];
+    out[0] = t[1];  // enumeration kernel(s)
+    out[1] = t[2];  // phase-2 kernel(s)
+    out[2] = t[3];  // sort (+ the next dimension's death bits / set inserts)
+    out[3] = t[0];  // setup (counter reset, next clearing bitmap / set reset)
+    out[4] = (double)P->R->stats[(size_t)d].survivors;
+    out[5] = dr.reads_a1;
+    out[6] = dr.reads_a5;
+    out[7] = dr.reads_a5_phase2;
+    out[8] = dr.decode + dr.decode_phase2;
+    out[9] = (double)dr.kernels;
   });
 }
 

@@ -78,3 +78,17 @@ def test_equals_library(name, D):
     got, _ = RS.barcode(lt, cfg.n, D, bc.threshold)
     for d in range(D + 1):
         np.testing.assert_array_equal(_sorted(got[d]), _sorted(bc.pairs[d]))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_sparse_mode_equals_oracle(seed):
+    # thresholds keeping <= 1/4 of the edges at n > 64 switch cpu_ripser to neighbour lists
+    n, D = 72 + seed, 1 + seed % 3
+    lt = G.random_cloud(n, 40 + seed) if seed % 2 else (np.round(G.random_cloud(n, 40 + seed) * 8) / 8).astype(np.float32)
+    thr = float(np.quantile(lt, 0.12 if D == 3 else 0.2))
+    ob = O.barcode(lt, n, D, thr)
+    got, st = RS.barcode(lt, n, D, thr)
+    for d in range(D + 1):
+        np.testing.assert_array_equal(got[d], ob.positive(d))
+    for d in range(1, D + 1):
+        assert st[d]["simplices"] == ob.n_simplices[d]
