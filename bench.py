@@ -172,7 +172,7 @@ def oracle_sample(cfg, D, m):
 
 def default_sample(cfg, D):
     if not math.isinf(cfg.threshold):
-        return 96  # the oracle's dense position index caps C(m, D+2) at 2e8
+        return 118  # the oracle's dense position index caps C(m, D+2) at 2e8
     return {1: 64, 2: 64, 3: 56}.get(D, 40) if cfg.n > 64 else cfg.n
 
 

@@ -29,6 +29,7 @@
 // non-apparent ones go to k_resolve_sparse for the clearing decision by recomputation.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "vr_common.cuh"
@@ -148,6 +149,42 @@ __device__ __forceinline__ int bm_list(const SparseRows& S, const int (&x)[K], i
 struct Acc {
   unsigned long long surv = 0, app = 0, scan = 0, clr = 0, next_bound = 0;
 };
+
+// Lemma 5.3.6 condition 1 over a lane's list cl[0..fill) (descending; ml = m(v), the
+// prefix part of the new edges' maximum; rw = the lane's rank-matrix row R[w][.]): the first
+// v with v != w and max(m(v), R[w][v]) <= rs.  Four candidates per round: their rank
+// gathers (only where m(v) <= rs) are in flight together, so a lane's scan of L candidates
+// costs ~L/4 dependent L2 round trips.  `examined` counts the candidates up to the hit, as a
+// one-at-a-time scan would.
+__device__ __forceinline__ void scan4(const uint16_t* cl, const uint32_t* ml, int fill, const uint32_t* rw, int w,
+                                      uint32_t rs, bool& active, int& hitv, int& examined) {
+  for (int k = 0; __any_sync(0xffffffffu, active); k += 4) {
+    if (!active) continue;
+    int v[4];
+    uint32_t r[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[i] = -1;
+      r[i] = VR_RINF;
+      if (k + i < fill) {
+        v[i] = cl[k + i];
+        if (v[i] != w && ml[k + i] <= rs) r[i] = __ldg(rw + v[i]);
+      }
+    }
+    int h = -1;
+#pragma unroll
+    for (int i = 3; i >= 0; --i)
+      if (r[i] <= rs) h = i;
+    if (h >= 0) {
+      hitv = v[h];
+      examined += h + 1;
+      active = false;
+    } else {
+      examined += (fill - k < 4 ? fill - k : 4);
+      if (k + 4 >= fill) active = false;
+    }
+  }
+}
 
 // Lemma 5.3.6 condition 1 over one list segment: the first v of cv[0..fill) (descending)
 // with v != w and max(m(v), R[w][v]) <= rs; all lanes step together (broadcast shared
@@ -281,8 +318,8 @@ __device__ __forceinline__ void row_from_list(const Tables& T, const DimParams& 
     const uint64_t cidx = cbase + (uint64_t)w;
     const bool cleared = survivor_head<D>(B, S, s, valid, nb, cidx, acc);
     bool active = valid && !cleared;
-    int examined = 0;
-    const int hitv = __any_sync(0xffffffffu, active) ? scan_list(T, cv, cm, fill, w, rs, active, examined) : -1;
+    int examined = 0, hitv = -1;
+    scan4(cv, cm, fill, T.rank + (uint32_t)w * (uint32_t)T.n, w, rs, active, hitv, examined);
     survivor_tail<D>(T, p, B, u, pm_up, pm_ex, s, w, rs, cidx, valid, cleared, hitv, examined, acc);
   }
 }
@@ -475,21 +512,34 @@ __global__ void __launch_bounds__(SP_THREADS, 4) k_enum_sparse(Tables T, DimPara
 // dimension D-2; the vertices for D = 2).  C(τ) is listed once, with m_τ(v) = max_{i>=2}
 // R[u_i][v]; each x ∈ C(τ), x < u_2 — a (D-1)-simplex σ = τ ∪ {x} — then gets its own
 // C(σ) = { v ∈ C(τ) : R[x][v] != RINF } with m_σ(v) = max(m_τ(v), R[x][v]): ONE rank gather
-// per list entry instead of the AND of D bitmap rows and D gathers.  τ lists longer than
-// SP_LCAP fall back to row_general per σ.
+// per list entry instead of the AND of D bitmap rows and D gathers.  The σ lists are packed
+// side by side in shared memory so that one batch of 32 lanes takes the survivors of
+// several σ (≈ 10 each at config 5, dimension 3): the survivor tests, scans and outputs run
+// with full warps.  τ lists longer than SP_LCAP fall back to row_general per σ.
+constexpr int SP_PCAP = 512;  // packed C(σ) entries per warp
+constexpr int SP_MAXG = 16;   // σ per group
+
+// one warp's shared memory: every array addressed from one base register
 template <int D>
-__global__ void __launch_bounds__(SP_THREADS, 4) k_enum_sparse2(Tables T, DimParams p, HotBuffers B, SparseRows S) {
-  __shared__ uint16_t s_tv[SP_WARPS][SP_LCAP];  // C(τ)
-  __shared__ uint32_t s_tm[SP_WARPS][SP_LCAP];  // m_τ
-  __shared__ uint16_t s_cv[SP_WARPS][SP_LCAP];  // C(σ)
-  __shared__ uint32_t s_cm[SP_WARPS][SP_LCAP];  // m_σ
-  __shared__ uint16_t s_w[SP_WARPS][128];
+struct alignas(16) Sp2Smem {
+  uint32_t tm[SP_LCAP];          // m_τ
+  uint32_t cm[SP_PCAP];          // m_σ, packed
+  uint32_t gpm[SP_MAXG][D + 1];  // per σ of the group: [0] pm_up, [j] pm_ex[j]
+  uint16_t tv[SP_LCAP];          // C(τ)
+  uint16_t cv[SP_PCAP];          // C(σ) lists, packed
+  uint16_t sw[128];              // (fallback path)
+  int16_t gx[SP_MAXG], goff[SP_MAXG], gfill[SP_MAXG], gfw[SP_MAXG], gslot[SP_MAXG + 1];
+};
+
+template <int D, int MINB>
+__global__ void __launch_bounds__(SP_THREADS, MINB) k_enum_sparse2(Tables T, DimParams p, HotBuffers B, SparseRows S) {
+  __shared__ Sp2Smem<D> smem[SP_WARPS];
   const int lane = threadIdx.x & 31;
-  const int wi = threadIdx.x >> 5;
-  uint16_t* tv = s_tv[wi];
-  uint32_t* tm = s_tm[wi];
-  uint16_t* cv = s_cv[wi];
-  uint32_t* cm = s_cm[wi];
+  Sp2Smem<D>& M = smem[threadIdx.x >> 5];
+  uint16_t* tv = M.tv;
+  uint32_t* tm = M.tm;
+  uint16_t* cv = M.cv;
+  uint32_t* cm = M.cm;
   Acc acc;
   const uint64_t W = (uint64_t)p.shard_world;
   const uint64_t all = p.row_end - p.row_begin;
@@ -533,7 +583,7 @@ __global__ void __launch_bounds__(SP_THREADS, 4) k_enum_sparse2(Tables T, DimPar
           for (int ix = 0; ix < nx; ++ix) {
             if ((base + ix) % (int)p.slices != slice) continue;
             u[1] = tv[ix];
-            row_general<D>(T, p, B, S, u, cv, cm, s_w[wi], acc);
+            row_general<D>(T, p, B, S, u, cv, cm, M.sw, acc);
           }
           base += nx;
           __syncwarp();
@@ -545,55 +595,150 @@ __global__ void __launch_bounds__(SP_THREADS, 4) k_enum_sparse2(Tables T, DimPar
       uint32_t pt_up;
       uint32_t pt_ex[D + 1];
       pair_maxima<D>(T, u, 2, pt_up, pt_ex);
+      uint32_t pt_ex_l = 0;  // lane j (2..D): pt_ex[j]
+#pragma unroll
+      for (int j = 2; j <= D; ++j)
+        if (lane == j) pt_ex_l = pt_ex[j];
       uint64_t cb_t = 0;
 #pragma unroll
       for (int i = 2; i <= D; ++i) cb_t += binom(T, u[i], i + 1);
-      for (int ix = nab + slice; ix < tfill; ix += (int)p.slices) {  // σ = τ ∪ {x}, x descending
-        const int x = tv[ix];
-        if (x == 0) continue;
-        u[1] = x;
-        // σ's pair maxima from τ's and the D-1 new edges (x, u_i)
-        uint32_t ax[D + 1];
-        uint32_t pm_up = pt_up;
-#pragma unroll
-        for (int i = 2; i <= D; ++i) {
-          ax[i] = rank_at(T, x, u[i]);
-          pm_up = umax(pm_up, ax[i]);
-        }
-        uint32_t pm_ex[D + 1];
-        pm_ex[0] = 0;
-        pm_ex[1] = pt_up;
-#pragma unroll
-        for (int j = 2; j <= D; ++j) {
-          uint32_t m = pt_ex[j];
-#pragma unroll
-          for (int i = 2; i <= D; ++i)
-            if (i != j) m = umax(m, ax[i]);
-          pm_ex[j] = m;
-        }
-        // C(σ): the entries of C(τ) adjacent to x, order kept (ballot compaction)
-        int fill = 0, first_w = 0;
-        for (int j0 = 0; j0 < tfill; j0 += 32) {
-          const int j = j0 + lane;
-          int v = 0;
-          uint32_t rx = VR_RINF;
-          if (j < tfill) {
-            v = tv[j];
-            rx = rank_at(T, x, v);  // RINF: not adjacent (or v = x)
+      int ix = nab + slice;  // the next σ (x = tv[ix], descending)
+      // a σ listed but left out of the previous group (its survivors did not fit) waits in
+      // the group tables at index `carry` with its list at g_off[carry]; it moves to the
+      // front of the next group
+      int carry = -1;
+      while (true) {
+        // ---- a group: σ lists packed in cv/cm, their survivors slot after slot
+        int ng = 0, poff = 0, slots = 0;
+        if (carry >= 0) {
+          const int c_off = M.goff[carry], c_fill = M.gfill[carry];
+          for (int j0 = 0; j0 < c_fill; j0 += 32) {  // move down (sources above destinations)
+            const int j = j0 + lane;
+            uint16_t v = 0;
+            uint32_t m = 0;
+            if (j < c_fill) { v = cv[c_off + j]; m = cm[c_off + j]; }
+            __syncwarp();
+            if (j < c_fill) { cv[j] = v; cm[j] = m; }
+            __syncwarp();
           }
-          const bool keep = rx != VR_RINF;
-          const uint32_t km = __ballot_sync(0xffffffffu, keep);
-          if (keep) {
-            const int pos = fill + __popc(km & lanemask_lt());
-            cv[pos] = (uint16_t)v;
-            cm[pos] = umax(tm[j], rx);
+          if (lane == 0) {
+            M.gx[0] = M.gx[carry];
+            M.goff[0] = 0;
+            M.gfill[0] = (int16_t)c_fill;
+            M.gfw[0] = M.gfw[carry];
+            M.gslot[0] = 0;
           }
-          first_w += __popc(__ballot_sync(0xffffffffu, keep && v > x));
-          fill += __popc(km);
+          if (lane <= D) M.gpm[0][lane] = M.gpm[carry][lane];
+          __syncwarp();
+          ng = 1;
+          poff = c_fill;
+          slots = c_fill - M.gfw[0];
+          carry = -1;
         }
+        while (ix < tfill && ng < SP_MAXG && poff + tfill <= SP_PCAP && slots < 32) {
+          const int x = tv[ix];
+          ix += (int)p.slices;
+          if (x == 0) continue;
+          // C(σ): the entries of C(τ) adjacent to x, order kept (ballot compaction); the
+          // rank gathers of two 32-entry rounds are issued together
+          const uint32_t* rx_row = T.rank + (uint32_t)x * (uint32_t)T.n;
+          uint32_t axl = 0;  // σ's new edges (x, u_i), lane i-2 holds one
+          if (lane < D - 1) axl = __ldg(rx_row + u[2 + lane]);
+          int fill = 0, first_w = 0;
+          for (int j0 = 0; j0 < tfill; j0 += 64) {
+            const int ja = j0 + lane, jb = j0 + 32 + lane;
+            int va = 0, vb = 0;
+            uint32_t ra = VR_RINF, rb = VR_RINF;
+            if (ja < tfill) va = tv[ja];
+            if (jb < tfill) vb = tv[jb];
+            if (ja < tfill) ra = __ldg(rx_row + va);  // RINF: not adjacent (or v = x)
+            if (jb < tfill) rb = __ldg(rx_row + vb);
+            const bool ka = ra != VR_RINF, kb = rb != VR_RINF;
+            const uint32_t kma = __ballot_sync(0xffffffffu, ka);
+            const uint32_t kmb = __ballot_sync(0xffffffffu, kb);
+            const int na = __popc(kma);
+            if (ka) {
+              const int pos = poff + fill + __popc(kma & lanemask_lt());
+              cv[pos] = (uint16_t)va;
+              cm[pos] = umax(tm[ja], ra);
+            }
+            if (kb) {
+              const int pos = poff + fill + na + __popc(kmb & lanemask_lt());
+              cv[pos] = (uint16_t)vb;
+              cm[pos] = umax(tm[jb], rb);
+            }
+            first_w += __popc(__ballot_sync(0xffffffffu, ka && va > x)) + __popc(__ballot_sync(0xffffffffu, kb && vb > x));
+            fill += na + __popc(kmb);
+          }
+          const int ns = fill - first_w;
+          if (ns <= 0) continue;  // no d-simplex in this σ's row
+          // σ's pair maxima from τ's and the D-1 new edges: [0] pm_up, [1] avoiding x (τ's),
+          // [j] avoiding u_j
+          if (lane <= D) {
+            uint32_t mine = lane == 1 ? pt_up : (lane == 0 ? pt_up : pt_ex_l);
+#pragma unroll
+            for (int i = 2; i <= D; ++i) {
+              const uint32_t ai = __shfl_sync(0x0000ffffu & ((1u << (D + 1)) - 1), axl, i - 2);
+              if (lane == 0 || (lane >= 2 && lane != i)) mine = umax(mine, ai);
+            }
+            M.gpm[ng][lane] = mine;
+          }
+          if (lane == 0) {
+            M.gx[ng] = (int16_t)x;
+            M.goff[ng] = (int16_t)poff;
+            M.gfill[ng] = (int16_t)fill;
+            M.gfw[ng] = (int16_t)first_w;
+            M.gslot[ng] = (int16_t)slots;
+          }
+          __syncwarp();
+          if (slots > 0 && slots + ns > 32) {  // does not fit: first of the next group
+            carry = ng;
+            break;
+          }
+          ++ng;
+          poff += fill;
+          slots += ns;
+        }
+        if (ng == 0) break;
+        if (lane == 0) M.gslot[ng] = (int16_t)slots;
         __syncwarp();
-        const uint64_t cbase = cb_t + binom(T, x, 2);
-        row_from_list<D>(T, p, B, S, u, pm_up, pm_ex, cbase, cv, cm, fill, first_w, acc);
+        // ---- the group's survivors, 32 slots per batch (several batches only for one σ
+        // with more than 32 survivors)
+        for (int b0 = 0; b0 < slots; b0 += 32) {
+          const int t = b0 + lane;
+          const bool valid = t < slots;
+          int q = 0;
+          while (q + 1 < ng && M.gslot[q + 1] <= t) ++q;
+          const int off = M.goff[q], qfill = M.gfill[q];
+          const int li = M.gfw[q] + (t - M.gslot[q]);
+          u[1] = M.gx[q];
+          uint32_t pm_ex[D + 1];
+          pm_ex[0] = 0;
+#pragma unroll
+          for (int j = 1; j <= D; ++j) pm_ex[j] = M.gpm[q][j];
+          const uint32_t pm_up = M.gpm[q][0];
+          int w = 0;
+          uint32_t rs = 0;
+          if (valid) {
+            w = cv[off + li];
+            rs = umax(pm_up, cm[off + li]);
+          }
+          int s[D + 1];
+#pragma unroll
+          for (int i = 0; i < D; ++i) s[i] = u[D - i];
+          s[D] = w;
+          const uint64_t cidx = cb_t + binom(T, u[1], 2) + (uint64_t)w;
+          const int nb = slots - b0 < 32 ? slots - b0 : 32;
+          const bool cleared = survivor_head<D>(B, S, s, valid, nb, cidx, acc);
+          bool active = valid && !cleared;
+          int examined = 0, hitv = -1;
+          // Lemma 5.3.6 condition 1 over the lane's own C(σ) (descending)
+          const uint16_t* cl = cv + off;
+          const uint32_t* ml = cm + off;
+          const uint32_t* rw = T.rank + (uint32_t)w * (uint32_t)T.n;
+          scan4(cl, ml, qfill, rw, w, rs, active, hitv, examined);
+          survivor_tail<D>(T, p, B, u, pm_up, pm_ex, s, w, rs, cidx, valid, cleared, hitv, examined, acc);
+        }
         __syncwarp();
       }
       __syncwarp();
@@ -741,7 +886,11 @@ static void enum_sparse_d(const DimParams& p, const Tables& T, const HotBuffers&
       if (blocks > cap) blocks = cap;
       if (blocks < 1) blocks = 1;
       q.grab = rows * (uint64_t)q.slices >= cap * SP_WARPS * 64 ? 4 : 1;
-      k_enum_sparse2<D><<<(unsigned)blocks, SP_THREADS, 0, st>>>(T, q, B, S);
+      // (tuning: VR_SP_MINB = resident CTAs per SM the registers are budgeted for)
+      static const int minb = std::getenv("VR_SP_MINB") ? std::atoi(std::getenv("VR_SP_MINB")) : 4;
+      if (minb == 2) k_enum_sparse2<D, 2><<<(unsigned)blocks, SP_THREADS, 0, st>>>(T, q, B, S);
+      else if (minb == 3) k_enum_sparse2<D, 3><<<(unsigned)blocks, SP_THREADS, 0, st>>>(T, q, B, S);
+      else k_enum_sparse2<D, 4><<<(unsigned)blocks, SP_THREADS, 0, st>>>(T, q, B, S);
       return;
     }
   }

@@ -32,8 +32,9 @@ __device__ __forceinline__ uint64_t binom(const Tables& T, int v, int k) {
   return __ldg(T.binom + (size_t)k * (size_t)(T.n + 1) + (size_t)v);
 }
 
+// (32-bit index arithmetic: n <= 65535 keeps i*n + j below 2^32)
 __device__ __forceinline__ uint32_t rank_at(const Tables& T, int i, int j) {
-  return __ldg(T.rank + (size_t)i * (size_t)T.n + (size_t)j);
+  return __ldg(T.rank + ((uint32_t)i * (uint32_t)T.n + (uint32_t)j));
 }
 
 // Largest v in [k-1, hi-1] with C(v, k) <= x  (C(., k) is non-decreasing; C(k-1, k) = 0).
