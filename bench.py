@@ -21,8 +21,9 @@ Roofline: the integer-ALU and L2 peaks are MEASURED on the box (vr_probe_peaks) 
 denominators of the dominant kernel's fraction.
 
 Multi-GPU: `--gpus N` without torchrun re-launches itself under torch.distributed.run with N
-ranks (one process per GPU); under torchrun the workload is sharded over the ranks (strong
-scaling) and value = survivors / max-over-ranks step time.  --impl reference times the CPU
+ranks (one process per GPU); under torchrun the workload is sharded over the ranks inside
+libvr (NCCL communicator from a unique id shared by torch.distributed; strong scaling) and
+value = survivors / max-over-ranks step time.  --impl reference times the CPU
 oracle (explicit boundary matrix + Alg 2) on a bounded sample of the same workload.
 """
 from __future__ import annotations
@@ -406,12 +407,15 @@ def run_ours(args, rank, world, local_rank):
             ms_per_step, stage, dims, launches = time_plan(vr, torch, plan, args.steps, args.warmup, stream, flush, D)
         assert plan.check() == a_ref, "replay did not reproduce the apparent/residual counts"
     else:
-        # shards of every dimension's hot path + the two exchanges per dimension (NCCL)
-        from paper_2502_05063_b200.dist import ShardedHotPath
-        plan = ShardedHotPath(dev_lt, n, D, cfg.threshold)
-        survivors = plan.survivors_total
+        # this rank's shard of every dimension's hot path with the exchanges inside libvr
+        # (NCCL: clearing bitmap all-reduce / apparent-cofacet all-gather, residual keys
+        # all-gather + device merge); replays time exactly that, max over ranks
+        from paper_2502_05063_b200.dist import nccl_comm
+        comm = nccl_comm(local_rank)
+        plan = vr.Plan(dev_lt, n, D, cfg.threshold, stream=stream, comm=comm)
+        survivors = plan.survivors
         for _ in range(args.warmup):
-            plan.step()
+            plan.replay()
         torch.cuda.synchronize()
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -422,7 +426,7 @@ def run_ours(args, rank, world, local_rank):
             for i in range(args.steps):
                 flush.zero_()
                 starts[i].record(stream)
-                launches += plan.step()
+                launches += plan.replay()
                 ends[i].record(stream)
             torch.cuda.synchronize()
         dist.barrier()
@@ -438,17 +442,19 @@ def run_ours(args, rank, world, local_rank):
     if single:
         e2e_s, bc = e2e_wall(vr, lt_host, n, D, cfg.threshold, args.e2e_steps)
     else:
-        from paper_2502_05063_b200.dist import barcodes_sharded
-        barcodes_sharded(torch.from_numpy(lt_host).cuda(non_blocking=True), n, D, cfg.threshold)
+        from paper_2502_05063_b200.dist import barcodes_comm
+        barcodes_comm(lt_host, n, D, cfg.threshold, comm)  # warm
         walls = []
         for _ in range(args.e2e_steps):
             dist.barrier()
             t0 = time.perf_counter()
-            bc = barcodes_sharded(torch.from_numpy(lt_host).cuda(non_blocking=True), n, D, cfg.threshold)
+            bc = barcodes_comm(lt_host, n, D, cfg.threshold, comm)
             walls.append(time.perf_counter() - t0)
         tt = torch.tensor([statistics.median(walls)], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
+        plan.close()
+        comm.close()
     pairs_bytes = sum(p.nbytes for p in bc.pairs)
     if rank != 0:
         return
@@ -457,7 +463,7 @@ def run_ours(args, rank, world, local_rank):
         roof = roofline(plan, D, dims, peaks, cfg.name)
     else:
         roof = {"bound": None, "kernel": "hot path step (sharded)", "achieved": None, "peak": None, "frac": None,
-                "traffic": None, "note": "per-kernel events are recorded by the single-GPU replay only"}
+                "traffic": None, "note": "per-kernel roofline from the single-GPU run"}
     roof["step"] = {"ms_per_step": ms_per_step,
                     "what": "whole hot-path step (tables, every dimension's kernels, sorts, exchanges)"}
     line = {
@@ -465,7 +471,7 @@ def run_ours(args, rank, world, local_rank):
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "u32", "data": "synthetic",
         "config": config_obj(cfg, D, {"survivors": survivors,
-                                      "parallelism": "single GPU" if single else f"row shards x{world}"}),
+                                      "parallelism": "single GPU" if single else f"row shards x{world} (NCCL)"}),
         "wall_s": e2e_s,
         "e2e": {"value": survivors / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(lt_host.nbytes),
                 "d2h_bytes_per_step": int(pairs_bytes), "wall_s_per_barcode": e2e_s},

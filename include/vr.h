@@ -85,7 +85,14 @@ typedef struct {
   int32_t sparse_mode;   /* -1/0 = auto (output-sensitive when <= 25% of the edges are under the
                             threshold, or when the dense index space is too large),
                             1 = always dense, 2 = always output-sensitive; same results */
-  int32_t reserved[4];
+  int32_t num_gpus;      /* vr_barcodes only: 0/1 = one GPU (options.device); G > 1 = devices
+                            0..G-1 of this process, one host thread each, NCCL between them
+                            (ncclCommInitAll), same result */
+  int32_t hot_path_only; /* diagnostics: 1 = run the GPU hot path of every dimension but not the
+                            host residual reduction (no pairs in dimensions >= 1; the counters
+                            of dimension 1 are exact, higher dimensions miss the clearing by
+                            residual deaths).  One GPU only */
+  int32_t reserved[2];
 } vr_options;
 
 /* Per-dimension statistics (Table 5.1 / 5.5 counters, stage times). */
@@ -193,44 +200,63 @@ int vr_plan_timing(vr_plan* plan, double out[9]);
 int vr_plan_dim_timing(vr_plan* plan, int32_t d, double out[10]);
 void vr_plan_free(vr_plan* plan);
 
-/* ----------------------------------------------------------------------------------
- * Distributed stepping (the a7 exchange).  One process per GPU.  Each
- * rank runs its shard of every dimension's hot path; the caller performs the two
- * exchanges of each dimension with its own collectives (paper_2502_05063_b200/dist.py
- * uses torch.distributed / NCCL):
- *   1. the next dimension's clearing bitmap: copy out (vr_dist_bitmap direction 0), SUM
- *      all-reduce over the ranks — every death bit is set by exactly one rank, so the sum
- *      is the bitwise OR — and copy back in (direction 1);
- *   2. the residual columns: copy the locally sorted keys out (vr_dist_copy_keys),
- *      all-gather, merge by key (coboundary order is the key order) and hand the merged
- *      host array to vr_dist_dim_finish, which every rank runs identically.
- * Shards: dense prefix rows are interleaved over the ranks (row r belongs to rank
- * r mod world, taken from the last row down); in the output-sensitive mode dimension 1
- * interleaves the vertices and dimension d >= 2 extends each rank's own survivors of
- * d-1, which partitions the d-simplices (each has exactly one prefix (d-1)-simplex).
- * Device pointers are on the current device; `stream` as in vr_barcodes_device.
- * ---------------------------------------------------------------------------------- */
-int vr_dist_begin(const float* d_dist_lower_tri, int64_t n, int32_t max_dim, float threshold, const vr_options* opt,
-                  void* stream, int32_t rank, int32_t world, vr_plan** plan);
-/* runs dimension d locally; *nkeys = local residual columns; *next_bitmap_words = size of
- * the dimension-(d+1) clearing bitmap in uint32 words (0 = recompute mode, no exchange) */
-int vr_dist_dim_local(vr_plan* plan, int32_t d, int64_t* nkeys, int64_t* next_bitmap_words);
-int vr_dist_copy_keys(vr_plan* plan, int32_t d, uint64_t* dst_device);
-int vr_dist_bitmap(vr_plan* plan, int32_t d, uint32_t* buf_device, int32_t direction /* 0 out, 1 in */);
-/* local counters of dimension d: survivors, apparent, cleared, queued, scanned, residual */
-int vr_dist_counters(vr_plan* plan, int32_t d, int64_t out[6]);
-int vr_dist_dim_finish(vr_plan* plan, int32_t d, const uint64_t* merged_keys_host, int64_t nkeys);
-/* assembles the barcode (every rank holds the same pairs); free the plan with vr_plan_free */
-int vr_dist_end(vr_plan* plan, vr_result** out);
-/* device-only replay of a finished distributed plan (benchmarking, asynchronous on the
- * plan's stream): tables; dimension d's local kernels + local sort; the residual-death
- * bits of dimension d into the bitmap of d+1 (call after exchange A of dimension d).
- * vr_dist_bitmap directions 2/3 and vr_dist_copy_keys_async are the asynchronous copies. */
-int vr_dist_replay_tables(vr_plan* plan);
-int vr_dist_replay_dim(vr_plan* plan, int32_t d);
-int vr_dist_replay_deaths(vr_plan* plan, int32_t d);
-int vr_dist_copy_keys_async(vr_plan* plan, int32_t d, uint64_t* dst_device);
 int64_t vr_plan_launches(const vr_plan* plan); /* kernels launched through this plan so far */
+
+/* ----------------------------------------------------------------------------------
+ * Multi-GPU (the a7 exchange).  The distance matrix is replicated; the
+ * rows of every dimension are sharded over the ranks (dense prefix rows and sparse vertex
+ * rows interleaved; sparse rows of higher dimensions are each rank's own survivors of a lower
+ * dimension, which partitions the simplices — Cor 5.3.7: columns are
+ * independent).  Per dimension, inside the library:
+ *   A. the next dimension's clearing input: SUM all-reduce of the clearing bitmap (every
+ *      death bit is set by exactly one rank, so the sum is the OR), or, for the hash-set
+ *      clearing of the output-sensitive mode, an all-gather of every rank's apparent
+ *      cofacets, inserted into each rank's set;
+ *   B. the residual columns: all-gather of the locally sorted keys (padded to the largest
+ *      count with ~0) and a device merge (every key's output position = its index + the
+ *      number of smaller keys in every other rank's list, by binary search);
+ *   C. rank 0 runs the host residual on the merged columns and broadcasts the deaths,
+ *      which every rank turns into the next dimension's clearing input.
+ * At the end rank 0 broadcasts the barcode (pairs + index pairs) and the counters are
+ * summed, so every rank returns the same vr_result, byte-identical to the one-GPU result.
+ *
+ * The transport is a vr_comm: three collectives on DEVICE buffers, ordered on `stream`
+ * (the caller's stream of that rank); each returns 0 or a VR_E* code.  The library
+ * provides NCCL communicators (one process per GPU: vr_comm_nccl with an id from
+ * vr_nccl_unique_id shared by any out-of-band channel, e.g. torch.distributed; one process
+ * driving several GPUs: vr_options.num_gpus in vr_barcodes) and an in-process group whose
+ * ranks are host threads sharing one GPU (vr_comm_local: tests of the multi-rank logic on
+ * one device; the collectives stage through host memory, no kernel waits on another).
+ * ---------------------------------------------------------------------------------- */
+typedef struct vr_comm {
+  void* ctx;
+  int32_t rank, world;
+  int (*allreduce_sum_u64)(void* ctx, uint64_t* buf, int64_t n, void* stream);          /* in place */
+  int (*allgather_u64)(void* ctx, const uint64_t* send, uint64_t* recv, int64_t n_each, void* stream);
+  int (*broadcast_u64)(void* ctx, uint64_t* buf, int64_t n, int32_t root, void* stream); /* in place */
+  void (*destroy)(void* ctx);
+} vr_comm;
+
+/* a fresh NCCL unique id (128 bytes) for vr_comm_nccl (call on one rank, share the bytes) */
+int vr_nccl_unique_id(uint8_t id[128]);
+/* this process's rank of an NCCL communicator over `world` ranks on CUDA device `device` */
+int vr_comm_nccl(const uint8_t id[128], int32_t rank, int32_t world, int32_t device, vr_comm** out);
+/* `world` ranks in this process sharing the current device (each rank is run by its own
+ * host thread); comms[r] is rank r's communicator */
+int vr_comm_local(int32_t world, vr_comm** comms);
+void vr_comm_free(vr_comm* c);
+
+/* This rank's part of a distributed computation: every rank calls it with the same input
+ * (host pointer, copied to the rank's current device), the same options and its own
+ * communicator; all ranks return the same result.  Collective: blocks until every rank has
+ * called it. */
+int vr_barcodes_comm(const float* dist_lower_tri, int64_t n, int32_t max_dim, float threshold, const vr_options* opt,
+                     const vr_comm* comm, vr_result** out);
+/* The same from a device matrix on the current device and `stream`, keeping a plan whose
+ * vr_plan_replay re-runs the sharded hot path with exchanges A and B (bench.py's timed
+ * multi-GPU step); *out (may be NULL) receives the result. */
+int vr_plan_create_comm(const float* d_dist_lower_tri, int64_t n, int32_t max_dim, float threshold, const vr_options* opt,
+                        const vr_comm* comm, void* stream, vr_plan** plan, vr_result** out);
 
 /* ----------------------------------------------------------------------------------
  * Component entry (tests, no GPU needed): the library's host residual reduction of

@@ -46,7 +46,8 @@ class _IndexPair(ctypes.Structure):
 class _Options(ctypes.Structure):
     _fields_ = [("include_zero", ctypes.c_int32), ("index_pairs", ctypes.c_int32), ("residual_mode", ctypes.c_int32),
                 ("apparent_steps", ctypes.c_int32), ("device", ctypes.c_int32), ("rows_per_grab", ctypes.c_int32),
-                ("scan_variant", ctypes.c_int32), ("sparse_mode", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
+                ("scan_variant", ctypes.c_int32), ("sparse_mode", ctypes.c_int32), ("num_gpus", ctypes.c_int32),
+                ("hot_path_only", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
 
 
 _STAT_FIELDS = ["candidates", "survivors", "apparent", "cleared", "residual_columns", "emergent", "pairs_all",
@@ -74,6 +75,16 @@ def load() -> ctypes.CDLL:
     if not os.path.exists(lib_path):
         raise ImportError(f"libvr.so not found at {lib_path}: run `python paper_2502_05063_b200/build.py` "
                           "(there is no CPU fallback for the hot path)")
+    if "VR_NCCL_LIB" not in os.environ:  # the NCCL torch uses (libvr loads it at the first communicator)
+        try:
+            import nvidia.nccl
+            for d in nvidia.nccl.__path__:
+                cand = os.path.join(d, "lib", "libnccl.so.2")
+                if os.path.exists(cand):
+                    os.environ["VR_NCCL_LIB"] = cand
+                    break
+        except ImportError:
+            pass
     lib = ctypes.CDLL(lib_path)
     vp, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
     sig = {
@@ -105,17 +116,12 @@ def load() -> ctypes.CDLL:
         "vr_w1_net_arcs": (i64, [vp]),
         "vr_w1_net_get": (None, [vp, vp, vp, vp, vp, vp]),
         "vr_w1_net_free": (None, [vp]),
-        "vr_dist_begin": (ctypes.c_int, [vp, i64, i32, f32, vp, vp, i32, i32, ctypes.POINTER(vp)]),
-        "vr_dist_dim_local": (ctypes.c_int, [vp, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
-        "vr_dist_copy_keys": (ctypes.c_int, [vp, i32, vp]),
-        "vr_dist_bitmap": (ctypes.c_int, [vp, i32, vp, i32]),
-        "vr_dist_counters": (ctypes.c_int, [vp, i32, ctypes.POINTER(i64)]),
-        "vr_dist_dim_finish": (ctypes.c_int, [vp, i32, vp, i64]),
-        "vr_dist_end": (ctypes.c_int, [vp, ctypes.POINTER(vp)]),
-        "vr_dist_replay_tables": (ctypes.c_int, [vp]),
-        "vr_dist_replay_dim": (ctypes.c_int, [vp, i32]),
-        "vr_dist_replay_deaths": (ctypes.c_int, [vp, i32]),
-        "vr_dist_copy_keys_async": (ctypes.c_int, [vp, i32, vp]),
+        "vr_nccl_unique_id": (ctypes.c_int, [vp]),
+        "vr_comm_nccl": (ctypes.c_int, [vp, i32, i32, i32, ctypes.POINTER(vp)]),
+        "vr_comm_local": (ctypes.c_int, [i32, vp]),
+        "vr_comm_free": (None, [vp]),
+        "vr_barcodes_comm": (ctypes.c_int, [vp, i64, i32, f32, vp, vp, ctypes.POINTER(vp)]),
+        "vr_plan_create_comm": (ctypes.c_int, [vp, i64, i32, f32, vp, vp, vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]),
         "vr_plan_launches": (i64, [vp]),
         "vr_probe_peaks": (ctypes.c_int, [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
         "vr_host_residual": (ctypes.c_int, [vp, vp, i64, i64, i32, ctypes.c_uint32, i32, vp, i64, i32, vp, vp, vp, vp,
@@ -135,8 +141,9 @@ def _check(rc: int):
 
 
 def _options(include_zero=False, index_pairs=False, residual_mode=0, apparent_steps=0, device=0, rows_per_grab=0,
-             scan_variant=0, sparse_mode=0) -> _Options:
+             scan_variant=0, sparse_mode=0, num_gpus=0, hot_path_only=False) -> _Options:
     o = _Options()
+    o.num_gpus, o.hot_path_only = int(num_gpus), int(hot_path_only)
     o.include_zero, o.index_pairs, o.residual_mode = int(include_zero), int(index_pairs), int(residual_mode)
     o.apparent_steps, o.device = int(apparent_steps), int(device)
     o.rows_per_grab, o.scan_variant, o.sparse_mode = int(rows_per_grab), int(scan_variant), int(sparse_mode)
@@ -379,14 +386,21 @@ class Plan:
     """vr_plan: one full run, then `replay()` re-launches the GPU hot path of every
     dimension (a0..a6) with the recorded sizes, asynchronously on `stream`."""
 
-    def __init__(self, d_dist_lower_tri, n: int, max_dim: int, threshold: float = math.inf, stream=None, **opts):
+    def __init__(self, d_dist_lower_tri, n: int, max_dim: int, threshold: float = math.inf, stream=None, comm=None,
+                 **opts):
+        """comm: a dist.Comm — this rank's part of a sharded plan (vr_plan_create_comm)."""
         lib = load()
-        self._keep = d_dist_lower_tri
+        self._keep = (d_dist_lower_tri, comm)
         ptr, st = _device_ptr_and_stream(d_dist_lower_tri, n, stream)
         self._h = ctypes.c_void_p()
         r = ctypes.c_void_p()
         o = _options(**opts)
-        _check(lib.vr_plan_create(ptr, n, max_dim, threshold, ctypes.byref(o), st, ctypes.byref(self._h), ctypes.byref(r)))
+        if comm is None:
+            _check(lib.vr_plan_create(ptr, n, max_dim, threshold, ctypes.byref(o), st, ctypes.byref(self._h),
+                                      ctypes.byref(r)))
+        else:
+            _check(lib.vr_plan_create_comm(ptr, n, max_dim, threshold, ctypes.byref(o), comm.ptr, st,
+                                           ctypes.byref(self._h), ctypes.byref(r)))
         try:
             self.result = _collect(r)
         finally:

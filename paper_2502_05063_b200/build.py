@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvr.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["vr_api.cu", "tables.cu", "sort.cu", "hotpath.cu", "sparse.cu", "hypha.cu", "hypha_host.cpp", "netsimplex.cpp", "w1.cu", "host.cpp", "probe.cu"]
+SOURCES = ["vr_api.cu", "tables.cu", "sort.cu", "hotpath.cu", "sparse.cu", "hypha.cu", "hypha_host.cpp", "netsimplex.cpp", "w1.cu", "host.cpp", "probe.cu", "comm.cu"]
 HEADERS = ["vr_common.cuh", "vr_internal.h", "vr_types.h"]
 
 FLAGS = [
@@ -37,7 +37,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     srcs = [os.path.join(CSRC, f) for f in SOURCES]
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(HERE, "..", "include"), "-o", tmp, *srcs]
+    cmd = [NVCC, *FLAGS, "-I", os.path.join(HERE, "..", "include"), "-o", tmp, *srcs, "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

@@ -15,6 +15,7 @@
 //               coalesced runs written to the digit's global offset (reads 8 + writes 8 B/key)
 // Stability: inside a tile order is (digit, position); across tiles the digit-major scan
 // orders tiles — so each pass is a stable counting sort, as LSD requires.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstdint>
@@ -636,6 +637,39 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit,
     uint64_t* t = src; src = dst; dst = t;
   }
   return src;
+}
+
+// ------------------------------------------------------------------ k-way merge (a7)
+// Every key's output position = its index in its own list + the number of smaller keys in
+// each other list (binary search; keys are distinct, so positions are distinct) — the
+// merge path of each element computed directly, no sequential cursor.
+__global__ void k_merge_gathered(const uint64_t* __restrict__ g, int world, uint64_t cap, uint64_t* __restrict__ out) {
+  const uint64_t total = (uint64_t)world * cap;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = __ldg(g + e);
+    if (x == ~0ull) continue;
+    const int r = (int)(e / cap);
+    uint64_t pos = e - (uint64_t)r * cap;
+    for (int h = 0; h < world; ++h) {
+      if (h == r) continue;
+      const uint64_t* L = g + (uint64_t)h * cap;
+      uint64_t lo = 0, hi = cap;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (__ldg(L + mid) < x) lo = mid + 1; else hi = mid;
+      }
+      pos += lo;
+    }
+    out[pos] = x;
+  }
+}
+
+void merge_gathered_u64(const uint64_t* gathered, int world, uint64_t cap, uint64_t* out, cudaStream_t st, int64_t* launches) {
+  const uint64_t total = (uint64_t)world * cap;
+  if (!total) return;
+  const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, 148ull * 8);
+  k_merge_gathered<<<(unsigned)blocks, 256, 0, st>>>(gathered, world, cap, out);
+  if (launches) *launches += 1;
 }
 
 }  // namespace vr

@@ -276,6 +276,10 @@ __device__ __forceinline__ void survivor_tail(const Tables& T, const DimParams& 
     const uint64_t tc = cofacet_cidx<D>(T, s, hitv);
     if (B.clr_next) bit_set(B.clr_next, tc);
     if (B.clr_next_set.table) set_put(B.clr_next_set, tc);
+    if (B.exp_list) {  // sharded: the other ranks' sets receive it too (exchange A)
+      const unsigned long long slot = atomicAdd(&B.ctr->exported, 1ull);
+      if (slot < B.exp_cap) B.exp_list[slot] = tc;
+    }
     if (B.app_pairs) {
       const unsigned long long slot = atomicAdd(&B.ctr->app_pairs, 1ull);
       if (slot < B.app_cap) {
@@ -846,8 +850,10 @@ __global__ void __launch_bounds__(SP_THREADS) k_resolve_sparse(Tables T, DimPara
 }
 
 __global__ void k_set_put(const uint64_t* __restrict__ list, int64_t m, ClearSet c) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-    set_put(c, __ldg(list + i));
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = __ldg(list + i);
+    if (k != ~0ull) set_put(c, k);  // ~0: the padding of a gathered list
+  }
 }
 
 // ------------------------------------------------------------------ launchers

@@ -20,6 +20,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -226,6 +227,10 @@ struct DimRun {
   uint64_t hash_mask = 0;  // slots - 1; 0 = no set (recompute mode)
   uint32_t bloom_words = 0;
   bool two_level = false;  // sparse: k_enum_sparse2 (rows = survivors of d-2)
+  // sharded runs (recorded by the first run, reused by replays): the largest per-rank count
+  // of residual keys and of exported apparent cofacets, this rank's exported count, the sum
+  std::vector<uint64_t> x_counts;
+  uint64_t x_cap = 0, x_total = 0, exp_cap = 0, exp_local = 0;
   // algorithmic work of the first run: rank reads of
   // the enumeration (a1) and of the apparent test (a5, both phases), decode compares
   double reads_a1 = 0, reads_a5 = 0, reads_a5_phase2 = 0, decode = 0, decode_phase2 = 0;
@@ -252,6 +257,8 @@ struct vr_plan {
   cudaEvent_t ev[8] = {};
   uint64_t* local_sorted = nullptr;  // this rank's sorted residual keys of the last dimension run
   int32_t rank_id = 0, world = 1;    // shard of the rows (distributed driver)
+  const vr_comm* comm = nullptr;     // the ranks' transport (world > 1)
+  DevBuf x_counts, x_send, x_gather, x_merged, x_exp, x_expg, x_ser;  // exchange buffers
   int64_t n = 0;
   int32_t D = 0;
   float threshold = 0.0f;
@@ -306,6 +313,9 @@ struct vr_plan {
   void hash_fields(vr::HotBuffers& B, int d) {
     B.clr_set = set_of(d);
     B.clr_next_set = set_of(d + 1);
+    // sharded: the apparent cofacets also go to the export list for the other ranks' sets
+    B.exp_list = (world > 1 && B.clr_next_set.table) ? x_exp.as<uint64_t>() : nullptr;
+    B.exp_cap = B.exp_list ? x_exp.bytes / 8 : 0;
   }
   // (the table is sized by the row bound, 2x rounded up to a power of two: most probes are
   // misses, and a low load keeps the few that reach it at one slot)
@@ -418,6 +428,41 @@ struct SectionTimer {
 // stage_result       barcode assembly
 // A single-GPU run calls them in sequence; the distributed driver (paper_2502_05063_b200/
 // dist.py) interleaves the two exchanges of SURVEY.md §8(e) between local and finish.
+// ------------------------------------------------------------------ collectives (sharded runs)
+void comm_ok(int rc, const char* what) {
+  if (rc) throw VrError(rc, std::string(what) + ": " + g_err);
+}
+// every rank's value v (host), in rank order
+std::vector<uint64_t> gather_u64(vr_plan& P, uint64_t v) {
+  const int W = P.world;
+  P.x_counts.ensure((size_t)(W + 1) * 8);
+  uint64_t* d = P.x_counts.as<uint64_t>();
+  CUDA_TRY(cudaMemcpyAsync(d, &v, 8, cudaMemcpyHostToDevice, P.st));
+  comm_ok(P.comm->allgather_u64(P.comm->ctx, d, d + 1, 1, P.st), "all-gather (counts)");
+  std::vector<uint64_t> all((size_t)W);
+  CUDA_TRY(cudaMemcpyAsync(all.data(), d + 1, (size_t)W * 8, cudaMemcpyDeviceToHost, P.st));
+  CUDA_TRY(cudaStreamSynchronize(P.st));
+  return all;
+}
+// rank 0's host words to every rank (the count first)
+void bcast_words(vr_plan& P, std::vector<uint64_t>& w) {
+  P.x_counts.ensure((size_t)(P.world + 1) * 8);
+  uint64_t* c = P.x_counts.as<uint64_t>();
+  uint64_t n = w.size();
+  CUDA_TRY(cudaMemcpyAsync(c, &n, 8, cudaMemcpyHostToDevice, P.st));
+  comm_ok(P.comm->broadcast_u64(P.comm->ctx, c, 1, 0, P.st), "broadcast (count)");
+  CUDA_TRY(cudaMemcpyAsync(&n, c, 8, cudaMemcpyDeviceToHost, P.st));
+  CUDA_TRY(cudaStreamSynchronize(P.st));
+  if (P.rank_id != 0) w.assign((size_t)n, 0);
+  if (!n) return;
+  P.x_ser.ensure((size_t)n * 8);
+  uint64_t* b = P.x_ser.as<uint64_t>();
+  if (P.rank_id == 0) CUDA_TRY(cudaMemcpyAsync(b, w.data(), (size_t)n * 8, cudaMemcpyHostToDevice, P.st));
+  comm_ok(P.comm->broadcast_u64(P.comm->ctx, b, (int64_t)n, 0, P.st), "broadcast");
+  if (P.rank_id != 0) CUDA_TRY(cudaMemcpyAsync(w.data(), b, (size_t)n * 8, cudaMemcpyDeviceToHost, P.st));
+  CUDA_TRY(cudaStreamSynchronize(P.st));
+}
+
 void stage_setup(vr_plan& P) {
   SectionTimer ST;
   vr_result* R = P.R.get();
@@ -572,7 +617,7 @@ void stage_setup(vr_plan& P) {
   for (int d = 2; d <= D; ++d) P.dims[(size_t)d].two_level = P.sparse && !std::getenv("VR_SPARSE_1LEVEL");
   CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
   // (tests: VR_FORCE_CLEAR_HASH puts sparse dimensions >= 2 on the hash-set path)
-  const bool force_hash = P.sparse && P.world == 1 && std::getenv("VR_FORCE_CLEAR_HASH") != nullptr;
+  const bool force_hash = P.sparse && std::getenv("VR_FORCE_CLEAR_HASH") != nullptr;
   for (int d = 1; d <= D; ++d) {
     const uint64_t cand = binom_host((uint64_t)n, (uint64_t)d + 1);
     const size_t words = (size_t)((cand + 31) / 32);
@@ -580,10 +625,12 @@ void stage_setup(vr_plan& P) {
     // output-sensitive mode on one GPU: a bitmap only while it stays small (its bits are
     // probed at random); beyond that the hash set of the pivots is smaller and L2-friendlier
     // (config 5: 1 MiB at dimension 1; 1.4 GiB at dimension 2 -> hash set)
-    if (P.sparse && P.world == 1 && d >= 2 && words * 4 > kSparseBitmapBytes) continue;
-    if (cand && P.m && words * 4 <= kMaxBitmapBytes && words * 4 <= free_b / 16) {
-      P.dims[(size_t)d].clr.ensure(words * 4);
-      P.dims[(size_t)d].clr_words = words;
+    if (P.sparse && d >= 2 && words * 4 > kSparseBitmapBytes) continue;
+    // (total, not free, memory: the decision must be the same on every rank)
+    if (cand && P.m && words * 4 <= kMaxBitmapBytes && words * 4 <= total_b / 16) {
+      const size_t w2 = (words + 1) & ~(size_t)1;  // even: summed as 64-bit words when sharded
+      P.dims[(size_t)d].clr.ensure(w2 * 4);
+      P.dims[(size_t)d].clr_words = w2;
     }
   }
   // deaths of dimension 0 -> clearing input of dimension 1
@@ -664,15 +711,23 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
   // pivots of this dimension (apparent cofacets + residual deaths, at most `bound`) go into a
   // hash set that dimension d+1 probes in phase 1 — instead of queueing every non-apparent
   // column for the phase-2 recomputation
-  if (P.sparse && P.world == 1 && d < D && !P.clr_of(d + 1) && !std::getenv("VR_NO_CLEAR_HASH")) {
+  if (P.sparse && d < D && !P.clr_of(d + 1) && !std::getenv("VR_NO_CLEAR_HASH")) {
     DimRun& nx = P.dims[(size_t)d + 1];
+    // sharded: every rank's set receives every rank's pivots — sized by the global bound
+    uint64_t gbound = bound;
+    if (P.world > 1) {
+      gbound = 0;
+      for (uint64_t b : gather_u64(P, bound)) gbound += b;
+      P.x_exp.ensure(std::max<uint64_t>(bound, 1) * 8);  // this rank's apparent cofacets
+    }
     uint64_t slots = 1024;
-    while (slots < 2 * std::max<uint64_t>(bound, 1) + 1024) slots <<= 1;
+    while (slots < 2 * std::max<uint64_t>(gbound, 1) + 1024) slots <<= 1;
     size_t fb = 0, tb = 0;
     CUDA_TRY(cudaMemGetInfo(&fb, &tb));
+    fb = tb;  // (the same decision on every rank)
     // Bloom filter: 16 bits per bounding key (3 bits set per key: ~0.1% false positives at
     // the pivots actually inserted)
-    const uint64_t bw = std::min<uint64_t>(std::max<uint64_t>(bound / 2, 1024), (uint64_t)UINT32_MAX);
+    const uint64_t bw = std::min<uint64_t>(std::max<uint64_t>(gbound / 2, 1024), (uint64_t)UINT32_MAX);
     if (slots * 8 + bw * 4 <= fb / 8) {
       nx.hash.ensure(slots * 8);
       nx.hash_mask = slots - 1;
@@ -843,13 +898,28 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
   return resid_count;
 }
 
+// The deaths of dimension d (P.deaths, sorted) -> the clearing input of dimension d+1:
+// the device death list, its bits in d+1's bitmap or its keys in d+1's clearing set.
+void apply_deaths(vr_plan& P, int d) {
+  if (d >= P.D) return;
+  auto tx = std::chrono::steady_clock::now();
+  cudaStream_t st = P.st;
+  DimRun& nx = P.dims[(size_t)d + 1];
+  nx.ndeaths_in = (int64_t)P.deaths.size();
+  nx.deaths_in.ensure(std::max<size_t>(P.deaths.size(), 1) * 8);
+  if (!P.deaths.empty())
+    CUDA_TRY(cudaMemcpyAsync(nx.deaths_in.p, P.deaths.data(), P.deaths.size() * 8, cudaMemcpyHostToDevice, st));
+  if (P.clr_of(d + 1)) vr::launch_set_bits(nx.deaths_in.as<uint64_t>(), nx.ndeaths_in, P.clr_of(d + 1), st, &P.launches);
+  P.hash_deaths(d + 1, st);
+  P.R->stats[(size_t)d].ms_transfer += ms_since(tx);
+}
+
 // Host residual of dimension d on the sorted residual columns (all ranks' columns when
 // distributed); deaths -> the clearing input of dimension d+1.
 void stage_dim_finish(vr_plan& P, int d, const uint64_t* keys, uint64_t nkeys) {
   SectionTimer ST;
   vr_result* R = P.R.get();
   const int D = P.D;
-  cudaStream_t st = P.st;
   DimRun& dr = P.dims[(size_t)d];
   vr_stats& stt = R->stats[(size_t)d];
   if (!dr.active) {
@@ -868,18 +938,7 @@ void stage_dim_finish(vr_plan& P, int d, const uint64_t* keys, uint64_t nkeys) {
     std::vector<uint64_t> kv(keys, keys + nkeys);
     dump_residual(dump, P.M, d, P.maxr, dr.p.cbits, kv);
   }
-  // deaths of dimension d -> clearing input of dimension d+1
-  if (d < D) {
-    auto tx = std::chrono::steady_clock::now();
-    DimRun& nx = P.dims[(size_t)d + 1];
-    nx.ndeaths_in = (int64_t)P.deaths.size();
-    nx.deaths_in.ensure(std::max<size_t>(P.deaths.size(), 1) * 8);
-    if (!P.deaths.empty())
-      CUDA_TRY(cudaMemcpyAsync(nx.deaths_in.p, P.deaths.data(), P.deaths.size() * 8, cudaMemcpyHostToDevice, st));
-    if (P.clr_of(d + 1)) vr::launch_set_bits(nx.deaths_in.as<uint64_t>(), nx.ndeaths_in, P.clr_of(d + 1), st, &P.launches);
-    P.hash_deaths(d + 1, st);
-    stt.ms_transfer += ms_since(tx);
-  }
+  apply_deaths(P, d);
   stt.residual_columns = (int64_t)nkeys;
   stt.emergent = rst.emergent;
   P.residual_total += (int64_t)nkeys;
@@ -910,10 +969,210 @@ void stage_result(vr_plan& P) {
   }
 }
 
-void run_full(vr_plan& P) {
+// Exchange A of a sharded dimension d (include/vr.h "Multi-GPU"): the clearing input of
+// d+1 from every rank — the SUM all-reduce of the bitmap (disjoint bits, reading R3), or
+// the all-gather of every rank's apparent cofacets into each rank's clearing set.
+// `replay`: the counts are the first run's (no host synchronisation).
+void exchange_clearing(vr_plan& P, int d, bool replay) {
+  if (P.world == 1 || d >= P.D) return;
+  DimRun& dr = P.dims[(size_t)d];
+  cudaStream_t st = P.st;
+  if (uint32_t* bm = P.clr_of(d + 1)) {
+    comm_ok(P.comm->allreduce_sum_u64(P.comm->ctx, (uint64_t*)bm, (int64_t)(P.dims[(size_t)d + 1].clr_words / 2), st),
+            "all-reduce (clearing bitmap)");
+    return;
+  }
+  const vr::ClearSet c = P.set_of(d + 1);
+  if (!c.table) return;
+  if (!replay) {
+    vr::DimCounters hc{};
+    CUDA_TRY(cudaMemcpyAsync(&hc, P.ctrs.as<vr::DimCounters>() + d, sizeof hc, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (hc.exported * 8 > P.x_exp.bytes) throw VrError(VR_ECAPACITY, "export list overflow");
+    dr.exp_local = hc.exported;
+    dr.exp_cap = 0;
+    for (uint64_t v : gather_u64(P, dr.exp_local)) dr.exp_cap = std::max(dr.exp_cap, v);
+  }
+  if (!dr.exp_cap) return;
+  P.x_exp.ensure((size_t)dr.exp_cap * 8);
+  uint64_t* L = P.x_exp.as<uint64_t>();
+  if (dr.exp_cap > dr.exp_local) CUDA_TRY(cudaMemsetAsync(L + dr.exp_local, 0xFF, (dr.exp_cap - dr.exp_local) * 8, st));
+  P.x_expg.ensure((size_t)P.world * dr.exp_cap * 8);
+  comm_ok(P.comm->allgather_u64(P.comm->ctx, L, P.x_expg.as<uint64_t>(), (int64_t)dr.exp_cap, st),
+          "all-gather (apparent cofacets)");
+  vr::launch_set_put(P.x_expg.as<uint64_t>(), (int64_t)(P.world * dr.exp_cap), c, st, &P.launches);
+}
+
+// Exchange B: every rank's sorted residual keys of dimension d, all-gathered (padded with ~0
+// to the largest count) and merged on the device into P.x_merged; returns the total.
+uint64_t exchange_residual(vr_plan& P, int d, uint64_t nk_local, bool replay) {
+  DimRun& dr = P.dims[(size_t)d];
+  if (P.world == 1) return nk_local;
+  cudaStream_t st = P.st;
+  if (!replay) {
+    dr.x_counts = gather_u64(P, nk_local);
+    dr.x_cap = 0;
+    dr.x_total = 0;
+    for (uint64_t v : dr.x_counts) {
+      dr.x_cap = std::max(dr.x_cap, v);
+      dr.x_total += v;
+    }
+  }
+  if (!dr.x_total) return 0;
+  P.x_send.ensure((size_t)dr.x_cap * 8);
+  uint64_t* snd = P.x_send.as<uint64_t>();
+  if (dr.x_cap > nk_local) CUDA_TRY(cudaMemsetAsync(snd + nk_local, 0xFF, (dr.x_cap - nk_local) * 8, st));
+  if (nk_local) CUDA_TRY(cudaMemcpyAsync(snd, P.local_sorted, nk_local * 8, cudaMemcpyDeviceToDevice, st));
+  P.x_gather.ensure((size_t)P.world * dr.x_cap * 8);
+  comm_ok(P.comm->allgather_u64(P.comm->ctx, snd, P.x_gather.as<uint64_t>(), (int64_t)dr.x_cap, st),
+          "all-gather (residual keys)");
+  P.x_merged.ensure((size_t)dr.x_total * 8);
+  vr::merge_gathered_u64(P.x_gather.as<uint64_t>(), P.world, dr.x_cap, P.x_merged.as<uint64_t>(), st, &P.launches);
+  return dr.x_total;
+}
+
+// The apparent index pairs of dimension d (debug output) from every rank to rank 0.
+void gather_index_pairs(vr_plan& P, int d) {
+  auto& ip = P.R->ipairs[(size_t)d];
+  std::vector<uint64_t> counts = gather_u64(P, ip.size());
+  uint64_t cap = 0;
+  for (uint64_t v : counts) cap = std::max(cap, v);
+  if (!cap) return;
+  std::vector<uint64_t> mine((size_t)cap * 2, ~0ull);
+  for (size_t i = 0; i < ip.size(); ++i) { mine[2 * i] = ip[i].birth_cidx; mine[2 * i + 1] = ip[i].death_cidx; }
+  P.x_send.ensure((size_t)cap * 16);
+  P.x_gather.ensure((size_t)P.world * cap * 16);
+  CUDA_TRY(cudaMemcpyAsync(P.x_send.p, mine.data(), (size_t)cap * 16, cudaMemcpyHostToDevice, P.st));
+  comm_ok(P.comm->allgather_u64(P.comm->ctx, P.x_send.as<uint64_t>(), P.x_gather.as<uint64_t>(), (int64_t)cap * 2, P.st),
+          "all-gather (index pairs)");
+  std::vector<uint64_t> all((size_t)P.world * cap * 2);
+  CUDA_TRY(cudaMemcpyAsync(all.data(), P.x_gather.p, all.size() * 8, cudaMemcpyDeviceToHost, P.st));
+  CUDA_TRY(cudaStreamSynchronize(P.st));
+  ip.clear();
+  for (size_t i = 0; i + 1 < all.size(); i += 2)
+    if (all[i] != ~0ull) ip.push_back(vr_index_pair{all[i], all[i + 1]});
+}
+
+// Rank 0's result to every rank: stats, pairs and index pairs of every dimension, and the
+// threshold applied, serialised as 64-bit words.
+void bcast_result(vr_plan& P) {
+  vr_result* R = P.R.get();
+  const size_t sw = (sizeof(vr_stats) + 7) / 8;
+  std::vector<uint64_t> w;
+  if (P.rank_id == 0) {
+    uint32_t tb;
+    std::memcpy(&tb, &R->tused, 4);
+    w.push_back(tb);
+    for (int d = 0; d <= P.D; ++d) {
+      const size_t o = w.size();
+      w.resize(o + sw, 0);
+      std::memcpy(&w[o], &R->stats[(size_t)d], sizeof(vr_stats));
+      w.push_back(R->pairs[(size_t)d].size());
+      for (const vr_pair& q : R->pairs[(size_t)d]) {
+        uint32_t b, e;
+        std::memcpy(&b, &q.birth, 4);
+        std::memcpy(&e, &q.death, 4);
+        w.push_back((uint64_t)b | ((uint64_t)e << 32));
+      }
+      w.push_back(R->ipairs[(size_t)d].size());
+      for (const vr_index_pair& q : R->ipairs[(size_t)d]) { w.push_back(q.birth_cidx); w.push_back(q.death_cidx); }
+    }
+  }
+  bcast_words(P, w);
+  if (P.rank_id == 0) return;
+  size_t k = 0;
+  const uint32_t tb = (uint32_t)w[k++];
+  std::memcpy(&R->tused, &tb, 4);
+  for (int d = 0; d <= P.D; ++d) {
+    std::memcpy(&R->stats[(size_t)d], &w[k], sizeof(vr_stats));
+    k += sw;
+    const uint64_t np = w[k++];
+    R->pairs[(size_t)d].resize((size_t)np);
+    for (uint64_t i = 0; i < np; ++i, ++k) {
+      const uint32_t b = (uint32_t)w[k], e = (uint32_t)(w[k] >> 32);
+      std::memcpy(&R->pairs[(size_t)d][(size_t)i].birth, &b, 4);
+      std::memcpy(&R->pairs[(size_t)d][(size_t)i].death, &e, 4);
+    }
+    const uint64_t ni = w[k++];
+    R->ipairs[(size_t)d].resize((size_t)ni);
+    for (uint64_t i = 0; i < ni; ++i, k += 2) R->ipairs[(size_t)d][(size_t)i] = vr_index_pair{w[k], w[k + 1]};
+  }
+}
+
+// A sharded run (P.comm, world > 1): every rank runs its shard of each dimension's hot path,
+// exchanges A and B, rank 0 the host residual and the deaths go to every rank (exchange C);
+// at the end the counters are summed and rank 0's result is broadcast.
+void run_distributed(vr_plan& P) {
   stage_setup(P);
   for (int d = 1; d <= P.D; ++d) {
     const uint64_t nk = stage_dim_local(P, d);
+    const bool active = P.dims[(size_t)d].active;
+    if (active) {
+      exchange_clearing(P, d, false);
+      if (P.opt.index_pairs) gather_index_pairs(P, d);
+    }
+    const uint64_t total = active ? exchange_residual(P, d, nk, false) : 0;
+    if (P.rank_id == 0) {
+      std::vector<uint64_t> hkeys((size_t)total);
+      auto tx = std::chrono::steady_clock::now();
+      if (total) CUDA_TRY(cudaMemcpy(hkeys.data(), P.x_merged.p, total * 8, cudaMemcpyDeviceToHost));
+      P.R->stats[(size_t)d].ms_transfer += ms_since(tx);
+      stage_dim_finish(P, d, hkeys.data(), total);
+    }
+    // exchange C: rank 0's deaths of dimension d to every rank
+    std::vector<uint64_t> deaths;
+    if (P.rank_id == 0) deaths = P.deaths;
+    bcast_words(P, deaths);
+    if (P.rank_id != 0) {
+      P.deaths = deaths;
+      if (active) apply_deaths(P, d);
+      else if (d < P.D) P.dims[(size_t)d + 1].ndeaths_in = 0;
+      P.R->stats[(size_t)d].residual_columns = (int64_t)total;
+      P.residual_total += (int64_t)total;
+    }
+  }
+  // the counters the ranks accumulated locally, summed
+  std::vector<uint64_t> c((size_t)(P.D + 1) * 5, 0);
+  for (int d = 1; d <= P.D; ++d) {
+    const vr_stats& s = P.R->stats[(size_t)d];
+    uint64_t* q = &c[(size_t)d * 5];
+    q[0] = (uint64_t)s.survivors; q[1] = (uint64_t)s.apparent; q[2] = (uint64_t)s.cleared; q[3] = (uint64_t)s.queued;
+    q[4] = (uint64_t)s.scanned;
+  }
+  P.x_ser.ensure(c.size() * 8);
+  CUDA_TRY(cudaMemcpyAsync(P.x_ser.p, c.data(), c.size() * 8, cudaMemcpyHostToDevice, P.st));
+  comm_ok(P.comm->allreduce_sum_u64(P.comm->ctx, P.x_ser.as<uint64_t>(), (int64_t)c.size(), P.st), "all-reduce (counters)");
+  CUDA_TRY(cudaMemcpyAsync(c.data(), P.x_ser.p, c.size() * 8, cudaMemcpyDeviceToHost, P.st));
+  CUDA_TRY(cudaStreamSynchronize(P.st));
+  P.survivors_total = P.apparent_total = 0;
+  for (int d = 1; d <= P.D; ++d) {
+    vr_stats& s = P.R->stats[(size_t)d];
+    const uint64_t* q = &c[(size_t)d * 5];
+    s.survivors = (int64_t)q[0]; s.apparent = (int64_t)q[1]; s.cleared = (int64_t)q[2]; s.queued = (int64_t)q[3];
+    s.scanned = (int64_t)q[4];
+    P.survivors_total += s.survivors;
+    P.apparent_total += s.apparent;
+  }
+  if (P.rank_id == 0) stage_result(P);
+  bcast_result(P);
+}
+
+void run_full(vr_plan& P) {
+  if (P.comm && P.world > 1) {
+    run_distributed(P);
+    return;
+  }
+  stage_setup(P);
+  for (int d = 1; d <= P.D; ++d) {
+    const uint64_t nk = stage_dim_local(P, d);
+    if (P.opt.hot_path_only) {  // diagnostics: no host residual, no deaths
+      P.R->stats[(size_t)d].residual_columns = (int64_t)nk;
+      P.residual_total += (int64_t)nk;
+      P.deaths.clear();
+      if (P.dims[(size_t)d].active) apply_deaths(P, d);
+      else if (d < P.D) P.dims[(size_t)d + 1].ndeaths_in = 0;
+      continue;
+    }
     std::vector<uint64_t> hkeys((size_t)nk);
     auto tx = std::chrono::steady_clock::now();
     if (nk) CUDA_TRY(cudaMemcpy(hkeys.data(), P.local_sorted, nk * 8, cudaMemcpyDeviceToHost));
@@ -995,10 +1254,17 @@ void replay(vr_plan& P) {
       else vr::launch_resolve(p, P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), P.kmax, B, c.queued, st, &P.launches);
       cudaEventRecord(e3.second, st);
     }
+    if (P.world > 1) {  // exchange A (timed with the enumeration stage)
+      auto& ex = ev(1);
+      cudaEventRecord(ex.first, st);
+      exchange_clearing(P, d, true);
+      cudaEventRecord(ex.second, st);
+    }
     auto& e4 = ev(3);
     cudaEventRecord(e4.first, st);
-    vr::radix_sort_u64(P.resid.as<uint64_t>(), P.resid_alt.as<uint64_t>(), dr.residual, 0, dr.sort_bits, P.sort_tmp.p,
-                       st, &P.launches);
+    P.local_sorted = vr::radix_sort_u64(P.resid.as<uint64_t>(), P.resid_alt.as<uint64_t>(), dr.residual, 0, dr.sort_bits,
+                                        P.sort_tmp.p, st, &P.launches);
+    if (P.world > 1) exchange_residual(P, d, dr.residual, true);  // exchange B (timed with the sort)
     if (d < P.D && clr_next)
       vr::launch_set_bits(P.dims[(size_t)d + 1].deaths_in.as<uint64_t>(), P.dims[(size_t)d + 1].ndeaths_in, clr_next,
                           st, &P.launches);
@@ -1092,33 +1358,90 @@ int vr_barcodes_coo(int64_t n, int64_t nnz, const int32_t* rows, const int32_t* 
   });
 }
 
+// restores the caller's current device on scope exit
+struct DeviceGuard {
+  int dev = -1;
+  DeviceGuard() { if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); dev = -1; } }
+  ~DeviceGuard() { if (dev >= 0) cudaSetDevice(dev); }
+};
+
+// The host-pointer computation on the current device, sharded when comm is given.
+void barcodes_host(const float* lt, int64_t n, int32_t max_dim, float threshold, const vr_options& o, const vr_comm* comm,
+                   vr_result** out) {
+  SectionTimer ST;
+  std::unique_ptr<vr_plan> P(new vr_plan());
+  P->n = n; P->D = max_dim; P->threshold = threshold; P->opt = o;
+  if (comm) {
+    P->comm = comm;
+    P->rank_id = comm->rank;
+    P->world = comm->world;
+  }
+  CUDA_TRY(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking));
+  struct SG { cudaStream_t s; ~SG() { cudaStreamDestroy(s); } } sg{P->st};
+  const size_t bytes = (size_t)n * (size_t)(n - 1) / 2 * sizeof(float);
+  P->lt_copy.ensure(std::max<size_t>(bytes, 4));
+  if (bytes) CUDA_TRY(cudaMemcpyAsync(P->lt_copy.p, lt, bytes, cudaMemcpyHostToDevice, P->st));
+  P->d_lt = P->lt_copy.as<float>();
+  ST.mark("H2D input");
+  run_full(*P);
+  CUDA_TRY(cudaStreamSynchronize(P->st));
+  ST.mark("run_full");
+  std::unique_ptr<vr_result> R(std::move(P->R));
+  P.reset();
+  ST.mark("release device buffers");
+  *out = R.release();
+}
+
+int vr_barcodes_comm(const float* lt, int64_t n, int32_t max_dim, float threshold, const vr_options* opt,
+                     const vr_comm* comm, vr_result** out) {
+  if (out) *out = nullptr;
+  DeviceGuard dg;
+  return guarded([&] {
+    if (!out || !comm) throw VrError(VR_EINVAL, "out / comm is NULL");
+    if (comm->world < 1 || comm->rank < 0 || comm->rank >= comm->world) throw VrError(VR_EINVAL, "bad rank / world");
+    check_args(lt, n, max_dim, threshold);
+    barcodes_host(lt, n, max_dim, threshold, default_options(opt), comm, out);
+  });
+}
+
 int vr_barcodes(const float* lt, int64_t n, int32_t max_dim, float threshold, const vr_options* opt, vr_result** out) {
   if (out) *out = nullptr;
-  SectionTimer ST;
+  DeviceGuard dg;
   int rc = guarded([&] {
     if (!out) throw VrError(VR_EINVAL, "out is NULL");
     check_args(lt, n, max_dim, threshold);
     vr_options o = default_options(opt);
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw VrError(VR_EDEVICE, "no CUDA device");
+    if (o.num_gpus > 1) {  // one process over devices 0..G-1: a host thread per device, NCCL
+      const int G = o.num_gpus;
+      if (G > ndev) throw VrError(VR_EINVAL, "options.num_gpus exceeds the visible devices");
+      std::vector<vr_comm*> comms = vr::comm_nccl_all(G);
+      if ((int)comms.size() != G) throw VrError(VR_EDEVICE, "ncclCommInitAll failed: " + g_err);
+      std::vector<vr_result*> res((size_t)G, nullptr);
+      std::vector<int> rcs((size_t)G, VR_OK);
+      std::vector<std::string> errs((size_t)G);
+      std::vector<std::thread> th;
+      for (int g = 0; g < G; ++g)
+        th.emplace_back([&, g] {
+          cudaSetDevice(g);
+          rcs[(size_t)g] = guarded([&] { barcodes_host(lt, n, max_dim, threshold, o, comms[(size_t)g], &res[(size_t)g]); });
+          if (rcs[(size_t)g]) errs[(size_t)g] = g_err;
+        });
+      for (auto& t : th) t.join();
+      for (vr_comm* c : comms) vr_comm_free(c);
+      for (int g = 1; g < G; ++g) delete res[(size_t)g];
+      for (int g = 0; g < G; ++g)
+        if (rcs[(size_t)g]) {
+          delete res[0];
+          throw VrError(rcs[(size_t)g], "rank " + std::to_string(g) + ": " + errs[(size_t)g]);
+        }
+      *out = res[0];
+      return;
+    }
     if (o.device < 0 || o.device >= ndev) throw VrError(VR_EINVAL, "options.device out of range");
     CUDA_TRY(cudaSetDevice(o.device));
-    std::unique_ptr<vr_plan> P(new vr_plan());
-    P->n = n; P->D = max_dim; P->threshold = threshold; P->opt = o;
-    CUDA_TRY(cudaStreamCreateWithFlags(&P->st, cudaStreamNonBlocking));
-    struct SG { cudaStream_t s; ~SG() { cudaStreamDestroy(s); } } sg{P->st};
-    const size_t bytes = (size_t)n * (size_t)(n - 1) / 2 * sizeof(float);
-    P->lt_copy.ensure(std::max<size_t>(bytes, 4));
-    if (bytes) CUDA_TRY(cudaMemcpyAsync(P->lt_copy.p, lt, bytes, cudaMemcpyHostToDevice, P->st));
-    P->d_lt = P->lt_copy.as<float>();
-    ST.mark("H2D input");
-    run_full(*P);
-    CUDA_TRY(cudaStreamSynchronize(P->st));
-    ST.mark("run_full");
-    std::unique_ptr<vr_result> R(std::move(P->R));
-    P.reset();
-    ST.mark("release device buffers");
-    *out = R.release();
+    barcodes_host(lt, n, max_dim, threshold, o, nullptr, out);
   });
   return rc;
 }
@@ -1159,6 +1482,31 @@ int vr_plan_create(const float* d_lt, int64_t n, int32_t max_dim, float threshol
     P->n = n; P->D = max_dim; P->threshold = threshold; P->opt = default_options(opt);
     P->opt.index_pairs = 0;
     P->st = (cudaStream_t)stream; P->d_lt = d_lt;
+    run_full(*P);
+    CUDA_TRY(cudaStreamSynchronize(P->st));
+    P->launches = 0;
+    std::unique_ptr<vr_result> R(std::move(P->R));
+    P->R.reset(new vr_result(*R));
+    *plan = P.release();
+    if (out) *out = R.release();
+  });
+}
+
+int vr_plan_create_comm(const float* d_lt, int64_t n, int32_t max_dim, float threshold, const vr_options* opt,
+                        const vr_comm* comm, void* stream, vr_plan** plan, vr_result** out) {
+  if (plan) *plan = nullptr;
+  if (out) *out = nullptr;
+  return guarded([&] {
+    if (!plan || !comm) throw VrError(VR_EINVAL, "plan / comm is NULL");
+    if (comm->world < 1 || comm->rank < 0 || comm->rank >= comm->world) throw VrError(VR_EINVAL, "bad rank / world");
+    check_args(d_lt, n, max_dim, threshold);
+    std::unique_ptr<vr_plan> P(new vr_plan());
+    P->n = n; P->D = max_dim; P->threshold = threshold; P->opt = default_options(opt);
+    P->opt.index_pairs = 0;
+    P->st = (cudaStream_t)stream; P->d_lt = d_lt;
+    P->comm = comm;
+    P->rank_id = comm->rank;
+    P->world = comm->world;
     run_full(*P);
     CUDA_TRY(cudaStreamSynchronize(P->st));
     P->launches = 0;
@@ -1266,160 +1614,8 @@ int vr_radix_sort_u64(uint64_t* keys, int64_t n, int32_t begin_bit, int32_t end_
 }
 
 // ---------------------------------------------------------------- distributed stepping
-int vr_dist_begin(const float* d_lt, int64_t n, int32_t max_dim, float threshold, const vr_options* opt, void* stream,
-                  int32_t rank, int32_t world, vr_plan** plan) {
-  if (plan) *plan = nullptr;
-  return guarded([&] {
-    if (!plan) throw VrError(VR_EINVAL, "plan is NULL");
-    if (world < 1 || rank < 0 || rank >= world) throw VrError(VR_EINVAL, "bad rank / world");
-    check_args(d_lt, n, max_dim, threshold);
-    std::unique_ptr<vr_plan> P(new vr_plan());
-    P->n = n; P->D = max_dim; P->threshold = threshold; P->opt = default_options(opt);
-    P->opt.index_pairs = 0;
-    P->st = (cudaStream_t)stream; P->d_lt = d_lt;
-    P->rank_id = rank;
-    P->world = world;
-    stage_setup(*P);
-    *plan = P.release();
-  });
-}
-
-int vr_dist_dim_local(vr_plan* P, int32_t d, int64_t* nkeys, int64_t* next_bitmap_words) {
-  return guarded([&] {
-    if (!P || d < 1 || d > P->D) throw VrError(VR_EINVAL, "bad plan / dimension");
-    const uint64_t nk = stage_dim_local(*P, d);
-    if (nkeys) *nkeys = (int64_t)nk;
-    if (next_bitmap_words) *next_bitmap_words = P->clr_of(d + 1) ? (int64_t)P->dims[(size_t)d + 1].clr_words : 0;
-  });
-}
-
-int vr_dist_copy_keys(vr_plan* P, int32_t d, uint64_t* dst) {
-  return guarded([&] {
-    if (!P || d < 1 || d > P->D) throw VrError(VR_EINVAL, "bad plan / dimension");
-    const uint64_t nk = P->dims[(size_t)d].residual;
-    if (nk && P->local_sorted)
-      CUDA_TRY(cudaMemcpyAsync(dst, P->local_sorted, nk * 8, cudaMemcpyDeviceToDevice, P->st));
-    CUDA_TRY(cudaStreamSynchronize(P->st));
-  });
-}
-
-int vr_dist_bitmap(vr_plan* P, int32_t d, uint32_t* buf, int32_t direction) {
-  return guarded([&] {
-    if (!P || d < 1) throw VrError(VR_EINVAL, "bad plan / dimension");
-    uint32_t* bm = P->clr_of(d);
-    if (!bm) return;
-    const size_t bytes = P->dims[(size_t)d].clr_words * 4;
-    // direction 0/1: copy out/in and synchronize; 2/3: the same, asynchronous on the stream
-    if (direction == 0 || direction == 2) CUDA_TRY(cudaMemcpyAsync(buf, bm, bytes, cudaMemcpyDeviceToDevice, P->st));
-    else CUDA_TRY(cudaMemcpyAsync(bm, buf, bytes, cudaMemcpyDeviceToDevice, P->st));
-    if (direction < 2) CUDA_TRY(cudaStreamSynchronize(P->st));
-  });
-}
-
-int vr_dist_copy_keys_async(vr_plan* P, int32_t d, uint64_t* dst) {
-  return guarded([&] {
-    if (!P || d < 1 || d > P->D) throw VrError(VR_EINVAL, "bad plan / dimension");
-    const uint64_t nk = P->dims[(size_t)d].residual;
-    if (nk && P->local_sorted) CUDA_TRY(cudaMemcpyAsync(dst, P->local_sorted, nk * 8, cudaMemcpyDeviceToDevice, P->st));
-  });
-}
-
-int vr_dist_counters(vr_plan* P, int32_t d, int64_t out[6]) {
-  return guarded([&] {
-    if (!P || d < 1 || d > P->D || !out) throw VrError(VR_EINVAL, "bad arguments");
-    const vr_stats& s = P->R->stats[(size_t)d];
-    out[0] = s.survivors; out[1] = s.apparent; out[2] = s.cleared; out[3] = s.queued; out[4] = s.scanned;
-    out[5] = (int64_t)P->dims[(size_t)d].residual;
-  });
-}
-
-int vr_dist_dim_finish(vr_plan* P, int32_t d, const uint64_t* keys, int64_t nkeys) {
-  return guarded([&] {
-    if (!P || d < 1 || d > P->D || nkeys < 0 || (nkeys && !keys)) throw VrError(VR_EINVAL, "bad arguments");
-    stage_dim_finish(*P, d, keys, (uint64_t)nkeys);
-  });
-}
-
-int vr_dist_end(vr_plan* P, vr_result** out) {
-  if (out) *out = nullptr;
-  return guarded([&] {
-    if (!P || !out) throw VrError(VR_EINVAL, "bad arguments");
-    stage_result(*P);
-    CUDA_TRY(cudaStreamSynchronize(P->st));
-    *out = new vr_result(*P->R);
-  });
-}
-
-// replay pieces of a distributed plan (after one full distributed run): tables, one
-// dimension's local kernels (bitmap of d+1 zeroed, then this rank's apparent cofacets),
-// and the residual-death bits of dimension d into the bitmap of d+1 (after exchange A)
-int vr_dist_replay_tables(vr_plan* P) {
-  return guarded([&] {
-    if (!P) throw VrError(VR_EINVAL, "plan is NULL");
-    uint64_t* sorted = nullptr;
-    vr::launch_tables(P->d_lt, P->n, P->threshold, P->keys.as<uint64_t>(), P->alt.as<uint64_t>(),
-                      P->rowmax.as<uint32_t>(), P->sort_tmp.p, P->tb_tmp.p, P->rank.as<uint32_t>(), P->tout.as<vr::TablesOut>(),
-                      (int64_t)P->m,
-                      &sorted, P->st, &P->launches);
-    if (P->sparse)
-      vr::launch_threshold_bitmap(P->rank.as<uint32_t>(), (int)P->n, P->nw, P->bm.as<uint32_t>(), P->deg.as<uint32_t>(),
-                                  P->deg_below.as<uint32_t>(), P->st, &P->launches);
-    if (P->D >= 1 && P->clr_of(1)) {
-      cudaMemsetAsync(P->clr_of(1), 0, P->dims[1].clr_words * 4, P->st);
-      vr::launch_set_bits(P->dims[1].deaths_in.as<uint64_t>(), P->dims[1].ndeaths_in, P->clr_of(1), P->st, &P->launches);
-    }
-    CUDA_TRY(cudaGetLastError());
-  });
-}
-
-int vr_dist_replay_dim(vr_plan* P, int32_t d) {
-  return guarded([&] {
-    if (!P || d < 1 || d > P->D) throw VrError(VR_EINVAL, "bad plan / dimension");
-    DimRun& dr = P->dims[(size_t)d];
-    if (dr.chunks.empty()) return;
-    cudaStream_t st = P->st;
-    vr::DimCounters* ctr = P->ctrs.as<vr::DimCounters>() + d;
-    uint32_t* clr_next = P->clr_of(d + 1);
-    cudaMemsetAsync(ctr, 0, sizeof(vr::DimCounters), st);
-    if (clr_next) cudaMemsetAsync(clr_next, 0, P->dims[(size_t)d + 1].clr_words * 4, st);
-    P->hash_reset(d + 1, st);
-    vr::DimParams p = dr.p;
-    for (const Chunk& c : dr.chunks) {
-      vr::HotBuffers B{P->queue.as<uint64_t>(), P->qvert.as<uint4>(), P->qcap, P->resid.as<uint64_t>(), P->rcap,
-                       P->clr_of(d), clr_next, dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, ctr, nullptr, 0};
-      P->hash_fields(B, d);
-      vr::SparseRows SR = P->sparse_rows(d, ctr);
-      p.row_begin = c.row_begin;
-      p.row_end = c.row_end;
-      cudaMemsetAsync(&ctr->row_next, 0, 8, st);
-      cudaMemsetAsync(&ctr->queued, 0, 8, st);
-      if (P->sparse)
-        vr::launch_enumerate_sparse(p, P->rank.as<uint32_t>(), P->binom.as<uint64_t>(), P->kmax, B, SR, dr.two_level, P->st,
-                                    &P->launches);
-      else vr::launch_enumerate(p, P->rank.as<uint32_t>(), P->binom.as<uint64_t>(), P->kmax, B, st, &P->launches);
-      if (P->sparse) vr::launch_resolve_sparse(p, P->rank.as<uint32_t>(), P->binom.as<uint64_t>(), P->kmax, B, SR, c.queued, st, &P->launches);
-      else vr::launch_resolve(p, P->rank.as<uint32_t>(), P->binom.as<uint64_t>(), P->kmax, B, c.queued, st, &P->launches);
-    }
-    P->local_sorted = vr::radix_sort_u64(P->resid.as<uint64_t>(), P->resid_alt.as<uint64_t>(), dr.residual, 0, dr.sort_bits,
-                                         P->sort_tmp.p, st, &P->launches);
-    CUDA_TRY(cudaGetLastError());
-  });
-}
-
-int vr_dist_replay_deaths(vr_plan* P, int32_t d) {
-  return guarded([&] {
-    if (!P || d < 1 || d > P->D) throw VrError(VR_EINVAL, "bad plan / dimension");
-    if (d < P->D && P->clr_of(d + 1))
-      vr::launch_set_bits(P->dims[(size_t)d + 1].deaths_in.as<uint64_t>(), P->dims[(size_t)d + 1].ndeaths_in,
-                          P->clr_of(d + 1), P->st, &P->launches);
-    if (d < P->D) P->hash_deaths(d + 1, P->st);
-    CUDA_TRY(cudaGetLastError());
-  });
-}
-
 int64_t vr_plan_launches(const vr_plan* P) { return P ? P->launches : 0; }
 
-// ---------------------------------------------------------------- host-only residual
 int vr_host_residual(const uint32_t* rank, const float* values, int64_t nvalues, int64_t n, int32_t d, uint32_t maxr,
                      int32_t cbits, const uint64_t* keys, int64_t nkeys, int32_t mode, float* birth, float* death,
                      uint64_t* birth_cidx, uint64_t* death_cidx, int64_t* emergent) {

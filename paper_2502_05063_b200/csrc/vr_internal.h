@@ -15,6 +15,9 @@ namespace vr {
 size_t scan_temp_bytes(size_t n);
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t n, void* temp, cudaStream_t st, int64_t* launches);
 size_t radix_sort_temp_bytes(size_t n);
+// merge of `world` ascending lists of `cap` keys each (gathered[r*cap ..], padded with ~0;
+// keys distinct across lists) into out (the non-padding keys, ascending)
+void merge_gathered_u64(const uint64_t* gathered, int world, uint64_t cap, uint64_t* out, cudaStream_t st, int64_t* launches);
 uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit, int end_bit, void* temp,
                          cudaStream_t st, int64_t* launches);
 
@@ -52,6 +55,7 @@ struct DimParams {
 struct DimCounters {   // device counters (unsigned long long each)
   unsigned long long survivors, apparent1, apparent2, cleared, queued, residual, row_next, app_pairs, scanned, scanned2, rows_out;
   unsigned long long next_bound;  // sparse: sum over survivors s of deg_below(min s) (bounds the next dimension)
+  unsigned long long exported;    // sharded sparse: apparent cofacets appended to exp_list
 };
 struct HotBuffers {
   uint64_t* qkey;        // phase-2 queue: column keys
@@ -70,6 +74,8 @@ struct HotBuffers {
   // d-1 as a hash set with a Bloom filter in front (vr_common.cuh ClearSet)
   ClearSet clr_set;       // table == nullptr: none
   ClearSet clr_next_set;  // receives this dimension's apparent cofacets
+  uint64_t* exp_list;     // sharded: this rank's apparent cofacets (for the other ranks' sets), or nullptr
+  uint64_t exp_cap;
 };
 void launch_set_put(const uint64_t* list, int64_t m, const ClearSet& c, cudaStream_t st, int64_t* launches);
 // returns the VR_KERNEL_* flags of the kernel launched (vr_stats.kernels)
@@ -116,6 +122,8 @@ void launch_coo_to_dense(const int32_t* ii, const int32_t* jj, const float* dd, 
                          cudaStream_t st);
 // message returned by vr_last_error() (thread-local)
 void set_last_error(const std::string& msg);
+// NCCL communicators over devices 0..G-1 of this process (comm.cu; empty on failure)
+std::vector<vr_comm*> comm_nccl_all(int G);
 // device blocks from the process-wide cache (vr_api.cu); bytes is rounded up on return
 void* dev_acquire(size_t& bytes);
 void dev_release(void* p, size_t bytes);

@@ -1,5 +1,7 @@
-"""Test-only model of one rank's device stage (the `Backend` interface of
-paper_2502_05063_b200/dist.py), for tiny inputs on CPU.
+"""Test-only model of the sharded protocol (include/vr.h "Multi-GPU", implemented by the
+library in C++: vr_api.cu run_distributed) on CPU: one rank's device stage, for tiny inputs,
+and the per-dimension orchestration with the exchanges over torch.distributed (gloo).  The
+GPU tests run the library's own implementation with emulated ranks (dist.run_ranks).
 
 The per-simplex facts the GPU kernels compute — survival under the threshold, the
 apparent pair (Def 5.3.4), clearing — are taken from the CPU oracle; the residual
@@ -133,3 +135,68 @@ class ModelBackend:
                 s["pairs_all"] += s["apparent"]
             bc.stats.append(s)
         return bc
+
+
+# ------------------------------------------------------------------ the protocol (model)
+def merge_sorted_keys(parts: list) -> np.ndarray:
+    """k-way merge of per-rank ascending uint64 key arrays (keys are distinct simplices)."""
+    parts = [np.asarray(p, dtype=np.uint64) for p in parts if len(p)]
+    if not parts:
+        return np.zeros(0, np.uint64)
+    out = np.concatenate(parts)
+    out.sort(kind="stable")
+    return out
+
+
+
+def _all_gather_varlen(t, group, dist, torch):
+    """all-gather of a 1-D tensor whose length differs per rank (padded to the max)."""
+    world = dist.get_world_size(group)
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    m = max(sizes) if sizes else 0
+    buf = torch.zeros(max(m, 1), dtype=t.dtype, device=t.device)
+    buf[: t.numel()] = t
+    outs = [torch.zeros_like(buf) for _ in range(world)]
+    dist.all_gather(outs, buf, group=group)
+    return [o[:s] for o, s in zip(outs, sizes)]
+
+
+def orchestrate(backend, max_dim: int, group=None):
+    """Run dimensions 1..max_dim with the two exchanges.  Returns (barcode, per-dimension
+    summed hot-path counters, per-dimension local counters)."""
+    import torch
+    import torch.distributed as dist
+    names = ["survivors", "apparent", "cleared", "queued", "scanned", "residual_local"]
+    totals, local = {}, {}
+    for d in range(1, max_dim + 1):
+        nkeys, words = backend.dim_local(d)
+        if words:  # exchange A: clearing bitmap of d+1, sum == OR (disjoint bits)
+            bm = backend.bitmap_out(d + 1, words)
+            dist.all_reduce(bm, op=dist.ReduceOp.SUM, group=group)
+            backend.bitmap_in(d + 1, bm)
+        # exchange B: residual columns
+        parts = _all_gather_varlen(backend.local_keys(d, nkeys), group, dist, torch)
+        merged = merge_sorted_keys([p.cpu().numpy().view(np.uint64) for p in parts])
+        backend.dim_finish(d, merged)
+        lc = backend.counters(d)
+        local[d] = dict(zip(names, lc))
+        local[d]["next_bitmap_words"] = words
+        c = torch.tensor(lc, dtype=torch.int64, device=backend.device)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM, group=group)
+        totals[d] = dict(zip(names, [int(x) for x in c.cpu().tolist()]))
+    return backend.end(), totals, local
+
+
+def globalize_stats(bc, totals: dict, local: dict):
+    """Hot-path counters of the returned barcode are local to the rank: replace them by
+    the sums over the ranks (pairs_all counts the apparent pairs, zero-length)."""
+    for d, t in totals.items():
+        bc.stats[d]["pairs_all"] += t["apparent"] - local[d]["apparent"]
+        for k in ("survivors", "apparent", "cleared", "queued", "scanned"):
+            bc.stats[d][k] = t[k]
+    return bc
+
+

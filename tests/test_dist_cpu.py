@@ -1,7 +1,12 @@
-"""The multi-GPU path's host logic on CPU: orchestration and the two exchanges of
-SURVEY.md §8(e) over torch.distributed with gloo at world size 2 (and 3), the per-rank
-device stage replaced by tests/_model_backend.py.  The final barcode must equal the
-oracle's, whatever the world size."""
+"""The multi-GPU path's host logic on CPU (gloo, world size 2 and 3):
+
+* the product's plumbing: dist.share_unique_id gives every rank rank 0's NCCL unique id
+  (vr_nccl_unique_id runs without a GPU);
+* the protocol — shards, exchanges A/B/C of include/vr.h "Multi-GPU" — modelled in
+  tests/_model_backend.py with the oracle as the device stage and the library's own host
+  residual: the final barcode must equal the oracle's, whatever the world size.  (The
+  library's C++ implementation of the same protocol is run on a GPU with emulated ranks in
+  tests/test_gpu_parity.py.)"""
 from __future__ import annotations
 
 import math
@@ -16,7 +21,6 @@ import torch.multiprocessing as mp
 
 from datagen import clouds as G
 from oracle import oracle as O
-from paper_2502_05063_b200.dist import globalize_stats, merge_sorted_keys, orchestrate
 
 
 def _free_port():
@@ -31,7 +35,7 @@ def _worker(rank, world, port, lt, n, D, q):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-    from _model_backend import ModelBackend
+    from _model_backend import ModelBackend, globalize_stats, orchestrate
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -76,7 +80,39 @@ def test_sharded_orchestration_matches_oracle(world, seed):
             assert stats[d]["pairs_all"] == ref.num_pairs_all(d)
 
 
+def _uid_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2502_05063_b200.dist import share_unique_id
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, share_unique_id()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_nccl_unique_id_shared(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_uid_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ids = set(out.values())
+    assert len(ids) == 1 and len(next(iter(ids))) == 128
+
+
 def test_merge_sorted_keys():
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from _model_backend import merge_sorted_keys
     rng = np.random.default_rng(0)
     allk = np.unique(rng.integers(0, 2**62, 1000, dtype=np.uint64))
     parts = [np.sort(allk[i::3]) for i in range(3)]

@@ -361,99 +361,120 @@ def test_config5_dim3_invariants(c5_lower_tri):
     assert E[0] == 2
 
 
-# ------------------------------------------------------------------ multi-GPU shards, emulated in one process
-def _emulated_ranks(lt, n, D, world, **opts):
-    """Runs `world` shards of the real device stage one after another on this GPU and
-    performs the two exchanges in-process (sum of bitmaps, merge of keys)."""
-    torch = pytest.importorskip("torch")
-    from paper_2502_05063_b200.dist import LibBackend, merge_sorted_keys
-    t = torch.from_numpy(np.ascontiguousarray(lt)).cuda()
-    bes = [LibBackend(t, n, D, math.inf, r, world, **opts) for r in range(world)]
-    try:
-        tot = {}
-        for d in range(1, D + 1):
-            outs = [be.dim_local(d) for be in bes]
-            words = outs[0][1]
-            if words:
-                s = sum(be.bitmap_out(d + 1, words).to(torch.int64) for be in bes)
-                s = (s & 0xFFFFFFFF).to(torch.int64)
-                s = torch.where(s >= 2**31, s - 2**32, s).to(torch.int32)
-                for be in bes:
-                    be.bitmap_in(d + 1, s.clone())
-            parts = [be.local_keys(d, nk).cpu().numpy().view(np.uint64) for be, (nk, _) in zip(bes, outs)]
-            merged = merge_sorted_keys(parts)
-            for be in bes:
-                be.dim_finish(d, merged)
-            tot[d] = np.sum([be.counters(d) for be in bes], axis=0)
-        return [be.end() for be in bes], tot
-    finally:
-        for be in bes:
-            be.close()
+# ------------------------------------------------------------------ multi-GPU: the library's sharded path
+# Ranks emulated in this process on the one GPU (dist.run_ranks: vr_comm_local, one host
+# thread per rank; the collectives stage through host memory).  Every rank runs the
+# library's run_distributed: its shard of each dimension, exchanges A (clearing bitmap
+# all-reduce / apparent-cofacet all-gather into the sets), B (residual keys all-gather +
+# device merge) and C (rank 0's residual deaths broadcast), then the result broadcast.
+def _ranks(lt, n, D, world, thr=math.inf, **opts):
+    from paper_2502_05063_b200.dist import barcodes_comm, run_ranks
+    return run_ranks(world, lambda c: barcodes_comm(lt, n, D, thr, c, **opts))
+
+
+SHARD_CASES = [("tied", 10, 2), ("cloud", 11, 3), ("c2", 24, 3), ("c5patch", 40, 2), ("c3", 36, 2)]
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("sparse", [1, 2])
+@pytest.mark.parametrize("kind,m,D", SHARD_CASES)
+def test_sharded_ranks_vs_oracle(world, sparse, kind, m, D):
+    thr = math.inf
+    if kind == "tied":
+        lt = G.random_tied(m, 77, levels=4)
+    elif kind == "cloud":
+        lt = G.random_cloud(m, 78)
+    elif kind == "c5patch":
+        lt, thr = G.CONFIGS["c5_o3_4096"].patch(m), 1.4
+    else:
+        lt = G.CONFIGS[{"c2": "c2_s3_192", "c3": "c3_trefoil1000"}[kind]].lower_tri(m)
+    res = _ranks(lt, m, D, world, thr, sparse_mode=sparse, index_pairs=True)
+    ref = O.barcode(lt, m, D, res[0].threshold)
+    for r, got in enumerate(res):  # every rank returns the oracle's barcode
+        assert_values_equal(got, ref, D)
+        assert_index_equal(got, ref, D)
+        assert_counts_equal(got, ref, D)
 
 
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("sparse", [1, 2])
-@pytest.mark.parametrize("name,m,D", [("c2_s3_192", 60, 3), ("c3_trefoil1000", 150, 2)])
-def test_emulated_shards_match_single_gpu(world, sparse, name, m, D):
+@pytest.mark.parametrize("name,m,D,sparse,hashset", [("c2_s3_192", 60, 3, 1, False), ("c3_trefoil1000", 150, 2, 2, False),
+                                                     ("c2_s3_192", 60, 3, 2, True), ("c5_o3_4096", 4096, 2, 0, False)])
+def test_sharded_ranks_match_single_gpu(world, name, m, D, sparse, hashset, monkeypatch):
+    # larger inputs (c5 at full size: the sparse path with the clearing set at dimension 2,
+    # its apparent cofacets all-gathered between the ranks) against the one-GPU result
+    if hashset:
+        monkeypatch.setenv("VR_FORCE_CLEAR_HASH", "1")
     cfg = G.CONFIGS[name]
     lt = cfg.lower_tri(m)
-    ref = vr.barcodes(lt, m, D, sparse_mode=sparse)
-    bcs, tot = _emulated_ranks(lt, m, D, world, sparse_mode=sparse)
-    for bc in bcs:
+    ref = vr.barcodes(lt, m, D, cfg.threshold, sparse_mode=sparse)
+    res = _ranks(lt, m, D, world, cfg.threshold, sparse_mode=sparse)
+    for got in res:
         for d in range(D + 1):
-            assert np.array_equal(bc.pairs[d], ref.pairs[d]), d
-    for d in range(1, D + 1):
-        assert tot[d][0] == ref.stats[d]["survivors"]
-        assert tot[d][1] == ref.stats[d]["apparent"]
-        assert tot[d][2] == ref.stats[d]["cleared"]
-        assert tot[d][5] == ref.stats[d]["residual_columns"]
+            assert np.array_equal(got.pairs[d].view(np.uint32), ref.pairs[d].view(np.uint32)), d
+        for d in range(1, D + 1):
+            for k in ("survivors", "apparent", "cleared", "residual_columns", "pairs_all", "essential", "emergent"):
+                assert got.stats[d][k] == ref.stats[d][k], (d, k)
 
 
-def test_sharded_single_rank_process_group():
-    torch = pytest.importorskip("torch")
+def test_sharded_plan_replay():
+    # the timed multi-rank step (bench.py): a plan per rank, replays of the sharded hot path
+    # with exchanges A and B; the counters of a replay equal the first run's
+    import torch
+    from paper_2502_05063_b200.dist import run_ranks
+    cfg = G.CONFIGS["c2_s3_192"]
+    lt = cfg.lower_tri(80)
+    t = torch.from_numpy(lt).cuda()
+    ref = vr.barcodes(lt, 80, 3)
+
+    def rank(c):
+        s = torch.cuda.Stream()
+        plan = vr.Plan(t, 80, 3, stream=s.cuda_stream, comm=c)
+        first = plan.check()
+        for _ in range(3):
+            assert plan.replay() > 0
+        again = plan.check()
+        res = plan.result
+        plan.close()
+        return first, again, res
+
+    for first, again, res in run_ranks(2, rank):
+        assert first == again
+        for d in range(4):
+            assert np.array_equal(res.pairs[d], ref.pairs[d])
+
+
+def test_nccl_single_rank_and_num_gpus():
+    # the NCCL transport itself (one rank here: every gpurun box has one GPU) and
+    # vr_options.num_gpus = 1 through vr_barcodes
     import socket
     import torch.distributed as tdist
     from paper_2502_05063_b200.dist import barcodes_sharded
     s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
     os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
-    tdist.init_process_group("nccl", rank=0, world_size=1)
+    tdist.init_process_group("gloo", rank=0, world_size=1)
     try:
         cfg = G.CONFIGS["c4a_sierpinski512"]
         lt = cfg.lower_tri(120)
         ref = vr.barcodes(lt, 120, 2)
-        got = barcodes_sharded(torch.from_numpy(lt).cuda(), 120, 2)
+        got = barcodes_sharded(lt, 120, 2)
+        one = vr.barcodes(lt, 120, 2, num_gpus=1)
         for d in range(3):
             assert np.array_equal(got.pairs[d], ref.pairs[d])
+            assert np.array_equal(one.pairs[d], ref.pairs[d])
             assert got.stats[d]["pairs_all"] == ref.stats[d]["pairs_all"]
     finally:
         tdist.destroy_process_group()
 
 
-def test_sharded_hot_path_replay_single_rank():
-    torch = pytest.importorskip("torch")
-    import socket
-    import torch.distributed as tdist
-    from paper_2502_05063_b200.dist import ShardedHotPath
-    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
-    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
-    tdist.init_process_group("nccl", rank=0, world_size=1)
-    try:
-        cfg = G.CONFIGS["c2_s3_192"]
-        lt = cfg.lower_tri(80)
-        hp = ShardedHotPath(torch.from_numpy(lt).cuda(), 80, 3)
-        first = {d: hp.be.counters(d) for d in range(1, 4)}
-        for _ in range(2):
-            assert hp.step() > 0
-        torch.cuda.synchronize()
-        for d in range(1, 4):
-            c = hp.be.counters(d)  # host-side copies of the last run: unchanged
-            assert c == first[d]
-        ref = vr.barcodes(lt, 80, 3)
-        for d in range(4):
-            assert np.array_equal(hp.result.pairs[d], ref.pairs[d])
-        hp.close()
-    finally:
-        tdist.destroy_process_group()
+def test_merge_of_gathered_keys():
+    # exchange B's device merge through the sharded path: many residual columns, 4 ranks
+    cfg = G.CONFIGS["c2_s3_192"]
+    lt = cfg.lower_tri(100)
+    ref = vr.barcodes(lt, 100, 3)
+    res = _ranks(lt, 100, 3, 4)
+    assert res[0].stats[3]["residual_columns"] > 1000
+    for d in range(4):
+        assert np.array_equal(res[0].pairs[d], ref.pairs[d])
 
 
 # ------------------------------------------------------------------ full sizes: sampled outputs vs the oracle
@@ -527,20 +548,15 @@ def test_apparent_rate_matches_paper_at_10000_points():
     # PAPER.md §5.6.6: random-permutation distance matrices, dimension 1, n = 10000:
     # average apparent fraction 0.991127743 (relative to the edges of the filtration, which
     # the enclosing-radius cut keeps).  One sample here (the paper averages 10; the sample
-    # spread at this n is ~5e-5): the GPU hot path alone, through vr_dist_* at world 1.
+    # spread at this n is ~5e-5): the GPU hot path alone (hot_path_only: no residual).
     import torch
-    from paper_2502_05063_b200.dist import LibBackend
     n = 10000
     N = n * (n - 1) // 2
     perm = np.random.default_rng(1000).permutation(N).astype(np.uint32)
     vals = (perm + np.uint32(0x3F800000)).view(np.float32)  # order-preserving (Obs 5.6.8)
     lt = torch.from_numpy(vals).cuda()
-    be = LibBackend(lt, n, 1, math.inf, 0, 1)
-    try:
-        be.dim_local(1)
-        surv, app = be.counters(1)[:2]
-    finally:
-        be.close()
+    bc = vr.barcodes_device(lt, n, 1, math.inf, hot_path_only=True)
+    surv, app = bc.stats[1]["survivors"], bc.stats[1]["apparent"]
     assert abs(app / surv - 0.991127743) < 3e-4
     assert app / N <= (n - 2) / n  # Theorem 5.4.2 bound
 

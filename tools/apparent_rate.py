@@ -5,7 +5,7 @@ random distance matrices (SURVEY.md §8(f) NEXT-2's scale smoke test).
 Input: a uniformly random permutation of 1..n(n-1)/2 fills the lower triangle
 (Obs 5.6.8: only the order matters; the permutation index k is mapped to the fp32 value
 with bit pattern 0x3F800000 + k — distinct, positive, order-preserving).  Only the GPU hot
-path of dimension 1 runs (vr_dist_* at world 1: enumeration, apparent test, compaction,
+path of dimension 1 runs (vr_options.hot_path_only: enumeration, apparent test, compaction,
 sort — no residual reduction).  Reported: apparent pairs / C(n, 2) (the paper's "apparent
 fraction" of the 1-dimensional coboundary matrix), apparent / survivors (edges <= R), the
 Theorem 5.4.2 bound (n-2)/n, and the paper's printed values at n = 10000 and 20000
@@ -32,7 +32,7 @@ def main():
     ap.add_argument("--n", type=int, nargs="*", default=[1000, 2000, 5000, 10000, 20000])
     ap.add_argument("--samples", type=int, default=3)
     args = ap.parse_args()
-    from paper_2502_05063_b200.dist import LibBackend
+    import paper_2502_05063_b200 as vr
     for n in args.n:
         N = n * (n - 1) // 2
         fr, fs, ts = [], [], []
@@ -43,13 +43,10 @@ def main():
             lt = torch.from_numpy(vals).cuda()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            be = LibBackend(lt, n, 1, math.inf, 0, 1)
-            be.dim_local(1)
-            c = be.counters(1)
+            bc = vr.barcodes_device(lt, n, 1, math.inf, hot_path_only=True)
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - t0)
-            be.close()
-            surv, app = c[0], c[1]
+            surv, app = bc.stats[1]["survivors"], bc.stats[1]["apparent"]
             fr.append(app / N)
             fs.append(app / max(surv, 1))
             del lt
