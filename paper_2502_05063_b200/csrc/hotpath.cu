@@ -872,15 +872,14 @@ __global__ void k_set_bits(const uint64_t* __restrict__ list, int64_t m, uint32_
 }
 
 // ------------------------------------------------------------------ launchers
-static int g_sms = 0;
 static int sm_count() {
-  if (!g_sms) {
-    int dev = 0;
+  static const char tag = 0;
+  return device_memo(&tag, [] {
+    int dev = 0, s = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_sms <= 0) g_sms = 148;
-  }
-  return g_sms;
+    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+    return s > 0 ? s : 148;
+  });
 }
 
 static uint64_t binom_u64(uint64_t v, int k) {
@@ -966,11 +965,10 @@ static int enumerate_d(const DimParams& p, const Tables& T, const HotBuffers& B,
   if (q.variant == 1 && q.n >= 32 && q.n <= kWinMaxN) {
     q.win = 1;
     smem = (size_t)q.n * 36 * 4 + (HP_THREADS / 32) * 32 * 4;
-    static bool attr = false;  // per instantiation
-    if (!attr) {
-      cudaFuncSetAttribute(k_enumerate<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kWinMaxN * 36 * 4 + 1024));
-      attr = true;
-    }
+    device_memo((const void*)k_enumerate<D>, [] {  // per instantiation and device
+      return (int)cudaFuncSetAttribute(k_enumerate<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(kWinMaxN * 36 * 4 + 1024));
+    });
   } else {
     q.win = 0;
   }
@@ -983,12 +981,10 @@ static int enumerate_d(const DimParams& p, const Tables& T, const HotBuffers& B,
       q.row_end == binom_u64((uint64_t)q.n, D) && !getenv_flag("VR_NO_FLAT")) {
     const FlatTable* ft = flat_table(q.n, D);
     if (ft) {
-      static bool attr_f = false;
-      if (!attr_f) {
-        cudaFuncSetAttribute(k_enumerate_flat<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kWinMaxN * 36 * 4 + 1024));
-        attr_f = true;
-      }
+      device_memo((const void*)k_enumerate_flat<D>, [] {
+        return (int)cudaFuncSetAttribute(k_enumerate_flat<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kWinMaxN * 36 * 4 + 1024));
+      });
       const uint64_t warps = (ft->nchunks + (uint64_t)q.shard_world - 1) / (uint64_t)q.shard_world;
       uint64_t fb = (warps * 32 + HP_THREADS - 1) / HP_THREADS;
       if (fb > cap) fb = cap;

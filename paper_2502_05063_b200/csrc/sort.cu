@@ -86,7 +86,8 @@ __global__ void __launch_bounds__(SC_THREADS) scan_tile_sums(const uint32_t* __r
 }
 
 // exclusive scan of one tile, plus an optional per-tile carry
-__global__ void __launch_bounds__(SC_THREADS) scan_tile_apply(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, size_t n,
+// (in and out may alias: exclusive_scan_u32 scans in place — no __restrict__ on them)
+__global__ void __launch_bounds__(SC_THREADS) scan_tile_apply(const uint32_t* in, uint32_t* out, size_t n,
                                                               const uint32_t* __restrict__ carry) {
   __shared__ uint32_t warp_tot[SC_THREADS / 32];
   __shared__ uint32_t total;
@@ -503,7 +504,6 @@ size_t radix_sort_temp_bytes(size_t n) {
   return align256(hist * sizeof(uint32_t)) + scan_temp_bytes(hist);
 }
 
-static bool g_rs_attr_done = false;
 
 // Sorts keys[0..n) ascending on bits [begin_bit, end_bit).  alt is a ping-pong buffer of
 // n keys.  Returns the buffer holding the result (keys or alt).
@@ -512,17 +512,17 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit,
   if (n <= 1 || end_bit <= begin_bit) return keys;
   const size_t smem = 2 * RS_TILE * sizeof(uint64_t) + (RS_WARPS * RS_BINS + 2 * RS_BINS) * sizeof(uint32_t);
   const size_t smem_small = 2 * RS_SMALL_CAP * sizeof(uint64_t) + (RS_WARPS * RS_BINS + 2 * RS_BINS) * sizeof(uint32_t);
-  if (!g_rs_attr_done) {
+  static const char attr_tag = 0, cl_tag = 0, coop_tag = 0;  // per-device memo keys
+  device_memo(&attr_tag, [&] {
     cudaFuncSetAttribute(rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(rs_scatter_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(rs_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_small);
-    g_rs_attr_done = true;
-  }
+    return 1;
+  });
   // one cluster, all passes in distributed shared memory
-  static int cl_max = -1;
   const size_t smem_cl = 2 * RS_SMALL_CAP * sizeof(uint64_t) + (CL_WARPS * RS_BINS + 2 * RS_BINS) * sizeof(uint32_t);
-  if (cl_max < 0) {
-    cl_max = 0;
+  const int cl_max = device_memo(&cl_tag, [&] {
+    int cl_max = 0;
     if (!std::getenv("VR_NO_CLUSTER_SORT") &&
         cudaFuncSetAttribute(rs_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cl) == cudaSuccess &&
         cudaFuncSetAttribute(rs_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
@@ -543,7 +543,8 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit,
       }
     }
     cudaGetLastError();
-  }
+    return cl_max;
+  });
   // one CTA, all passes in shared memory: up to RS_SMALL_CAP keys without clusters, else
   // up to VR_SMALL_SORT_MAX (default 2048) keys — above that a cluster of 2-4 CTAs of 1024
   // threads sorts faster than one 256-thread CTA
@@ -587,16 +588,15 @@ uint64_t* radix_sort_u64(uint64_t* keys, uint64_t* alt, size_t n, int begin_bit,
   }
   const uint32_t ntiles = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
   uint32_t* hist = (uint32_t*)temp;
-  static int coop_cap = -1;
-  if (coop_cap < 0) {
+  const int coop_cap = device_memo(&coop_tag, [&] {
     int dev = 0, sms = 0, per = 0, coop = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
     cudaFuncSetAttribute(rs_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rs_coop, RS_THREADS, smem);
-    coop_cap = coop ? sms * per : 0;
-  }
+    return coop ? sms * per : 0;
+  });
   if ((int)ntiles <= coop_cap) {  // every pass in one cooperative launch
     const int passes = (end_bit - begin_bit + 7) / 8;
     // halve the tile while the grid stays small: a pass's latency scales with the keys per

@@ -81,18 +81,20 @@ class DevCache {
     }
     return p;
   }
-  void release(void* p, size_t b) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  void release(void* p, size_t b, int dev) {  // dev: the device the block was allocated on
     std::lock_guard<std::mutex> g(mu_);
     if (cached_ + b > kCap) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      if (cur != dev) cudaSetDevice(dev);
       cudaFree(p);
+      if (cur != dev) cudaSetDevice(cur);
       return;
     }
     free_.emplace(Key{dev, b}, p);
     cached_ += b;
   }
-  void trim(int dev) {
+  void trim(int dev) {  // (called with `dev` current)
     std::lock_guard<std::mutex> g(mu_);
     for (auto it = free_.begin(); it != free_.end();) {
       if (it->first.dev == dev) {
@@ -169,8 +171,24 @@ namespace {
 
 namespace vr {
 void set_last_error(const std::string& msg) { g_err = msg; }
+int device_memo(const void* key, const std::function<int()>& f) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> memo;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = memo.find({dev, key});
+  if (it != memo.end()) return it->second;
+  const int v = f();
+  memo[{dev, key}] = v;
+  return v;
+}
 void* dev_acquire(size_t& bytes) { return DevCache::get().alloc(bytes); }
-void dev_release(void* p, size_t bytes) { DevCache::get().release(p, bytes); }
+void dev_release(void* p, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevCache::get().release(p, bytes, dev);
+}
 }  // namespace vr
 
 namespace {
@@ -178,15 +196,17 @@ namespace {
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  int dev = 0;  // the device the block belongs to
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }  // (vector<DimRun>)
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), dev(o.dev) { o.p = nullptr; o.bytes = 0; }  // (vector<DimRun>)
   DevBuf& operator=(DevBuf&&) = delete;
   ~DevBuf() { release(); }
-  // the owner must have synchronised the stream that used the buffer
+  // the owner must have synchronised the stream that used the buffer; the block goes back
+  // to the cache under its own device, whatever device is current
   void release() {
-    if (p) DevCache::get().release(p, bytes);
+    if (p) DevCache::get().release(p, bytes, dev);
     p = nullptr;
     bytes = 0;
   }
@@ -194,6 +214,7 @@ struct DevBuf {
     if (b <= bytes && p) return;
     release();
     if (b == 0) b = 16;
+    cudaGetDevice(&dev);
     p = DevCache::get().alloc(b);
     bytes = b;
   }
@@ -934,6 +955,10 @@ void stage_dim_finish(vr_plan& P, int d, const uint64_t* keys, uint64_t nkeys) {
   vr::residual_reduce(P.M, d, P.maxr, dr.p.cbits, keys, nkeys, P.opt.residual_mode, P.hp[(size_t)d], P.deaths, rst);
   stt.ms_residual = ms_since(tr);
   ST.mark("  residual (host)");
+  if (std::getenv("VR_TIMING"))
+    std::fprintf(stderr, "[vr]   residual d=%d: columns %llu emergent %lld additions %lld coboundaries %lld apparent checks %lld\n", d,
+                 (unsigned long long)nkeys, (long long)rst.emergent, (long long)rst.additions, (long long)rst.coboundaries,
+                 (long long)rst.apparent_checks);
   if (const char* dump = std::getenv("VR_DUMP_RESIDUAL")) {
     std::vector<uint64_t> kv(keys, keys + nkeys);
     dump_residual(dump, P.M, d, P.maxr, dr.p.cbits, kv);

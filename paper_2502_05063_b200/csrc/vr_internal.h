@@ -2,6 +2,7 @@
 #pragma once
 #include <algorithm>
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 #include <cuda_runtime.h>
@@ -122,6 +123,10 @@ void launch_coo_to_dense(const int32_t* ii, const int32_t* jj, const float* dd, 
                          cudaStream_t st);
 // message returned by vr_last_error() (thread-local)
 void set_last_error(const std::string& msg);
+// Per-(current device, key) memo, thread-safe: f runs once per device and its value is
+// returned afterwards (function attributes, occupancy and cluster probes apply to the current
+// device's context only) (vr_api.cu)
+int device_memo(const void* key, const std::function<int()>& f);
 // NCCL communicators over devices 0..G-1 of this process (comm.cu; empty on failure)
 std::vector<vr_comm*> comm_nccl_all(int G);
 // device blocks from the process-wide cache (vr_api.cu); bytes is rounded up on return
