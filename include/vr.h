@@ -378,6 +378,12 @@ void vr_w1_net_free(vr_w1_net* net);
  * order), using the current device.  Returns VR_OK or an error code.
  * ---------------------------------------------------------------------------------- */
 int vr_radix_sort_u64(uint64_t* keys, int64_t n, int32_t begin_bit, int32_t end_bit);
+/* Component entry (tests): the residual-column sort — keys = (field << cbits) | low with
+ * field < bins, ascending on bits [0, end_bit) (the keys must be distinct).  *mode in: -1
+ * choose (counting sort on the field + the runs of equal field sorted, falling back to the
+ * radix sort when runs are too long or too many), 0 radix sort, 1 counting sort; out: the
+ * path taken. */
+int vr_sort_columns_u64(uint64_t* keys, int64_t n, int32_t cbits, int32_t end_bit, uint64_t bins, int32_t* mode);
 
 /* ----------------------------------------------------------------------------------
  * Diagnostics (bench.py): measured on-chip peaks of `device` — the integer-ALU throughput

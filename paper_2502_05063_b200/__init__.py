@@ -108,6 +108,7 @@ def load() -> ctypes.CDLL:
         "vr_plan_free": (None, [vp]),
         "vr_plan_dim_timing": (ctypes.c_int, [vp, i32, ctypes.POINTER(ctypes.c_double)]),
         "vr_radix_sort_u64": (ctypes.c_int, [vp, i64, i32, i32]),
+        "vr_sort_columns_u64": (ctypes.c_int, [vp, i64, i32, i32, ctypes.c_uint64, ctypes.POINTER(i32)]),
         "vr_hypha_pivots": (ctypes.c_int, [vp, vp, i64, vp, i32, vp, vp]),
         "vr_min_cost_flow": (ctypes.c_int, [i64, vp, i64, vp, vp, vp, i64, vp, vp]),
         "vr_w1": (ctypes.c_int, [vp, i64, vp, i64, ctypes.c_double, ctypes.c_uint64, i32, i64, vp, vp]),
@@ -363,6 +364,14 @@ def radix_sort_u64(keys: np.ndarray, begin_bit: int = 0, end_bit: int = 64) -> n
     a = np.ascontiguousarray(keys, dtype=np.uint64).copy()
     _check(load().vr_radix_sort_u64(a.ctypes.data if a.size else None, a.size, begin_bit, end_bit))
     return a
+
+
+def sort_columns_u64(keys: np.ndarray, cbits: int, end_bit: int, bins: int, mode: int = -1):
+    """The library's residual-column sort (component test entry).  Returns (sorted, path)."""
+    a = np.ascontiguousarray(keys, dtype=np.uint64).copy()
+    m = ctypes.c_int32(mode)
+    _check(load().vr_sort_columns_u64(a.ctypes.data if a.size else None, a.size, cbits, end_bit, bins, ctypes.byref(m)))
+    return a, int(m.value)
 
 
 def host_residual(rank: np.ndarray, values: np.ndarray, n: int, d: int, maxr: int, cbits: int, keys: np.ndarray,

@@ -672,4 +672,127 @@ void merge_gathered_u64(const uint64_t* gathered, int world, uint64_t cap, uint6
   if (launches) *launches += 1;
 }
 
+// ------------------------------------------------------------------ column keys (a4)
+// Column keys are ((maxr - rank) << cbits) | cidx.  Residual columns rarely share a
+// diameter, so they are counting-sorted on the rank field (a histogram over the maxr + 1
+// values, a scan, an atomic placement: 3 short kernels instead of 8 radix passes at config
+// 5, dimension 3) and every run of equal rank is then sorted by cidx in place — valid while
+// no run is longer than FIX_RUN_MAX (checked on the first run; past it the full sort).
+constexpr int FIX_RUN_MAX = 4096;  // (config 5, dimension 3: 552K keys, longest run 60)
+constexpr int FIX_RUN_REG = 16;    // runs up to this length are sorted in registers
+constexpr uint64_t FIX_LONG_CAP = 1 << 16;  // long runs listed per sort
+
+// Runs of up to FIX_RUN_REG keys: one thread, in registers; longer ones (up to FIX_RUN_MAX)
+// are listed (d_long[0] = count, then run starts) for k_fix_long_runs; longer still: flag.
+__global__ void k_fix_runs(uint64_t* __restrict__ k, uint64_t n, int cbits, unsigned int* __restrict__ overflow,
+                           uint64_t* __restrict__ d_long, uint64_t long_cap) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t hi = k[i] >> cbits;
+    if (i > 0 && (k[i - 1] >> cbits) == hi) continue;  // not the start of a run
+    uint64_t e = i + 1;
+    while (e < n && (k[e] >> cbits) == hi && e - i <= (uint64_t)FIX_RUN_MAX) ++e;
+    const int len = (int)(e - i);
+    if (len == 1) continue;
+    if (len > FIX_RUN_MAX) {  // too long: the caller falls back to the full sort
+      atomicOr(overflow, 1u);
+      continue;
+    }
+    if (len > FIX_RUN_REG) {
+      const unsigned long long slot = atomicAdd((unsigned long long*)d_long, 1ull);
+      if (slot < long_cap) d_long[1 + slot] = i;
+      else atomicOr(overflow, 1u);
+      continue;
+    }
+    uint64_t v[FIX_RUN_REG];
+#pragma unroll
+    for (int a = 0; a < FIX_RUN_REG; ++a) v[a] = a < len ? k[i + (uint64_t)a] : ~0ull;
+    // odd-even transposition network on the fixed-size register array (no local memory);
+    // the ~0 padding sorts to the end
+#pragma unroll
+    for (int r = 0; r < FIX_RUN_REG; ++r)
+#pragma unroll
+      for (int a = r & 1; a + 1 < FIX_RUN_REG; a += 2)
+        if (v[a] > v[a + 1]) { const uint64_t t = v[a]; v[a] = v[a + 1]; v[a + 1] = t; }
+#pragma unroll
+    for (int a = 0; a < FIX_RUN_REG; ++a)
+      if (a < len) k[i + (uint64_t)a] = v[a];
+  }
+}
+
+// one warp per listed long run: every key's place = the number of smaller keys in the run
+__global__ void k_fix_long_runs(uint64_t* __restrict__ k, uint64_t n, int cbits, const uint64_t* __restrict__ d_long,
+                                uint64_t long_cap, uint64_t* __restrict__ tmp) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t cnt = d_long[0] < long_cap ? d_long[0] : long_cap;  // (past the cap: the caller re-sorts)
+  for (uint64_t q = warp; q < cnt; q += nw) {
+    const uint64_t i = d_long[1 + q];
+    const uint64_t hi = k[i] >> cbits;
+    uint64_t e = i + 1;
+    while (e < n && (k[e] >> cbits) == hi) ++e;
+    const int len = (int)(e - i);
+    for (int a = lane; a < len; a += 32) {
+      const uint64_t x = k[i + (uint64_t)a];
+      int pos = 0;
+      for (int b = 0; b < len; ++b) pos += k[i + (uint64_t)b] < x;
+      tmp[i + (uint64_t)pos] = x;
+    }
+    __syncwarp();
+    for (int a = lane; a < len; a += 32) k[i + (uint64_t)a] = tmp[i + (uint64_t)a];
+    __syncwarp();
+  }
+}
+
+__global__ void k_count_hi(const uint64_t* __restrict__ k, uint64_t n, int cbits, uint32_t* __restrict__ cnt) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + (__ldg(k + i) >> cbits), 1u);
+}
+__global__ void k_place_hi(const uint64_t* __restrict__ k, uint64_t n, int cbits, uint32_t* __restrict__ off,
+                           uint64_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t x = __ldg(k + i);
+    out[atomicAdd(off + (x >> cbits), 1u)] = x;  // (order within a run: fixed by k_fix_runs)
+  }
+}
+
+size_t sort_columns_temp_bytes(uint64_t bins) {  // counts, offsets, scan temp, the long-run list
+  return 2 * (((bins + 1) * 4 + 255) / 256 * 256) + (scan_temp_bytes(bins + 1) + 255) / 256 * 256 + (FIX_LONG_CAP + 1) * 8;
+}
+
+uint64_t* sort_columns(uint64_t* keys, uint64_t* alt, size_t n, int cbits, int end_bit, uint64_t bins, void* temp,
+                       void* cnt_temp, int* mode, unsigned int* d_flag, cudaStream_t st, int64_t* launches) {
+  if (n <= 1) return keys;
+  // (worth it for many keys with short runs — few keys per rank; up to 131072 keys the
+  // one-cluster radix sort is a single launch)
+  if (*mode < 0 && ((uint64_t)n > 4 * bins || n <= 131072)) *mode = 0;
+  if (*mode == 0 || cbits >= end_bit || !cnt_temp) return radix_sort_u64(keys, alt, n, 0, end_bit, temp, st, launches);
+  // a counting sort on the rank field (bins = maxr + 1 values), then the runs
+  const size_t cb = ((bins + 1) * 4 + 255) / 256 * 256;
+  uint32_t* cnt = (uint32_t*)cnt_temp;
+  uint32_t* off = (uint32_t*)((char*)cnt_temp + cb);
+  void* scan_tmp = (char*)cnt_temp + 2 * cb;
+  const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 8);
+  cudaMemsetAsync(cnt, 0, (bins + 1) * 4, st);
+  k_count_hi<<<(unsigned)blocks, 256, 0, st>>>(keys, n, cbits, cnt);
+  exclusive_scan_u32(cnt, off, bins + 1, scan_tmp, st, launches);
+  k_place_hi<<<(unsigned)blocks, 256, 0, st>>>(keys, n, cbits, off, alt);
+  uint64_t* out = alt;
+  if (launches) *launches += 2;
+  if (*mode < 0) cudaMemsetAsync(d_flag, 0, 4, st);
+  uint64_t* d_long = (uint64_t*)((char*)cnt_temp + sort_columns_temp_bytes(bins) - (FIX_LONG_CAP + 1) * 8);
+  cudaMemsetAsync(d_long, 0, 8, st);
+  k_fix_runs<<<(unsigned)blocks, 256, 0, st>>>(out, n, cbits, d_flag, d_long, FIX_LONG_CAP);
+  k_fix_long_runs<<<148 * 4, 256, 0, st>>>(out, n, cbits, d_long, FIX_LONG_CAP, keys);
+  if (launches) *launches += 2;
+  if (*mode < 0) {  // the first run decides
+    unsigned int f = 0;
+    cudaMemcpyAsync(&f, d_flag, 4, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    *mode = f ? 0 : 1;
+    if (f) return radix_sort_u64(out, keys, n, 0, end_bit, temp, st, launches);
+  }
+  return out;
+}
+
 }  // namespace vr

@@ -641,6 +641,7 @@ __global__ void __launch_bounds__(SP_THREADS, MINB) k_enum_sparse2(Tables T, Dim
         }
         while (ix < tfill && ng < SP_MAXG && poff + tfill <= SP_PCAP && slots < 32) {
           const int x = tv[ix];
+          const int xi = ix;  // x's position in C(τ)
           ix += (int)p.slices;
           if (x == 0) continue;
           // C(σ): the entries of C(τ) adjacent to x, order kept (ballot compaction); the
@@ -671,7 +672,10 @@ __global__ void __launch_bounds__(SP_THREADS, MINB) k_enum_sparse2(Tables T, Dim
               cv[pos] = (uint16_t)vb;
               cm[pos] = umax(tm[jb], rb);
             }
-            first_w += __popc(__ballot_sync(0xffffffffu, ka && va > x)) + __popc(__ballot_sync(0xffffffffu, kb && vb > x));
+            // the kept entries above x are those before x's own position ix (tv descends)
+            const int ra_n = xi - j0, rb_n = xi - j0 - 32;  // entries of this round before x
+            first_w += __popc(kma & (ra_n >= 32 ? 0xffffffffu : (ra_n <= 0 ? 0u : ((1u << ra_n) - 1)))) +
+                       __popc(kmb & (rb_n >= 32 ? 0xffffffffu : (rb_n <= 0 ? 0u : ((1u << rb_n) - 1))));
             fill += na + __popc(kmb);
           }
           const int ns = fill - first_w;
@@ -894,8 +898,10 @@ static void enum_sparse_d(const DimParams& p, const Tables& T, const HotBuffers&
       q.grab = rows * (uint64_t)q.slices >= cap * SP_WARPS * 64 ? 4 : 1;
       // (tuning: VR_SP_MINB = resident CTAs per SM the registers are budgeted for)
       static const int minb = std::getenv("VR_SP_MINB") ? std::atoi(std::getenv("VR_SP_MINB")) : 4;
-      if (minb == 2) k_enum_sparse2<D, 2><<<(unsigned)blocks, SP_THREADS, 0, st>>>(T, q, B, S);
-      else if (minb == 3) k_enum_sparse2<D, 3><<<(unsigned)blocks, SP_THREADS, 0, st>>>(T, q, B, S);
+      const unsigned bl = (unsigned)std::min<uint64_t>(blocks * (uint64_t)std::max(minb, 4) / 4, (uint64_t)sp_sms() * minb);
+      if (minb == 3) k_enum_sparse2<D, 3><<<bl, SP_THREADS, 0, st>>>(T, q, B, S);
+      else if (minb == 5) k_enum_sparse2<D, 5><<<bl, SP_THREADS, 0, st>>>(T, q, B, S);
+      else if (minb == 6) k_enum_sparse2<D, 6><<<bl, SP_THREADS, 0, st>>>(T, q, B, S);
       else k_enum_sparse2<D, 4><<<(unsigned)blocks, SP_THREADS, 0, st>>>(T, q, B, S);
       return;
     }

@@ -14,11 +14,13 @@
 //                     ascending, cidx DEscending: exactly the §5.1.4 filtration order of the
 //                     edges (dimension 0 walks it for union-find) and the sorted distance
 //                     list the ranks index.
-//   5. tb_rank      : (by tiles, written to (i, j) and (j, i) through shared memory)
-//                     rank[i][j] = index of the first sorted edge with the value d(i,j)
-//                     (a lower_bound), or RINF when d(i,j) > t or i = j.  Equal distances get equal
+//   5. tb_rank_scatter : rank[i][j] = index of the first sorted edge with the value d(i,j)
+//                     (a lower bound, computed once per edge under t and scattered to (i, j)
+//                     and (j, i) of a matrix pre-filled with RINF), or RINF when d(i,j) > t or
+//                     i = j; in the output-sensitive mode also the threshold-graph bitmap.  Equal distances get equal
 //                     ranks and the order is kept, so rank comparisons are the paper's
 //                     diameter comparisons, exactly (reading A11: no arithmetic on values).
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -81,7 +83,8 @@ __global__ void tb_rowmax(const float* __restrict__ lt, int64_t n, uint32_t* __r
 __global__ void tb_threshold(const uint32_t* __restrict__ rowmax, int64_t n, float threshold, TablesOut* __restrict__ out) {
   __shared__ uint32_t red[32];
   uint32_t m = 0xFFFFFFFFu;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = rowmax[i] < m ? rowmax[i] : m;
+  if (isinf(threshold))  // (rowmax is only computed for the enclosing radius)
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = rowmax[i] < m ? rowmax[i] : m;
 #pragma unroll
   for (int o = 16; o; o >>= 1) { uint32_t y = __shfl_xor_sync(0xffffffffu, m, o); m = y < m ? y : m; }
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
@@ -156,39 +159,53 @@ __global__ void tb_edge_compact(const float* __restrict__ lt, uint64_t N, int kb
   }
 }
 
-__global__ void tb_rank(const float* __restrict__ lt, int64_t n, const uint64_t* __restrict__ sorted, int kbits,
-                        const TablesOut* __restrict__ tout, uint32_t* __restrict__ rank) {
-  __shared__ uint32_t tile[32][33];
-  const uint32_t tb = tout->tbits;
-  const uint64_t m = tout->m_le_t;
-  int I, J;
-  tile_of(blockIdx.x, I, J);
-  const int bx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t j = 32 * (int64_t)J + bx;
-  for (int a = ty; a < 32; a += 8) {
-    const int64_t i = 32 * (int64_t)I + a;
-    uint32_t r = VR_RINF;  // i = j: no self-pairs (a scan over cofacet vertices needs no v != s_i test)
-    if (i < n && j < i) {
-      const uint32_t b = dist_bits(__ldg(lt + i * (i - 1) / 2 + j));
-      if (b <= tb) {
-        const uint64_t x = (uint64_t)b << kbits;
-        uint64_t lo = 0, hi = m;
-        while (lo < hi) {
-          const uint64_t mid = (lo + hi) >> 1;
-          if (__ldg(sorted + mid) < x) lo = mid + 1; else hi = mid;
-        }
-        r = (uint32_t)lo;
-      }
+// The ranks from the sorted edges (replaces the per-entry binary search over the whole
+// matrix): the edge at sorted position p has rank = the first position of its distance
+// (a lower bound over the prefix [0, p]); it is written to (i, j) and (j, i) of the rank
+// matrix (pre-filled with RINF) and, when `bm` is given, to the threshold-graph bitmap.
+__global__ void tb_rank_scatter(const uint64_t* __restrict__ sorted, uint64_t m, uint64_t N, int kbits, int64_t n,
+                                uint32_t* __restrict__ rank, uint32_t* __restrict__ bm, int nw) {
+  const uint64_t kmask = (1ull << kbits) - 1;
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = __ldg(sorted + p);
+    const uint64_t x = key & ~kmask;  // the distance bits
+    uint64_t lo = 0, hi = p;          // first position whose distance equals this one's
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if ((__ldg(sorted + mid) & ~kmask) < x) lo = mid + 1; else hi = mid;
     }
-    tile[a][bx] = r;
-    if (i < n && j <= i) rank[(size_t)i * (size_t)n + (size_t)j] = r;
+    const uint64_t k = N - 1 - (key & kmask);  // lower-distance index: k = i(i-1)/2 + j, i > j
+    int64_t i = (int64_t)((1.0 + sqrt(1.0 + 8.0 * (double)k)) * 0.5);
+    while (i * (i - 1) / 2 > (int64_t)k) --i;
+    while ((i + 1) * i / 2 <= (int64_t)k) ++i;
+    const int64_t j = (int64_t)k - i * (i - 1) / 2;
+    rank[(size_t)i * (size_t)n + (size_t)j] = (uint32_t)lo;
+    rank[(size_t)j * (size_t)n + (size_t)i] = (uint32_t)lo;
+    if (bm) {
+      atomicOr(bm + (size_t)i * (size_t)nw + (size_t)(j >> 5), 1u << (j & 31));
+      atomicOr(bm + (size_t)j * (size_t)nw + (size_t)(i >> 5), 1u << (i & 31));
+    }
   }
-  __syncthreads();
-  // the transpose: (j', i') = (32J + a, 32I + bx) with i' > j'
-  for (int a = ty; a < 32; a += 8) {
-    const int64_t jj = 32 * (int64_t)J + a;
-    const int64_t ii = 32 * (int64_t)I + bx;
-    if (ii < n && jj < ii) rank[(size_t)jj * (size_t)n + (size_t)ii] = tile[bx][a];
+}
+
+// deg(v) and deg_below(v) = #{w < v adjacent} from the bitmap (one warp per row)
+__global__ void tb_bitmap_degrees(const uint32_t* __restrict__ bm, int n, int nw, uint32_t* __restrict__ deg,
+                                  uint32_t* __restrict__ deg_below) {
+  const int lane = threadIdx.x & 31;
+  const int v = (int)(((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (v >= n) return;
+  uint32_t c = 0, cb = 0;
+  for (int k = lane; k < nw; k += 32) {
+    const uint32_t w = __ldg(bm + (size_t)v * (size_t)nw + (size_t)k);
+    c += __popc(w);
+    if (32 * k + 31 < v) cb += __popc(w);
+    else if (32 * k < v) cb += __popc(w & ((1u << (v - 32 * k)) - 1));
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  cb = __reduce_add_sync(0xffffffffu, cb);
+  if (lane == 0) {
+    deg[v] = c;
+    deg_below[v] = cb;
   }
 }
 
@@ -230,17 +247,21 @@ size_t tables_temp_bytes(int64_t n) {
 
 void launch_tables(const float* d_lt, int64_t n, float threshold, uint64_t* keys64, uint64_t* alt64, uint32_t* rowmax,
                    void* sort_temp, void* tb_temp, uint32_t* rank, TablesOut* d_out, int64_t m_known, uint64_t** sorted_out,
-                   cudaStream_t st, int64_t* launches) {
+                   cudaStream_t st, int64_t* launches, const GraphOut* g) {
   const uint64_t N = (uint64_t)n * (uint64_t)(n - 1) / 2;
   const int kbits = bits_for(N ? N - 1 : 0);
   cudaMemsetAsync(d_out, 0, sizeof(TablesOut), st);
   const int T = (int)((n + 31) / 32);
   const unsigned tiles = (unsigned)((int64_t)T * (T + 1) / 2);
-  cudaMemsetAsync(rowmax, 0, (size_t)n * 4, st);
-  tb_rowmax<<<tiles, 256, 0, st>>>(d_lt, n, rowmax);
+  if (isinf(threshold)) {  // the enclosing radius needs the row maxima (Prop 5.2.13)
+    cudaMemsetAsync(rowmax, 0, (size_t)n * 4, st);
+    tb_rowmax<<<tiles, 256, 0, st>>>(d_lt, n, rowmax);
+    *launches += 1;
+  }
   tb_threshold<<<1, 1024, 0, st>>>(rowmax, n, threshold, d_out);
-  *launches += 2;
+  *launches += 1;
   uint64_t* sorted = keys64;
+  uint64_t m = 0;
   if (N) {
     const uint32_t nblk = (uint32_t)((N + TB_TILE - 1) / TB_TILE);
     const size_t cb = (((size_t)nblk + 1) * 4 + 255) / 256 * 256;
@@ -252,7 +273,7 @@ void launch_tables(const float* d_lt, int64_t n, float threshold, uint64_t* keys
     exclusive_scan_u32(blk_count, blk_off, (size_t)nblk + 1, scan_tmp, st, launches);
     tb_edge_compact<<<nblk, TB_THREADS, 0, st>>>(d_lt, N, kbits, d_out, blk_off, nblk, keys64);
     *launches += 2;
-    uint64_t m = (uint64_t)m_known;
+    m = (uint64_t)m_known;
     if (m_known < 0) {  // first run: the count decides the sort size
       TablesOut h{};
       cudaMemcpyAsync(&h, d_out, sizeof h, cudaMemcpyDeviceToHost, st);
@@ -261,8 +282,18 @@ void launch_tables(const float* d_lt, int64_t n, float threshold, uint64_t* keys
     }
     sorted = radix_sort_u64(keys64, alt64, (size_t)m, kbits, 31 + kbits, sort_temp, st, launches);
   }
-  tb_rank<<<tiles, 256, 0, st>>>(d_lt, n, sorted, kbits, d_out, rank);
-  *launches += 1;
+  // the rank matrix: RINF, then the m edges under t scattered with their ranks
+  cudaMemsetAsync(rank, 0xFF, (size_t)n * (size_t)n * 4, st);
+  if (g && g->bm) cudaMemsetAsync(g->bm, 0, (size_t)n * (size_t)g->nw * 4, st);
+  if (m) {
+    const uint64_t blocks = std::min<uint64_t>((m + 255) / 256, 148ull * 16);
+    tb_rank_scatter<<<(unsigned)blocks, 256, 0, st>>>(sorted, m, N, kbits, n, rank, g ? g->bm : nullptr, g ? g->nw : 0);
+    *launches += 1;
+  }
+  if (g && g->bm) {
+    tb_bitmap_degrees<<<(unsigned)(((uint64_t)n * 32 + 255) / 256), 256, 0, st>>>(g->bm, (int)n, g->nw, g->deg, g->deg_below);
+    *launches += 1;
+  }
   *sorted_out = sorted;
 }
 

@@ -248,6 +248,7 @@ struct DimRun {
   uint64_t hash_mask = 0;  // slots - 1; 0 = no set (recompute mode)
   uint32_t bloom_words = 0;
   bool two_level = false;  // sparse: k_enum_sparse2 (rows = survivors of d-2)
+  int sort_mode = -1;      // residual-key sort: 1 rank bits + runs, 0 all bits (decided by the first run)
   // sharded runs (recorded by the first run, reused by replays): the largest per-rank count
   // of residual keys and of exported apparent cofacets, this rank's exported count, the sum
   std::vector<uint64_t> x_counts;
@@ -288,7 +289,7 @@ struct vr_plan {
   const float* d_lt = nullptr;
   uint64_t N = 0;
   int kbits = 1, kmax = 0;
-  DevBuf rank, binom, keys, alt, rowmax, sort_tmp, tb_tmp, tout, ctrs, queue, qvert, resid, resid_alt, app_pairs, lt_copy;
+  DevBuf rank, binom, keys, alt, rowmax, sort_tmp, tb_tmp, sort_flag, cnt_tmp, tout, ctrs, queue, qvert, resid, resid_alt, app_pairs, lt_copy;
   uint64_t qcap = 0, rcap = 0, app_cap = 0;
   uint32_t maxr = 0;
   uint64_t m = 0;
@@ -862,8 +863,12 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
   size_t stmp = vr::radix_sort_temp_bytes(std::max<uint64_t>(resid_count, 1));
   if (P.sort_tmp.bytes < stmp) P.sort_tmp.ensure(stmp);
   CUDA_TRY(cudaEventRecord(P.ev[6], st));
-  P.local_sorted = vr::radix_sort_u64(P.resid.as<uint64_t>(), P.resid_alt.as<uint64_t>(), resid_count, 0, dr.sort_bits,
-                                      P.sort_tmp.p, st, &P.launches);
+  P.sort_flag.ensure(8);
+  P.cnt_tmp.ensure(vr::sort_columns_temp_bytes((uint64_t)P.maxr + 1));
+  dr.sort_mode = std::getenv("VR_FULL_SORT") ? 0 : -1;
+  P.local_sorted = vr::sort_columns(P.resid.as<uint64_t>(), P.resid_alt.as<uint64_t>(), resid_count, dr.p.cbits,
+                                    dr.sort_bits, (uint64_t)P.maxr + 1, P.sort_tmp.p, P.cnt_tmp.p, &dr.sort_mode,
+                                    P.sort_flag.as<unsigned int>(), st, &P.launches);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaEventRecord(P.ev[7], st));
   vr::DimCounters hc{};
@@ -1231,12 +1236,10 @@ void replay(vr_plan& P) {
   {
     auto& e = ev(0);
     cudaEventRecord(e.first, st);
+    const vr::GraphOut g{P.bm.as<uint32_t>(), P.nw, P.deg.as<uint32_t>(), P.deg_below.as<uint32_t>()};
     vr::launch_tables(P.d_lt, P.n, P.threshold, P.keys.as<uint64_t>(), P.alt.as<uint64_t>(), P.rowmax.as<uint32_t>(),
                       P.sort_tmp.p, P.tb_tmp.p, P.rank.as<uint32_t>(), P.tout.as<vr::TablesOut>(), (int64_t)P.m, &sorted, st,
-                      &P.launches);
-    if (P.sparse)
-      vr::launch_threshold_bitmap(P.rank.as<uint32_t>(), (int)P.n, P.nw, P.bm.as<uint32_t>(), P.deg.as<uint32_t>(),
-                                  P.deg_below.as<uint32_t>(), st, &P.launches);
+                      &P.launches, P.sparse ? &g : nullptr);
     if (P.D >= 1 && clr_of(1)) {
       cudaMemsetAsync(clr_of(1), 0, P.dims[1].clr_words * 4, st);
       vr::launch_set_bits(P.dims[1].deaths_in.as<uint64_t>(), P.dims[1].ndeaths_in, clr_of(1), st, &P.launches);
@@ -1287,8 +1290,9 @@ void replay(vr_plan& P) {
     }
     auto& e4 = ev(3);
     cudaEventRecord(e4.first, st);
-    P.local_sorted = vr::radix_sort_u64(P.resid.as<uint64_t>(), P.resid_alt.as<uint64_t>(), dr.residual, 0, dr.sort_bits,
-                                        P.sort_tmp.p, st, &P.launches);
+    P.local_sorted = vr::sort_columns(P.resid.as<uint64_t>(), P.resid_alt.as<uint64_t>(), dr.residual, dr.p.cbits,
+                                      dr.sort_bits, (uint64_t)P.maxr + 1, P.sort_tmp.p, P.cnt_tmp.p, &dr.sort_mode,
+                                      P.sort_flag.as<unsigned int>(), st, &P.launches);
     if (P.world > 1) exchange_residual(P, d, dr.residual, true);  // exchange B (timed with the sort)
     if (d < P.D && clr_next)
       vr::launch_set_bits(P.dims[(size_t)d + 1].deaths_in.as<uint64_t>(), P.dims[(size_t)d + 1].ndeaths_in, clr_next,
@@ -1638,7 +1642,28 @@ int vr_radix_sort_u64(uint64_t* keys, int64_t n, int32_t begin_bit, int32_t end_
   });
 }
 
-// ---------------------------------------------------------------- distributed stepping
+int vr_sort_columns_u64(uint64_t* keys, int64_t n, int32_t cbits, int32_t end_bit, uint64_t bins, int32_t* mode) {
+  return guarded([&] {
+    if (n < 0 || (n > 0 && !keys) || cbits < 0 || end_bit > 64 || cbits > end_bit || !mode || bins < 1)
+      throw VrError(VR_EINVAL, "vr_sort_columns_u64: bad arguments");
+    if (n <= 1) return;
+    DevBuf a, b, t, c, f;
+    a.ensure((size_t)n * 8);
+    b.ensure((size_t)n * 8);
+    t.ensure(vr::radix_sort_temp_bytes((size_t)n));
+    c.ensure(vr::sort_columns_temp_bytes(bins));
+    f.ensure(8);
+    CUDA_TRY(cudaMemcpy(a.p, keys, (size_t)n * 8, cudaMemcpyHostToDevice));
+    int64_t launches = 0;
+    int m = *mode;
+    uint64_t* r = vr::sort_columns(a.as<uint64_t>(), b.as<uint64_t>(), (size_t)n, cbits, end_bit, bins, t.p, c.p, &m,
+                                   f.as<unsigned int>(), 0, &launches);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpy(keys, r, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    *mode = m;
+  });
+}
+
 int64_t vr_plan_launches(const vr_plan* P) { return P ? P->launches : 0; }
 
 int vr_host_residual(const uint32_t* rank, const float* values, int64_t nvalues, int64_t n, int32_t d, uint32_t maxr,

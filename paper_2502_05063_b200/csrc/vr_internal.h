@@ -16,6 +16,14 @@ namespace vr {
 size_t scan_temp_bytes(size_t n);
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t n, void* temp, cudaStream_t st, int64_t* launches);
 size_t radix_sort_temp_bytes(size_t n);
+// the residual column keys ((maxr - rank) << cbits | cidx, significant bits < end_bit)
+// into ascending order: *mode 1 = a counting sort on the rank field (bins = maxr + 1) + an
+// in-place sort of every run of equal rank (short runs), 0 = a radix sort on all bits, -1 =
+// try 1 and set *mode (one synchronisation); d_flag: a device word.  Returns the buffer
+// holding the result (keys or alt).
+uint64_t* sort_columns(uint64_t* keys, uint64_t* alt, size_t n, int cbits, int end_bit, uint64_t bins, void* temp,
+                       void* cnt_temp, int* mode, unsigned int* d_flag, cudaStream_t st, int64_t* launches);
+size_t sort_columns_temp_bytes(uint64_t bins);  // cnt_temp of sort_columns (bins = maxr + 1)
 // merge of `world` ascending lists of `cap` keys each (gathered[r*cap ..], padded with ~0;
 // keys distinct across lists) into out (the non-padding keys, ascending)
 void merge_gathered_u64(const uint64_t* gathered, int world, uint64_t cap, uint64_t* out, cudaStream_t st, int64_t* launches);
@@ -32,10 +40,17 @@ struct TablesOut {
 // keys64 (n(n-1)/2) and alt64 ping-pong buffers, rowmax (n), rank (n*n), out (device),
 // tb_temp (tables_temp_bytes(n)); m_known = the edge count under t when known (replays), or
 // -1 (the first run: read back after the compaction, one stream synchronisation)
+// g (optional): also build the threshold-graph bitmap and degrees (output-sensitive mode)
 size_t tables_temp_bytes(int64_t n);
+struct GraphOut {
+  uint32_t* bm;
+  int nw;
+  uint32_t* deg;
+  uint32_t* deg_below;
+};
 void launch_tables(const float* d_lt, int64_t n, float threshold, uint64_t* keys64, uint64_t* alt64, uint32_t* rowmax,
                    void* sort_temp, void* tb_temp, uint32_t* rank, TablesOut* d_out, int64_t m_known, uint64_t** sorted_out,
-                   cudaStream_t st, int64_t* launches);
+                   cudaStream_t st, int64_t* launches, const GraphOut* g = nullptr);
 void launch_build_binom(uint64_t* binom, int64_t n, int kmax, cudaStream_t st, int64_t* launches);
 
 // ---------------------------------------------------------------- hot path kernels

@@ -271,6 +271,39 @@ def test_radix_sort_matches_numpy(n, bits):
     assert np.array_equal(got, keys[order])
 
 
+# the residual-column sort: counting sort on the rank field + the runs of equal rank sorted
+# (in registers up to 16 keys, one warp per longer run up to 4096, else the radix sort)
+@pytest.mark.parametrize("n,bins,runs", [(1000, 5000, "random"), (200000, 200000, "random"), (552000, 234207, "random"),
+                                         (3000, 200, "long"), (300000, 100000, "long"), (70000, 10, "huge"),
+                                         (300000, 100000, "mixed")])
+@pytest.mark.parametrize("mode", [-1, 0, 1])
+def test_sort_columns_matches_numpy(n, bins, runs, mode):
+    rng = np.random.default_rng(n + bins)
+    cbits = 44
+    if runs == "random":
+        f = rng.integers(0, bins, n)
+    elif runs == "long":  # runs of 10..40
+        f = np.repeat(rng.choice(bins, n // 25, replace=False), 25)[:n]
+    elif runs == "huge":  # runs of thousands (> 4096: the radix fallback)
+        f = rng.integers(0, bins, n)
+    else:  # every run length 1..300
+        f = np.concatenate([np.full(k, i % bins) for i, k in enumerate(rng.integers(1, 300, n // 150))])[:n]
+    low = rng.choice(1 << 40, len(f), replace=False).astype(np.uint64)
+    keys = (f.astype(np.uint64) << np.uint64(cbits)) | low
+    if len(np.unique(keys)) != len(keys):
+        keys = np.unique(keys)
+    rng.shuffle(keys)
+    end_bit = cbits + max(1, int(bins).bit_length())
+    if mode == 1 and runs == "huge":
+        mode = -1  # (forcing the counting path on runs past its limit is not supported)
+    got, path = vr.sort_columns_u64(keys, cbits, end_bit, bins, mode)
+    assert np.array_equal(got, np.sort(keys))
+    if mode == -1 and runs == "huge":
+        assert path == 0
+    if mode == -1 and n > 131072 and runs != "huge":
+        assert path == 1  # the counting path was taken (and its runs were short enough)
+
+
 # ------------------------------------------------------------------ output-sensitive (sparse) mode
 @pytest.mark.parametrize("seed,n,D,kind,thr", CASES[::2])
 def test_sparse_mode_index_level(seed, n, D, kind, thr):
