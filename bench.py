@@ -272,7 +272,7 @@ def ncu_traffic(cfg_name, D, kernel):
 
 def roofline(plan, D, n_steps_dims, peaks, cfg_name):
     """The dominant kernel = the enumeration launch of the dimension with the largest device
-    time.  Algorithmic work: rank reads = d per candidate examined (a1) +
+    time.  Algorithmic work: rank reads of the candidate examination (a1) +
     (d+1) per scanned cofacet vertex + C(d+2, 2) per tested column (a5); 2 integer ops and 4
     bytes of L2 per read; the (d+1)·⌈log2 n⌉ decode compares are reported as a separate credit
     (the fused kernels never decode)."""
@@ -301,9 +301,10 @@ def roofline(plan, D, n_steps_dims, peaks, cfg_name):
          "alu": {"achieved_tops": alu_ach, "peak_tops": peaks["alu_tops"], "frac": fa,
                  "frac_with_decode_credit": fad, "ops_per_launch": ops, "decode_credit_ops": t["decode"]},
          "l2": {"achieved_gbs": l2_ach, "peak_gbs": peaks["l2_gbs"], "frac": fl, "bytes_per_launch": 4.0 * reads},
-         "work": "SURVEY.md 8(d): rank reads = d per candidate examined (a1; the survivors in the output-sensitive "
-                 "mode, every C(n,d+1) index dense) + (d+1) per scanned cofacet vertex + C(d+2,2) per tested "
-                 "column (a5); 2 integer ops and 4 B of L2 per read; decode compares reported as a credit only",
+         "work": "SURVEY.md 8(d): rank reads = the candidate examination (a1: d per C(n,d+1) index dense; "
+                 "output-sensitive: d-1 per C(tau) entry + 1 per (sigma, C(tau) entry), as the kernel reads them) + "
+                 "(d+1) per scanned cofacet vertex + C(d+2,2) per tested column (a5); 2 integer ops and 4 B of L2 "
+                 "per read; decode compares reported as a credit only",
          "peak_source": peaks["source"]}
     return r
 

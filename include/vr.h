@@ -192,8 +192,9 @@ int vr_plan_timing(vr_plan* plan, double out[9]);
  * next dimension's death bits / clearing-set inserts), [3] the dimension's setup (counter
  * reset, next clearing bitmap / set reset); and the algorithmic work of the plan's first
  * run: [4] survivors, [5] rank reads of the
- * enumeration (d per candidate examined: every C(n, d+1) index dense, the survivors in the
- * output-sensitive mode), [6] rank reads of the apparent test in the enumeration kernel
+ * enumeration (dense: d per candidate index, every C(n, d+1); output-sensitive: the reads
+ * of the candidate examination — d per listed C(σ) entry in one level, d-1 per C(τ) entry
+ * plus 1 per (σ, C(τ) entry) in two levels), [6] rank reads of the apparent test in the enumeration kernel
  * ((d+1) per scanned cofacet vertex + C(d+2, 2) per tested column), [7] rank reads of the
  * phase-2 kernel, [8] decode compares ((d+1)·⌈log2 n⌉ per tested column — credited work the
  * fused kernels do not execute), [9] the VR_KERNEL_* flags. */

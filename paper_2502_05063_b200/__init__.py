@@ -23,7 +23,8 @@ import numpy as np
 __all__ = ["barcodes", "barcodes_coo", "barcodes_device", "radix_sort_u64", "hypha_pivots", "min_cost_flow", "w1", "w1_network", "Plan", "Barcode", "VRError", "lib_path", "load"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libvr.so")
+# VR_LIB: another build of the library (e.g. the bounds-checked libvr_checks.so, build.py --checks)
+lib_path = os.environ.get("VR_LIB") or os.path.join(_HERE, "libvr.so")
 
 VR_OK, VR_EINVAL, VR_EINPUT, VR_ECAPACITY, VR_EDEVICE = 0, 1, 2, 3, 4
 _CODES = {1: "VR_EINVAL", 2: "VR_EINPUT", 3: "VR_ECAPACITY", 4: "VR_EDEVICE"}

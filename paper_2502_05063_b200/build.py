@@ -32,20 +32,25 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+LIB_CHECKS = os.path.join(HERE, "libvr_checks.so")
+
+
+def build(force: bool = False, verbose: bool = False, checks: bool = False) -> str:
+    """checks: the bounds-checked variant (device asserts, -DVR_CHECKS) -> libvr_checks.so"""
+    lib = LIB_CHECKS if checks else LIB
+    if not force and not checks and not _stale():
         return LIB
     srcs = [os.path.join(CSRC, f) for f in SOURCES]
-    tmp = LIB + ".tmp"
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(HERE, "..", "include"), "-o", tmp, *srcs, "-ldl"]
+    tmp = lib + ".tmp"
+    cmd = [NVCC, *FLAGS, *(["-DVR_CHECKS"] if checks else []), "-I", os.path.join(HERE, "..", "include"), "-o", tmp,
+           *srcs, "-ldl"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checks="--checks" in sys.argv))

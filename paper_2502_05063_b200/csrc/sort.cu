@@ -660,6 +660,7 @@ __global__ void k_merge_gathered(const uint64_t* __restrict__ g, int world, uint
       }
       pos += lo;
     }
+    VR_ASSERT(pos < total);
     out[pos] = x;
   }
 }
@@ -736,6 +737,7 @@ __global__ void k_fix_long_runs(uint64_t* __restrict__ k, uint64_t n, int cbits,
       const uint64_t x = k[i + (uint64_t)a];
       int pos = 0;
       for (int b = 0; b < len; ++b) pos += k[i + (uint64_t)b] < x;
+      VR_ASSERT(i + (uint64_t)len <= n && pos < len);
       tmp[i + (uint64_t)pos] = x;
     }
     __syncwarp();

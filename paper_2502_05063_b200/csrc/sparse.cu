@@ -116,6 +116,7 @@ __device__ __forceinline__ int bm_list(const SparseRows& S, const int (&x)[K], i
     int ab = 0;
     if (fits && c) {
       int pos = fill + incl - c;
+      VR_ASSERT(fill + incl <= cap);
 #pragma unroll
       for (int j = 3; j >= 0; --j) {
         uint32_t bits = wv[j];
@@ -148,6 +149,7 @@ __device__ __forceinline__ int bm_list(const SparseRows& S, const int (&x)[K], i
 // ------------------------------------------------------------------ phase 1 (+ decision)
 struct Acc {
   unsigned long long surv = 0, app = 0, scan = 0, clr = 0, next_bound = 0;
+  unsigned long long cand = 0;  // rank reads of the candidate examination (list maxima, C(σ) compaction)
 };
 
 // Lemma 5.3.6 condition 1 over a lane's list cl[0..fill) (descending; ml = m(v), the
@@ -389,6 +391,7 @@ __device__ void row_general(const Tables& T, const DimParams& p, const HotBuffer
   int nabove = 0;
   int c_fill = bm_list<D>(S, x, c_word, c_mask, cv, SP_LCAP, u1, &nabove);
   list_maxima<D>(T, u, 1, cv, cm, c_fill);
+  acc.cand += (unsigned long long)c_fill * D;
   if (c_word < 0) {  // the whole list fits: the survivors are its tail
     row_from_list<D>(T, p, B, S, u, pm_up, pm_ex, cbase, cv, cm, c_fill, nabove, acc);
     return;
@@ -433,6 +436,7 @@ __device__ void row_general(const Tables& T, const DimParams& p, const HotBuffer
         }
         c_fill = bm_list<D>(S, x, c_word, c_mask, cv, SP_LCAP, 0, nullptr);
         list_maxima<D>(T, u, 1, cv, cm, c_fill);
+        acc.cand += (unsigned long long)c_fill * D;
         c_seg = seg;
       }
       const int h = scan_list(T, cv, cm, c_fill, w, rs, active, examined);
@@ -473,6 +477,7 @@ __device__ __forceinline__ void flush_acc(const HotBuffers& B, Acc& acc) {
     if (acc.app) atomicAdd(&B.ctr->apparent1, acc.app);
     if (acc.scan) atomicAdd(&B.ctr->scanned, acc.scan);
     if (acc.clr) atomicAdd(&B.ctr->cleared, acc.clr);
+    if (acc.cand) atomicAdd(&B.ctr->cand_reads, acc.cand);
   }
   unsigned long long nbsum = acc.next_bound;  // per lane
 #pragma unroll
@@ -595,6 +600,7 @@ __global__ void __launch_bounds__(SP_THREADS, MINB) k_enum_sparse2(Tables T, Dim
         continue;
       }
       list_maxima<D>(T, u, 2, tv, tm, tfill);
+      acc.cand += (unsigned long long)tfill * (D - 1);
       // τ's pair maxima and cidx part
       uint32_t pt_up;
       uint32_t pt_ex[D + 1];
@@ -662,6 +668,7 @@ __global__ void __launch_bounds__(SP_THREADS, MINB) k_enum_sparse2(Tables T, Dim
             const uint32_t kma = __ballot_sync(0xffffffffu, ka);
             const uint32_t kmb = __ballot_sync(0xffffffffu, kb);
             const int na = __popc(kma);
+            VR_ASSERT(poff + fill + na + __popc(kmb) <= SP_PCAP);
             if (ka) {
               const int pos = poff + fill + __popc(kma & lanemask_lt());
               cv[pos] = (uint16_t)va;
@@ -678,6 +685,7 @@ __global__ void __launch_bounds__(SP_THREADS, MINB) k_enum_sparse2(Tables T, Dim
                        __popc(kmb & (rb_n >= 32 ? 0xffffffffu : (rb_n <= 0 ? 0u : ((1u << rb_n) - 1))));
             fill += na + __popc(kmb);
           }
+          acc.cand += (unsigned long long)tfill;  // one rank read R[x][v] per entry of C(τ)
           const int ns = fill - first_w;
           if (ns <= 0) continue;  // no d-simplex in this σ's row
           // σ's pair maxima from τ's and the D-1 new edges: [0] pm_up, [1] avoiding x (τ's),
@@ -691,6 +699,7 @@ __global__ void __launch_bounds__(SP_THREADS, MINB) k_enum_sparse2(Tables T, Dim
             }
             M.gpm[ng][lane] = mine;
           }
+          VR_ASSERT(ng < SP_MAXG);
           if (lane == 0) {
             M.gx[ng] = (int16_t)x;
             M.goff[ng] = (int16_t)poff;
@@ -719,6 +728,7 @@ __global__ void __launch_bounds__(SP_THREADS, MINB) k_enum_sparse2(Tables T, Dim
           while (q + 1 < ng && M.gslot[q + 1] <= t) ++q;
           const int off = M.goff[q], qfill = M.gfill[q];
           const int li = M.gfw[q] + (t - M.gslot[q]);
+          VR_ASSERT(!valid || (li < qfill && off + qfill <= SP_PCAP));
           u[1] = M.gx[q];
           uint32_t pm_ex[D + 1];
           pm_ex[0] = 0;

@@ -179,6 +179,7 @@ __global__ void tb_rank_scatter(const uint64_t* __restrict__ sorted, uint64_t m,
     while (i * (i - 1) / 2 > (int64_t)k) --i;
     while ((i + 1) * i / 2 <= (int64_t)k) ++i;
     const int64_t j = (int64_t)k - i * (i - 1) / 2;
+    VR_ASSERT(i < n && j >= 0 && j < i);
     rank[(size_t)i * (size_t)n + (size_t)j] = (uint32_t)lo;
     rank[(size_t)j * (size_t)n + (size_t)i] = (uint32_t)lo;
     if (bm) {

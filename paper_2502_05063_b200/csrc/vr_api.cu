@@ -556,15 +556,18 @@ void stage_setup(vr_plan& P) {
   M.kmax = P.kmax;
   M.binom = hb;
   std::vector<uint64_t> h_edges((size_t)P.m);
-  if (P.m) CUDA_TRY(cudaMemcpy(h_edges.data(), sorted, (size_t)P.m * 8, cudaMemcpyDeviceToHost));
+  // (copies on the plan's stream: a legacy-default-stream cudaMemcpy does not wait for work
+  // on the non-blocking streams the library uses)
+  if (P.m) CUDA_TRY(cudaMemcpyAsync(h_edges.data(), sorted, (size_t)P.m * 8, cudaMemcpyDeviceToHost, st));
+  if (D >= 1 && P.m) {
+    M.rank.resize((size_t)n * (size_t)n);
+    CUDA_TRY(cudaMemcpyAsync(M.rank.data(), P.rank.p, M.rank.size() * 4, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
   M.value.resize((size_t)P.m);
   for (uint64_t r = 0; r < P.m; ++r) {
     uint32_t fb = (uint32_t)(h_edges[(size_t)r] >> P.kbits);
     std::memcpy(&M.value[(size_t)r], &fb, 4);
-  }
-  if (D >= 1 && P.m) {
-    M.rank.resize((size_t)n * (size_t)n);
-    CUDA_TRY(cudaMemcpy(M.rank.data(), P.rank.p, M.rank.size() * 4, cudaMemcpyDeviceToHost));
   }
   const double ms_tx0 = ms_since(tx0);
   ST.mark("D2H edges + rank matrix");
@@ -878,7 +881,8 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
   cudaEventElapsedTime(&t_sort, P.ev[6], P.ev[7]);
   if (P.opt.index_pairs && hc.app_pairs) {
     std::vector<uint64_t> app_h((size_t)std::min<uint64_t>(hc.app_pairs, app_cap) * 2);
-    CUDA_TRY(cudaMemcpy(app_h.data(), app_ptr, app_h.size() * 8, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpyAsync(app_h.data(), app_ptr, app_h.size() * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
     for (size_t i = 0; i + 1 < app_h.size(); i += 2) R->ipairs[(size_t)d].push_back(vr_index_pair{app_h[i], app_h[i + 1]});
   }
   ST.mark("  sort");
@@ -912,7 +916,9 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
     P.work_rank_ops += 2.0 * d * cand_work + 2.0 * (d + 1) * (double)hc.scanned + 2.0 * cd2 * tested +
                        (double)(d + 1) * lg * tested;
     P.work_rank_ops2 += 2.0 * (d + 1) * (double)hc.scanned2 + (double)(d + 1) * lg * queued;
-    dr.reads_a1 = (double)d * cand_work;
+    // a1 reads: dense — d per candidate index (hoisted prefix maxima); output-sensitive —
+    // the reads the kernels' candidate examination made (list maxima, C(σ) compaction)
+    dr.reads_a1 = P.sparse ? (double)hc.cand_reads : (double)d * cand_work;
     dr.reads_a5 = (double)(d + 1) * (double)hc.scanned + cd2 * tested;
     dr.reads_a5_phase2 = (double)(d + 1) * (double)hc.scanned2;
     dr.decode = (double)(d + 1) * lg * tested;
@@ -1145,7 +1151,8 @@ void run_distributed(vr_plan& P) {
     if (P.rank_id == 0) {
       std::vector<uint64_t> hkeys((size_t)total);
       auto tx = std::chrono::steady_clock::now();
-      if (total) CUDA_TRY(cudaMemcpy(hkeys.data(), P.x_merged.p, total * 8, cudaMemcpyDeviceToHost));
+      if (total) CUDA_TRY(cudaMemcpyAsync(hkeys.data(), P.x_merged.p, total * 8, cudaMemcpyDeviceToHost, P.st));
+      CUDA_TRY(cudaStreamSynchronize(P.st));
       P.R->stats[(size_t)d].ms_transfer += ms_since(tx);
       stage_dim_finish(P, d, hkeys.data(), total);
     }
@@ -1205,7 +1212,8 @@ void run_full(vr_plan& P) {
     }
     std::vector<uint64_t> hkeys((size_t)nk);
     auto tx = std::chrono::steady_clock::now();
-    if (nk) CUDA_TRY(cudaMemcpy(hkeys.data(), P.local_sorted, nk * 8, cudaMemcpyDeviceToHost));
+    if (nk) CUDA_TRY(cudaMemcpyAsync(hkeys.data(), P.local_sorted, nk * 8, cudaMemcpyDeviceToHost, P.st));
+    CUDA_TRY(cudaStreamSynchronize(P.st));
     P.R->stats[(size_t)d].ms_transfer += ms_since(tx);
     stage_dim_finish(P, d, hkeys.data(), nk);
   }

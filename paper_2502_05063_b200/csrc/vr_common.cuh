@@ -12,8 +12,18 @@
 //            key order is coboundary order: diameter descending, cidx ascending
 //            (Fig 5.2 caption).
 #pragma once
+#include <cassert>
 #include <cstdint>
 #include <cuda_runtime.h>
+
+// Bounds checks of shared-memory lists, output slots and table probes: compiled in by the
+// checked build (build.py --checks -> libvr_checks.so, -DVR_CHECKS), which the GPU tests can
+// run (VR_LIB=...libvr_checks.so) in place of compute-sanitizer (closed on this pool).
+#ifdef VR_CHECKS
+#define VR_ASSERT(c) assert(c)
+#else
+#define VR_ASSERT(c) ((void)0)
+#endif
 
 #include "vr_types.h"
 
@@ -138,7 +148,14 @@ __device__ __forceinline__ uint64_t hash_slot(uint64_t x) {
   return x;
 }
 __device__ __forceinline__ void hash_put(uint64_t* t, uint64_t mask, uint64_t k) {
+  VR_ASSERT(k != ~0ull);
+#ifdef VR_CHECKS
+  uint64_t probes = 0;
+#endif
   for (uint64_t i = hash_slot(k) & mask;; i = (i + 1) & mask) {
+#ifdef VR_CHECKS
+    assert(++probes <= mask + 1);  // (a full table would loop forever)
+#endif
     const unsigned long long prev = atomicCAS((unsigned long long*)(t + i), ~0ull, (unsigned long long)k);
     if (prev == ~0ull || prev == k) return;
   }

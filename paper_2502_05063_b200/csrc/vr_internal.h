@@ -72,6 +72,7 @@ struct DimCounters {   // device counters (unsigned long long each)
   unsigned long long survivors, apparent1, apparent2, cleared, queued, residual, row_next, app_pairs, scanned, scanned2, rows_out;
   unsigned long long next_bound;  // sparse: sum over survivors s of deg_below(min s) (bounds the next dimension)
   unsigned long long exported;    // sharded sparse: apparent cofacets appended to exp_list
+  unsigned long long cand_reads;  // sparse: rank reads of the candidate examination (a1)
 };
 struct HotBuffers {
   uint64_t* qkey;        // phase-2 queue: column keys
