@@ -16,6 +16,9 @@ res = {}
 for r in rows[2:]:
     name = r[h.index("Kernel Name")]
     short = name.split("(")[0].replace("void ", "").replace("vr::", "").replace("(int)", "")
+    if "<" in short:  # the first template argument (the dimension) names the launch: k<3, 4> -> k<3>
+        head, args = short.split("<", 1)
+        short = head + "<" + args.split(",")[0].rstrip(">").strip() + ">"
     b = 0.0
     for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         i = h.index(m)
