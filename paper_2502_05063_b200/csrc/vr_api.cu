@@ -726,6 +726,8 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
   if (P.sparse) {
     const int src = dr.two_level ? d - 2 : d - 1;
     nrows_sp = src <= 0 ? (uint64_t)n : P.rows_count[(size_t)src];
+    if (dr.two_level && nrows_sp >= (1ull << 32))
+      throw VrError(VR_ECAPACITY, "output-sensitive mode: more than 2^32 rows in one dimension");
     bound = d == 1 ? P.m : std::min<uint64_t>(cand, P.next_bound[(size_t)d - 1]);
     if (P.rows_needed(d)) {
       P.rows[(size_t)d].ensure(std::max<uint64_t>(bound, 1) * 16);
