@@ -147,9 +147,11 @@ __device__ __forceinline__ int bm_list(const SparseRows& S, const int (&x)[K], i
 }
 
 // ------------------------------------------------------------------ phase 1 (+ decision)
+// per-warp counters in 32 bits (registers are the kernel's limit), flushed into the 64-bit
+// device counters before any can overflow (maybe_flush after every row)
 struct Acc {
-  unsigned long long surv = 0, app = 0, scan = 0, clr = 0, next_bound = 0;
-  unsigned long long cand = 0;  // rank reads of the candidate examination (list maxima, C(σ) compaction)
+  uint32_t surv = 0, app = 0, scan = 0, clr = 0, next_bound = 0;  // next_bound: per lane
+  uint32_t cand = 0;  // rank reads of the candidate examination (list maxima, C(σ) compaction)
 };
 
 // Lemma 5.3.6 condition 1 over a lane's list cl[0..fill) (descending; ml = m(v), the
@@ -224,7 +226,7 @@ __device__ __forceinline__ int scan_list(const Tables& T, const uint16_t* cv, co
 template <int D>
 __device__ __forceinline__ bool survivor_head(const HotBuffers& B, const SparseRows& S, const int (&s)[D + 1], bool valid,
                                               int nb, uint64_t cidx, Acc& acc) {
-  acc.surv += (unsigned long long)nb;
+  acc.surv += (uint32_t)nb;
   if (S.rows_out) {
     const unsigned long long slot = warp_append(valid, S.rows_out_count);
     if (valid && slot < S.rows_out_cap) S.rows_out[slot] = pack_vertices<D>(s);
@@ -248,7 +250,7 @@ __device__ __forceinline__ void survivor_tail(const Tables& T, const DimParams& 
                                               uint32_t pm_up, const uint32_t (&pm_ex)[D + 1], const int (&s)[D + 1], int w,
                                               uint32_t rs, uint64_t cidx, bool valid, bool cleared, int hitv, int examined,
                                               Acc& acc) {
-  acc.scan += (unsigned long long)__reduce_add_sync(0xffffffffu, (unsigned)examined);
+  acc.scan += __reduce_add_sync(0xffffffffu, (unsigned)examined);
   bool app = false;
   if (hitv >= 0) {
     app = true;
@@ -391,7 +393,7 @@ __device__ void row_general(const Tables& T, const DimParams& p, const HotBuffer
   int nabove = 0;
   int c_fill = bm_list<D>(S, x, c_word, c_mask, cv, SP_LCAP, u1, &nabove);
   list_maxima<D>(T, u, 1, cv, cm, c_fill);
-  acc.cand += (unsigned long long)c_fill * D;
+  acc.cand += (uint32_t)(c_fill * D);
   if (c_word < 0) {  // the whole list fits: the survivors are its tail
     row_from_list<D>(T, p, B, S, u, pm_up, pm_ex, cbase, cv, cm, c_fill, nabove, acc);
     return;
@@ -436,7 +438,7 @@ __device__ void row_general(const Tables& T, const DimParams& p, const HotBuffer
         }
         c_fill = bm_list<D>(S, x, c_word, c_mask, cv, SP_LCAP, 0, nullptr);
         list_maxima<D>(T, u, 1, cv, cm, c_fill);
-        acc.cand += (unsigned long long)c_fill * D;
+        acc.cand += (uint32_t)(c_fill * D);
         c_seg = seg;
       }
       const int h = scan_list(T, cv, cm, c_fill, w, rs, active, examined);
@@ -473,16 +475,22 @@ __device__ __forceinline__ void unpack_row(const uint4* rows, uint64_t r, int (&
 __device__ __forceinline__ void flush_acc(const HotBuffers& B, Acc& acc) {
   const int lane = threadIdx.x & 31;
   if (lane == 0) {
-    if (acc.surv) atomicAdd(&B.ctr->survivors, acc.surv);
-    if (acc.app) atomicAdd(&B.ctr->apparent1, acc.app);
-    if (acc.scan) atomicAdd(&B.ctr->scanned, acc.scan);
-    if (acc.clr) atomicAdd(&B.ctr->cleared, acc.clr);
-    if (acc.cand) atomicAdd(&B.ctr->cand_reads, acc.cand);
+    if (acc.surv) atomicAdd(&B.ctr->survivors, (unsigned long long)acc.surv);
+    if (acc.app) atomicAdd(&B.ctr->apparent1, (unsigned long long)acc.app);
+    if (acc.scan) atomicAdd(&B.ctr->scanned, (unsigned long long)acc.scan);
+    if (acc.clr) atomicAdd(&B.ctr->cleared, (unsigned long long)acc.clr);
+    if (acc.cand) atomicAdd(&B.ctr->cand_reads, (unsigned long long)acc.cand);
   }
   unsigned long long nbsum = acc.next_bound;  // per lane
 #pragma unroll
   for (int o = 16; o; o >>= 1) nbsum += __shfl_xor_sync(0xffffffffu, nbsum, o);
   if (lane == 0 && nbsum) atomicAdd(&B.ctr->next_bound, nbsum);
+  acc = Acc{};
+}
+// flushes when a counter passes 2^30 (a row adds far less)
+__device__ __forceinline__ void maybe_flush(const HotBuffers& B, Acc& acc) {
+  const uint32_t big = acc.surv | acc.app | acc.scan | acc.clr | acc.cand;
+  if (__any_sync(0xffffffffu, (big | acc.next_bound) >= (1u << 30))) flush_acc(B, acc);
 }
 
 // Single level: a row is a (D-1)-simplex σ (a survivor of dimension D-1; the vertices for
@@ -512,6 +520,7 @@ __global__ void __launch_bounds__(SP_THREADS, 4) k_enum_sparse(Tables T, DimPara
         for (int i = 1; i <= D; ++i) u[i] = t[D - i];
       }
       row_general<D>(T, p, B, S, u, s_cv[wi], s_cm[wi], s_w[wi], acc);
+      maybe_flush(B, acc);
     }
   }
   flush_acc(B, acc);
@@ -557,13 +566,13 @@ __global__ void __launch_bounds__(SP_THREADS, MINB) k_enum_sparse2(Tables T, Dim
   const uint32_t top_word_mask = (T.n & 31) ? ((1u << (T.n & 31)) - 1) : 0xffffffffu;
   // work item g = (row g / slices, slice g % slices): slice k takes every slices-th x
   // (few rows with long lists, e.g. D = 2 with vertex rows, are split over warps)
-  const uint64_t NS = (uint64_t)p.slices;
+  const uint32_t NS = (uint32_t)p.slices;  // (rows x slices < 2^32: checked by the launcher / caller)
   uint64_t g0, gend;
   while (next_rows(p, B, nrows * NS, g0, gend)) {
-    for (uint64_t gi = g0; gi < gend; ++gi) {
-      const uint64_t g = gi / NS;
+    for (uint32_t gi = (uint32_t)g0; gi < (uint32_t)gend; ++gi) {
+      const uint32_t g = gi / NS;
       const int slice = (int)(gi - g * NS);
-      const uint64_t r = p.row_begin + g * W + (uint64_t)p.shard_rank;
+      const uint64_t r = p.row_begin + (uint64_t)g * W + (uint64_t)p.shard_rank;
       int u[D + 1];
       u[0] = u[1] = 0;
       if (S.rows_in == nullptr) {  // D = 2: τ is a vertex
@@ -593,6 +602,7 @@ __global__ void __launch_bounds__(SP_THREADS, MINB) k_enum_sparse2(Tables T, Dim
             if ((base + ix) % (int)p.slices != slice) continue;
             u[1] = tv[ix];
             row_general<D>(T, p, B, S, u, cv, cm, M.sw, acc);
+            maybe_flush(B, acc);
           }
           base += nx;
           __syncwarp();
@@ -600,7 +610,7 @@ __global__ void __launch_bounds__(SP_THREADS, MINB) k_enum_sparse2(Tables T, Dim
         continue;
       }
       list_maxima<D>(T, u, 2, tv, tm, tfill);
-      acc.cand += (unsigned long long)tfill * (D - 1);
+      acc.cand += (uint32_t)(tfill * (D - 1));
       // τ's pair maxima and cidx part
       uint32_t pt_up;
       uint32_t pt_ex[D + 1];
@@ -685,7 +695,7 @@ __global__ void __launch_bounds__(SP_THREADS, MINB) k_enum_sparse2(Tables T, Dim
                        __popc(kmb & (rb_n >= 32 ? 0xffffffffu : (rb_n <= 0 ? 0u : ((1u << rb_n) - 1))));
             fill += na + __popc(kmb);
           }
-          acc.cand += (unsigned long long)tfill;  // one rank read R[x][v] per entry of C(τ)
+          acc.cand += (uint32_t)tfill;  // one rank read R[x][v] per entry of C(τ)
           const int ns = fill - first_w;
           if (ns <= 0) continue;  // no d-simplex in this σ's row
           // σ's pair maxima from τ's and the D-1 new edges: [0] pm_up, [1] avoiding x (τ's),
@@ -760,6 +770,7 @@ __global__ void __launch_bounds__(SP_THREADS, MINB) k_enum_sparse2(Tables T, Dim
         __syncwarp();
       }
       __syncwarp();
+      maybe_flush(B, acc);
     }
   }
   flush_acc(B, acc);
@@ -906,6 +917,8 @@ static void enum_sparse_d(const DimParams& p, const Tables& T, const HotBuffers&
       if (blocks > cap) blocks = cap;
       if (blocks < 1) blocks = 1;
       q.grab = rows * (uint64_t)q.slices >= cap * SP_WARPS * 64 ? 4 : 1;
+      if (rows * (uint64_t)q.slices >= (1ull << 32)) q.slices = 1;  // (32-bit work-item indices; rows < 2^32
+                                                                     // is checked by the caller)
       // (tuning: VR_SP_MINB = resident CTAs per SM the registers are budgeted for)
       static const int minb = std::getenv("VR_SP_MINB") ? std::atoi(std::getenv("VR_SP_MINB")) : 4;
       const unsigned bl = (unsigned)std::min<uint64_t>(blocks * (uint64_t)std::max(minb, 4) / 4, (uint64_t)sp_sms() * minb);
