@@ -508,7 +508,10 @@ __global__ void __launch_bounds__(SP_THREADS, 4) k_enum_sparse(Tables T, DimPara
   uint64_t g0, gend;
   while (next_rows(p, B, nrows, g0, gend)) {
     for (uint64_t g = g0; g < gend; ++g) {
-      const uint64_t r = p.row_begin + g * W + (uint64_t)p.shard_rank;
+      // vertex rows from the top down: a vertex's rows grow with its index (its neighbours
+      // below it), so the largest go first (no long tail at the end of the launch)
+      const uint64_t gg = S.rows_in == nullptr ? nrows - 1 - g : g;
+      const uint64_t r = p.row_begin + gg * W + (uint64_t)p.shard_rank;
       int u[D + 1];  // u[1] < ... < u[D] (u[0] unused)
       u[0] = 0;
       if (S.rows_in == nullptr) {
@@ -572,7 +575,8 @@ __global__ void __launch_bounds__(SP_THREADS, MINB) k_enum_sparse2(Tables T, Dim
     for (uint32_t gi = (uint32_t)g0; gi < (uint32_t)gend; ++gi) {
       const uint32_t g = gi / NS;
       const int slice = (int)(gi - g * NS);
-      const uint64_t r = p.row_begin + (uint64_t)g * W + (uint64_t)p.shard_rank;
+      const uint64_t gg = S.rows_in == nullptr ? nrows - 1 - (uint64_t)g : (uint64_t)g;  // (largest vertex rows first)
+      const uint64_t r = p.row_begin + gg * W + (uint64_t)p.shard_rank;
       int u[D + 1];
       u[0] = u[1] = 0;
       if (S.rows_in == nullptr) {  // D = 2: τ is a vertex
