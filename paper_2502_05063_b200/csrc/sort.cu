@@ -704,6 +704,17 @@ __global__ void k_fix_runs(uint64_t* __restrict__ k, uint64_t n, int cbits, unsi
       else atomicOr(overflow, 1u);
       continue;
     }
+    if (len <= 4) {  // the common case (config 5, dimension 3: mean run 2.4): a 4-key network
+      uint64_t a0 = k[i], a1 = k[i + 1], a2 = len > 2 ? k[i + 2] : ~0ull, a3 = len > 3 ? k[i + 3] : ~0ull;
+#define VR_CS(x, y) { const uint64_t lo_ = x < y ? x : y, hi_ = x < y ? y : x; x = lo_; y = hi_; }
+      VR_CS(a0, a1) VR_CS(a2, a3) VR_CS(a0, a2) VR_CS(a1, a3) VR_CS(a1, a2)
+#undef VR_CS
+      k[i] = a0;
+      k[i + 1] = a1;
+      if (len > 2) k[i + 2] = a2;
+      if (len > 3) k[i + 3] = a3;
+      continue;
+    }
     uint64_t v[FIX_RUN_REG];
 #pragma unroll
     for (int a = 0; a < FIX_RUN_REG; ++a) v[a] = a < len ? k[i + (uint64_t)a] : ~0ull;

@@ -103,7 +103,7 @@ __global__ void tb_threshold(const uint32_t* __restrict__ rowmax, int64_t n, flo
 // edges in DEscending index order k = N-1-j, j = TB_TILE * block + ...: a block counts the
 // edges with d <= t of its tile (and validates the input)
 constexpr int TB_THREADS = 256;
-constexpr int TB_TILE = 2048;
+constexpr int TB_TILE = 8192;
 __global__ void tb_edge_count(const float* __restrict__ lt, uint64_t N, TablesOut* __restrict__ out,
                               uint32_t* __restrict__ blk_count) {
   __shared__ uint32_t red[TB_THREADS / 32];
