@@ -115,6 +115,13 @@ typedef struct {
   double ms_residual;      /* host: residual reduction (dim 0: union-find) */
   double ms_transfer;      /* host<->device copies of this dimension's columns / pairs */
   int64_t kernels;         /* VR_KERNEL_* flags of the enumeration kernels this dimension ran */
+  int64_t bytes_l2;        /* algorithmic L2 bytes of the dimension's kernels: 4 per rank read
+                              (vr_plan_dim_timing [5]-[7]) */
+  int64_t bytes_hbm;       /* algorithmic HBM bytes of its outputs: 16 per row kept for a later
+                              dimension, 8 + 16 per residual column (written, then sorted: one
+                              read + write), 24 per column queued for phase 2 */
+  double ms_exchange;      /* sharded runs: wall ms of the dimension's exchanges (clearing input,
+                              residual keys all-gather + merge, deaths broadcast); 0 on one GPU */
 } vr_stats;
 #define VR_KERNEL_ROW 1          /* k_enumerate: one warp per prefix row (dense) */
 #define VR_KERNEL_FLAT 2         /* k_enumerate_flat: flattened (u_1, v_0) chunks (dense) */

@@ -58,7 +58,8 @@ _STAT_TIMES = ["ms_enumerate", "ms_resolve", "ms_sort", "ms_residual", "ms_trans
 
 class _Stats(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int64) for f in _STAT_FIELDS] + [(f, ctypes.c_double) for f in _STAT_TIMES] + \
-               [("kernels", ctypes.c_int64)]
+               [("kernels", ctypes.c_int64), ("bytes_l2", ctypes.c_int64), ("bytes_hbm", ctypes.c_int64),
+                ("ms_exchange", ctypes.c_double)]
 
 
 # vr_stats.kernels flags (include/vr.h)
@@ -178,7 +179,8 @@ def _collect(h) -> Barcode:
         bc.index_pairs.append(ip)
         s = _Stats()
         _check(lib.vr_stats_get(h, d, ctypes.byref(s)))
-        bc.stats.append({f: getattr(s, f) for f in _STAT_FIELDS + _STAT_TIMES + ["kernels"]})
+        bc.stats.append({f: getattr(s, f) for f in _STAT_FIELDS + _STAT_TIMES + ["kernels", "bytes_l2", "bytes_hbm",
+                                                                                "ms_exchange"]})
     return bc
 
 

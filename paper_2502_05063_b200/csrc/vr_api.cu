@@ -926,6 +926,9 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
     dr.decode = (double)(d + 1) * lg * tested;
     dr.decode_phase2 = (double)(d + 1) * lg * queued;
     dr.kernels = kernels;
+    stt.bytes_l2 = (int64_t)(4.0 * (dr.reads_a1 + dr.reads_a5 + dr.reads_a5_phase2));
+    stt.bytes_hbm = (int64_t)(16.0 * (double)(P.sparse && P.rows_needed(d) ? P.rows_count[(size_t)d] : 0) +
+                              24.0 * (double)resid_count + 24.0 * queued);
   }
   P.survivors_total += stt.survivors;
   P.apparent_total += stt.apparent;
@@ -1145,11 +1148,14 @@ void run_distributed(vr_plan& P) {
   for (int d = 1; d <= P.D; ++d) {
     const uint64_t nk = stage_dim_local(P, d);
     const bool active = P.dims[(size_t)d].active;
+    auto tx = std::chrono::steady_clock::now();
     if (active) {
       exchange_clearing(P, d, false);
       if (P.opt.index_pairs) gather_index_pairs(P, d);
     }
     const uint64_t total = active ? exchange_residual(P, d, nk, false) : 0;
+    CUDA_TRY(cudaStreamSynchronize(P.st));
+    double ms_x = ms_since(tx);
     if (P.rank_id == 0) {
       std::vector<uint64_t> hkeys((size_t)total);
       auto tx = std::chrono::steady_clock::now();
@@ -1161,7 +1167,10 @@ void run_distributed(vr_plan& P) {
     // exchange C: rank 0's deaths of dimension d to every rank
     std::vector<uint64_t> deaths;
     if (P.rank_id == 0) deaths = P.deaths;
+    tx = std::chrono::steady_clock::now();
     bcast_words(P, deaths);
+    ms_x += ms_since(tx);
+    P.R->stats[(size_t)d].ms_exchange = ms_x;
     if (P.rank_id != 0) {
       P.deaths = deaths;
       if (active) apply_deaths(P, d);
