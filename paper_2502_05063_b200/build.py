@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvr.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["vr_api.cu", "tables.cu", "sort.cu", "hotpath.cu", "sparse.cu", "hypha.cu", "hypha_host.cpp", "netsimplex.cpp", "w1.cu", "host.cpp", "probe.cu", "comm.cu"]
+SOURCES = ["vr_api.cu", "tables.cu", "sort.cu", "hotpath.cu", "sparse.cu", "hypha.cu", "hypha_host.cpp", "netsimplex.cpp", "w1.cu", "host.cpp", "probe.cu", "comm.cu", "residual_prep.cu"]
 HEADERS = ["vr_common.cuh", "vr_internal.h", "vr_types.h"]
 
 FLAGS = [

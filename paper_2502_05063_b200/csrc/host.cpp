@@ -26,6 +26,7 @@
 #include <immintrin.h>
 #endif
 #include <atomic>
+#include <memory>
 #include <thread>
 #include <functional>
 #include <chrono>
@@ -47,6 +48,7 @@ namespace vr {
 // ------------------------------------------------------------------ dimension 0
 void dim0_union_find(int64_t n, const uint64_t* edges_sorted, uint64_t m, int kbits, HostPairs& out,
                      std::vector<uint64_t>& deaths_sorted) {
+  std::vector<uint64_t>& deaths = deaths_sorted;
   const uint64_t N = (uint64_t)n * (uint64_t)(n - 1) / 2;
   const uint64_t kmask = kbits >= 64 ? ~0ull : ((1ull << kbits) - 1);
   std::vector<int32_t> parent((size_t)n), name((size_t)n);
@@ -59,7 +61,7 @@ void dim0_union_find(int64_t n, const uint64_t* edges_sorted, uint64_t m, int kb
     return x;
   };
   int64_t comps = n;
-  deaths_sorted.clear();
+  deaths.clear();
   for (uint64_t e = 0; e < m && comps > 1; ++e) {
     const uint64_t key = edges_sorted[e];
     const uint64_t k = N - 1 - (key & kmask);  // lower-distance index == edge cidx
@@ -76,13 +78,13 @@ void dim0_union_find(int64_t n, const uint64_t* edges_sorted, uint64_t m, int kb
     int32_t young = name[(size_t)ri] < name[(size_t)rj] ? ri : rj;
     int32_t old = young == ri ? rj : ri;
     out.push(0.0f, diam, (uint64_t)name[(size_t)young], k);
-    deaths_sorted.push_back(k);
+    deaths.push_back(k);
     parent[(size_t)young] = old;
     --comps;
   }
   for (int64_t i = 0; i < n; ++i)
     if (find((int32_t)i) == (int32_t)i) out.push(0.0f, INFINITY, (uint64_t)name[(size_t)i], UINT64_MAX);
-  std::sort(deaths_sorted.begin(), deaths_sorted.end());
+  std::sort(deaths.begin(), deaths.end());
 }
 
 // ------------------------------------------------------------------ residual reduction
@@ -157,42 +159,48 @@ struct Ctx {
     }
   }
   // coboundary of the d-simplex s in lex-decreasing order (Alg 14, reading A2), with ranks.
-  // The rank matrix is symmetric, so R[v][s_q] is read as the contiguous row R[s_q][.].
-  // With a threshold-graph adjacency only the neighbours of the vertex of s with the
-  // fewest neighbours are visited (a cofacet under the threshold needs v adjacent to all
-  // of s), in the same descending order; the cofacet index is then computed in closed
-  // form: with j vertices of s above v, cidx(s ∪ {v}) = A_j + C(v, d+2-j) + B_j.
+  // Dense mode: the rank matrix is symmetric, so R[v][s_q] is read as the contiguous row
+  // R[s_q][.].  Output-sensitive mode (threshold-graph bitmap): only the common neighbours
+  // of s are visited — the AND of its bitmap rows, in the same descending order (a cofacet
+  // under the threshold needs v adjacent to all of s) — with their ranks from the packed
+  // neighbour ranks, and the cofacet index in closed form: with j vertices of s above v,
+  // cidx(s ∪ {v}) = A_j + C(v, d+2-j) + B_j.
   template <class F>
   void cofacets(const int* s, uint64_t cidx, uint32_t rs, F&& emit) const {
-    const uint32_t* rows[16];
-    for (int q = 0; q <= d; ++q) rows[q] = &M.rank[(size_t)s[q] * (size_t)M.n];
-    if (!M.adj_off.empty()) {
+    if (!M.bm.empty()) {  // common neighbours = AND of the bitmap rows, descending
       uint64_t A[17], B[17];
       A[0] = 0;
       for (int j = 0; j <= d; ++j) A[j + 1] = A[j] + M.C(s[j], d + 2 - j);
       B[d + 1] = 0;
       for (int j = d; j >= 0; --j) B[j] = B[j + 1] + M.C(s[j], d + 1 - j);
-      int anchor = s[0];
-      uint32_t best = ~0u;
+      const uint64_t* bw[16];
+      const uint32_t* pre[16];
       for (int q = 0; q <= d; ++q) {
-        const uint32_t dg = M.adj_off[(size_t)s[q] + 1] - M.adj_off[(size_t)s[q]];
-        if (dg < best) { best = dg; anchor = s[q]; }
+        bw[q] = &M.bm[(size_t)s[q] * (size_t)M.bmw];
+        pre[q] = &M.nb_pre[(size_t)s[q] * (size_t)M.bmw];
       }
-      const uint16_t* L = M.adj.data() + M.adj_off[(size_t)anchor];
+      const uint32_t* NR = M.nb_rank.data();
       int j = 0;  // vertices of s above v
-      for (uint32_t k = 0; k < best; ++k) {
-        const int v = L[k];
-        while (j <= d && s[j] > v) ++j;
-        if (j <= d && s[j] == v) continue;
-        uint32_t r = rs;
-        for (int q = 0; q <= d; ++q) r = std::max(r, rows[q][v]);
-        if (r == VR_RINF_H) continue;
-        if (!emit(Entry{r, A[j] + M.C(v, d + 2 - j) + B[j]})) return;
+      for (int64_t w = M.bmw - 1; w >= 0; --w) {
+        uint64_t x = bw[0][w];
+        for (int q = 1; q <= d; ++q) x &= bw[q][w];
+        while (x) {
+          const int b = 63 - __builtin_clzll(x);
+          x ^= 1ull << b;
+          const int v = (int)(w * 64 + b);  // never a vertex of s (no self loops)
+          while (j <= d && s[j] > v) ++j;
+          const uint64_t below = (1ull << b) - 1;
+          uint32_t r = rs;
+          for (int q = 0; q <= d; ++q) r = std::max(r, NR[pre[q][w] + (uint32_t)__builtin_popcountll(bw[q][w] & below)]);
+          if (!emit(Entry{r, A[j] + M.C(v, d + 2 - j) + B[j]})) return;
+        }
       }
       return;
     }
-    // blocks of 8 vertices: the rank maxima of a block in one vector pass, then the
+    // dense: blocks of 8 vertices, the rank maxima of a block in one vector pass, then the
     // (sequential) cofacet-index bookkeeping and the emits
+    const uint32_t* rows[16];
+    for (int q = 0; q <= d; ++q) rows[q] = &M.rank[(size_t)s[q] * (size_t)M.n];
     uint64_t below = cidx, above = 0;
     int k = d + 1, j = 0;
     alignas(32) uint32_t rb[8];
@@ -224,24 +232,30 @@ struct Ctx {
   }
   // first v (descending) not in S (K vertices) with max_{w in S} R[w][v] <= r, or -1
   int64_t first_equal_cofacet_vertex(const int* S, int K, uint32_t r) const {
-    const uint32_t* rows[16];
-    for (int q = 0; q < K; ++q) rows[q] = &M.rank[(size_t)S[q] * (size_t)M.n];
-    if (!M.adj_off.empty()) {
-      int anchor = S[0];
-      uint32_t best = ~0u;
+    if (!M.bm.empty()) {
+      const uint64_t* bw[16];
+      const uint32_t* pre[16];
       for (int q = 0; q < K; ++q) {
-        const uint32_t dg = M.adj_off[(size_t)S[q] + 1] - M.adj_off[(size_t)S[q]];
-        if (dg < best) { best = dg; anchor = S[q]; }
+        bw[q] = &M.bm[(size_t)S[q] * (size_t)M.bmw];
+        pre[q] = &M.nb_pre[(size_t)S[q] * (size_t)M.bmw];
       }
-      const uint16_t* L = M.adj.data() + M.adj_off[(size_t)anchor];
-      for (uint32_t k = 0; k < best; ++k) {
-        const int v = L[k];
-        bool ok = true;
-        for (int q = 0; q < K && ok; ++q) ok = (v != S[q]) && rows[q][v] <= r;
-        if (ok) return v;
+      const uint32_t* NR = M.nb_rank.data();
+      for (int64_t w = M.bmw - 1; w >= 0; --w) {
+        uint64_t x = bw[0][w];
+        for (int q = 1; q < K; ++q) x &= bw[q][w];
+        while (x) {
+          const int b = 63 - __builtin_clzll(x);
+          x ^= 1ull << b;
+          const uint64_t below = (1ull << b) - 1;
+          bool ok = true;
+          for (int q = 0; q < K && ok; ++q) ok = NR[pre[q][w] + (uint32_t)__builtin_popcountll(bw[q][w] & below)] <= r;
+          if (ok) return w * 64 + b;
+        }
       }
       return -1;
     }
+    const uint32_t* rows[16];
+    for (int q = 0; q < K; ++q) rows[q] = &M.rank[(size_t)S[q] * (size_t)M.n];
 #if defined(__x86_64__)
     if (g_host_avx2) return first_equal_dense_avx2(rows, S, K, r, M.n);
 #endif
@@ -258,14 +272,18 @@ struct Ctx {
     int t[16];
     decode(tcidx, d + 2, t);
     int64_t res = -1;
+    uint32_t P[16][16];  // the edge ranks of t, read once
+    for (int a = 0; a < d + 2; ++a)
+      for (int b = a + 1; b < d + 2; ++b) P[a][b] = R(t[a], t[b]);
     // youngest facet: the first in Alg 16 order (drop t[0], t[1], ...) with diameter rt
     for (int j = 0; j < d + 2 && res < 0; ++j) {
       int f[16], m = 0;
       uint32_t df = 0;
       for (int q = 0; q < d + 2; ++q)
         if (q != j) f[m++] = t[q];
-      for (int a = 0; a < m; ++a)
-        for (int b = a + 1; b < m; ++b) df = std::max(df, M.R(f[a], f[b]));
+      for (int a = 0; a < d + 2; ++a)
+        for (int b = a + 1; b < d + 2; ++b)
+          if (a != j && b != j) df = std::max(df, P[a][b]);
       if (df != rt) continue;
       if (first_equal_cofacet_vertex(f, d + 1, rt) == t[j]) {
         uint64_t c = 0;
@@ -276,11 +294,12 @@ struct Ctx {
     }
     return res;
   }
-  uint32_t diam_rank(const int* s) const {
-    uint32_t r = 0;
-    for (int a = 0; a <= d; ++a)
-      for (int b = a + 1; b <= d; ++b) r = std::max(r, M.R(s[a], s[b]));
-    return r;
+  // R(u, v) from the packed neighbour ranks when present (u, v adjacent: cache-resident),
+  // else from the n*n matrix
+  uint32_t R(int u, int v) const {
+    if (M.nb_pre.empty()) return M.R(u, v);
+    const size_t w = (size_t)u * (size_t)M.bmw + (size_t)(v >> 6);
+    return M.nb_rank[M.nb_pre[w] + (uint32_t)__builtin_popcountll(M.bm[w] & ((1ull << (v & 63)) - 1))];
   }
 };
 
@@ -416,7 +435,8 @@ struct BinHeap {
 
 template <class HeapT>
 void residual_reduce_t(const HostMatrix& M, int d, uint32_t maxr, int cbits, const uint64_t* keys, uint64_t nkeys,
-                       int mode, HeapT& W, HostPairs& out, std::vector<uint64_t>& deaths_sorted, ResidualStats& st) {
+                       const ResidualHints* hints, int mode, HeapT& W, HostPairs& out, std::vector<uint64_t>& deaths,
+                       ResidualStats& st) {
   Ctx cx(M, d);
   const uint64_t cmask = cbits >= 64 ? ~0ull : ((1ull << cbits) - 1);
   auto colkey = [&](uint32_t r, uint64_t c) -> uint64_t { return ((uint64_t)(maxr - r) << cbits) | c; };
@@ -426,7 +446,7 @@ void residual_reduce_t(const HostMatrix& M, int d, uint32_t maxr, int cbits, con
   U64Map pivot_col((size_t)nkeys + 16);             // row cidx -> index into vcol
   U64Map app_memo(1024);                            // row cidx -> apparent partner cidx or -1
   std::vector<uint64_t> work_v;
-  deaths_sorted.clear();
+  deaths.clear();
   int s[16], f[16];
 
   auto apparent_of = [&](const Entry& e) -> int64_t {
@@ -453,7 +473,16 @@ void residual_reduce_t(const HostMatrix& M, int d, uint32_t maxr, int cbits, con
     // initial coboundary; emergent check on the first equal-diameter cofacet (§5.2.11)
     bool check = true, emergent = false;
     Entry first{0, 0};
-    cx.cofacets(s, sc, rs, [&](const Entry& e) {
+    if (hints) {  // the first equal-diameter cofacet and its apparent claim, precomputed
+      const uint64_t t = hints->first[c];
+      int64_t col;
+      check = false;
+      if (t != UINT64_MAX && !hints->claimed[c] && !pivot_col.get(t, col)) {
+        first = Entry{rs, t};
+        emergent = true;
+      }
+    }
+    if (!emergent) cx.cofacets(s, sc, rs, [&](const Entry& e) {
       if (check && e.r == rs) {
         int64_t col;
         if (!pivot_col.get(e.cidx, col) && apparent_of(e) < 0) { first = e; emergent = true; return false; }
@@ -466,7 +495,7 @@ void residual_reduce_t(const HostMatrix& M, int d, uint32_t maxr, int cbits, con
     if (emergent) {
       ++st.emergent;
       out.push(birth, M.value[first.r], sc, first.cidx);
-      deaths_sorted.push_back(first.cidx);
+      deaths.push_back(first.cidx);
       pivot_col.put(first.cidx, (int64_t)vcol.size());
       vcol.push_back({vpool.size(), 1});
       vpool.push_back(key);
@@ -491,18 +520,16 @@ void residual_reduce_t(const HostMatrix& M, int d, uint32_t maxr, int cbits, con
       } else {
         const int64_t a = apparent_of(pe);
         if (a < 0) break;  // unclaimed pivot
-        int fv[16];
-        cx.decode((uint64_t)a, d + 1, fv);
-        const uint32_t fr = cx.diam_rank(fv);
-        push_coboundary((uint64_t)a, fr);
-        if (mode == 0) work_v.push_back(colkey(fr, (uint64_t)a));
+        // an apparent pair has zero persistence: diam(a) = diam(pivot row)
+        push_coboundary((uint64_t)a, pe.r);
+        if (mode == 0) work_v.push_back(colkey(pe.r, (uint64_t)a));
       }
       ++st.additions;
       have = W.pivot(pe.r, pe.cidx);
     }
     if (have) {
       out.push(birth, M.value[pe.r], sc, pe.cidx);
-      deaths_sorted.push_back(pe.cidx);
+      deaths.push_back(pe.cidx);
       pivot_col.put(pe.cidx, (int64_t)vcol.size());
       const size_t off = vpool.size();
       if (mode == 0 && work_v.size() > 1) {
@@ -523,51 +550,62 @@ void residual_reduce_t(const HostMatrix& M, int d, uint32_t maxr, int cbits, con
       out.push(birth, INFINITY, sc, UINT64_MAX);  // zero column: essential class
     }
   }
-  std::sort(deaths_sorted.begin(), deaths_sorted.end());
   st.apparent_checks += cx.apparent_checks;
 }
 
 // ------------------------------------------------------------------ parallel (speculative)
-// Reduction-matrix mode on T threads with IN-ORDER COMMIT.  Threads take columns in
-// coboundary order and reduce them concurrently against the pivots committed so far
-// (every addition of an earlier column with the same pivot is a step the standard
-// algorithm, Alg 11, could take).  A column may only claim its final pivot when every
-// earlier column has committed: it waits for its turn, re-checks the pivot against the
-// now complete table of earlier pivots, keeps reducing if needed, then commits.  The
-// committed pivots are therefore exactly the sequential algorithm's.
+// Reduction-matrix mode on T threads with IN-ORDER COMMIT.  The columns (in coboundary
+// order) are cut into blocks of B; a thread takes a block and first reduces each of its
+// columns speculatively against the pivots committed so far (every addition of an earlier
+// column with the same pivot is a step the standard algorithm, Alg 11, could take), keeping
+// each column's working heap.  It then waits until every earlier block has committed and
+// commits its columns in order: re-check the pivot against the now complete table of earlier
+// pivots, keep reducing if needed, claim it.  The committed pivots are therefore exactly the
+// sequential algorithm's; one hand-off between threads per block, not per column.
 struct ConcPivotMap {  // insert-only, one writer at a time (the committing column)
-  std::vector<std::atomic<uint64_t>> k;
-  std::vector<int64_t> v;
+  struct Slot {
+    std::atomic<uint64_t> k;
+    int64_t v;
+  };
+  std::unique_ptr<Slot[]> t;  // key and value in one slot: one cache line per probe
   size_t mask;
   explicit ConcPivotMap(size_t cap) {
     size_t c = 16;
-    while (c < cap * 2) c <<= 1;
-    k = std::vector<std::atomic<uint64_t>>(c);
-    for (auto& x : k) x.store(~0ull, std::memory_order_relaxed);
-    v.assign(c, -1);
+    while (c < cap + cap / 2) c <<= 1;  // load <= 2/3
+    t.reset(new Slot[c]);
+    for (size_t i = 0; i < c; ++i) {
+      t[i].k.store(~0ull, std::memory_order_relaxed);
+      t[i].v = -1;
+    }
     mask = c - 1;
   }
+  void prefetch(uint64_t key) const { __builtin_prefetch(&t[U64Map::h(key) & mask]); }
   bool get(uint64_t key, int64_t& out) const {
     for (size_t i = U64Map::h(key) & mask;; i = (i + 1) & mask) {
-      const uint64_t x = k[i].load(std::memory_order_acquire);
-      if (x == key) { out = v[i]; return true; }
+      const uint64_t x = t[i].k.load(std::memory_order_acquire);
+      if (x == key) { out = t[i].v; return true; }
       if (x == ~0ull) return false;
     }
   }
-  void put(uint64_t key, int64_t val) {
+  // insert key -> val unless present (then false): one probe sequence
+  bool put_if_absent(uint64_t key, int64_t val) {
     for (size_t i = U64Map::h(key) & mask;; i = (i + 1) & mask) {
-      if (k[i].load(std::memory_order_relaxed) == ~0ull) {
-        v[i] = val;
-        k[i].store(key, std::memory_order_release);
-        return;
+      const uint64_t x = t[i].k.load(std::memory_order_relaxed);
+      if (x == key) return false;
+      if (x == ~0ull) {
+        t[i].v = val;
+        t[i].k.store(key, std::memory_order_release);
+        return true;
       }
     }
   }
+  void put(uint64_t key, int64_t val) { put_if_absent(key, val); }
 };
 
 template <class K>
 void residual_reduce_par(const HostMatrix& M, int d, uint32_t maxr, int cbits, const uint64_t* keys, uint64_t nkeys, int cb,
-                         int nthreads, HostPairs& out, std::vector<uint64_t>& deaths_sorted, ResidualStats& stats) {
+                         const ResidualHints* hints, int nthreads, HostPairs& out, std::vector<uint64_t>& deaths,
+                         ResidualStats& stats) {
   const uint64_t cmask = cbits >= 64 ? ~0ull : ((1ull << cbits) - 1);
   struct ColOut {
     uint32_t death_r = 0;
@@ -576,15 +614,29 @@ void residual_reduce_par(const HostMatrix& M, int d, uint32_t maxr, int cbits, c
     int64_t adds = 0, cobs = 0;
   };
   std::vector<ColOut> res((size_t)nkeys);
-  std::vector<std::vector<uint64_t>> vcols((size_t)nkeys);
+  // reduction columns V_j = {keys[j]} + vextra[j] (empty for most columns: no allocation)
+  std::vector<std::vector<uint64_t>> vextra((size_t)nkeys);
   ConcPivotMap pivots((size_t)nkeys + 16);
-  std::atomic<uint64_t> next_commit{0}, next_col{0};
+  // block size: whole blocks are speculated by one thread, so small blocks where the
+  // columns are few (and long: dimension 1), up to 32 where they are many and short
+  int64_t B = std::max<int64_t>(1, std::min<int64_t>(32, (int64_t)(nkeys / ((uint64_t)nthreads * 256))));
+  if (const char* e = std::getenv("VR_RESIDUAL_BLOCK")) B = std::max<int64_t>(1, std::atoll(e));
+  const uint64_t nblocks = (nkeys + (uint64_t)B - 1) / (uint64_t)B;
+  std::atomic<uint64_t> next_commit{0}, next_block{0};
 
   auto worker = [&]() {
     Ctx cx(M, d);
     U64Map app_memo(1024);
-    RadixHeap<K> W(maxr, cb);
-    std::vector<uint64_t> work_v;
+    // per column of the block: its working heap, its reduction column, its state
+    std::vector<RadixHeap<K>> heaps;
+    heaps.reserve((size_t)B);
+    for (int64_t i = 0; i < B; ++i) heaps.emplace_back(maxr, cb);
+    std::vector<std::vector<uint64_t>> works((size_t)B);
+    struct St {
+      Entry pe, first;
+      bool have, emergent;
+    };
+    std::vector<St> sts((size_t)B);
     int s[16], f[16];
     auto apparent_of = [&](const Entry& e) -> int64_t {
       int64_t a;
@@ -593,112 +645,140 @@ void residual_reduce_par(const HostMatrix& M, int d, uint32_t maxr, int cbits, c
       app_memo.put(e.cidx, a);
       return a;
     };
-    auto wait_turn = [&](uint64_t j) {
-      int spins = 0;
-      while (next_commit.load(std::memory_order_acquire) != j) {
-        if (++spins > 64) std::this_thread::yield();
-      }
-    };
-    for (;;) {
-      const uint64_t j = next_col.fetch_add(1, std::memory_order_relaxed);
-      if (j >= nkeys) break;
+    // reduce column j's heap while its pivot is claimed by a committed column or an
+    // apparent pair
+    auto reduce = [&](uint64_t j, RadixHeap<K>& W, std::vector<uint64_t>& work_v, St& S) {
       ColOut& R = res[(size_t)j];
-      const uint64_t key = keys[j];
-      const uint32_t rs = maxr - (uint32_t)(key >> cbits);
-      const uint64_t sc = key & cmask;
-      cx.decode(sc, d + 1, s);
-      W.clear();
-      work_v.clear();
-      work_v.push_back(key);
       auto push_coboundary = [&](uint64_t cidx, uint32_t r) {
         ++R.cobs;
         cx.decode(cidx, d + 1, f);
         cx.cofacets(f, cidx, r, [&](const Entry& e) { W.push(e.r, e.cidx); return true; });
       };
-      // initial coboundary with the emergent check (§5.2.11), speculative
-      bool check = true, emergent = false;
-      Entry first{0, 0};
-      cx.cofacets(s, sc, rs, [&](const Entry& e) {
-        if (check && e.r == rs) {
-          int64_t col;
-          if (!pivots.get(e.cidx, col) && apparent_of(e) < 0) { first = e; emergent = true; return false; }
-          check = false;
-        }
-        W.push(e.r, e.cidx);
-        return true;
-      });
-      if (emergent) {
-        wait_turn(j);
+      while (S.have) {
         int64_t col;
-        if (!pivots.get(first.cidx, col)) {
-          R.emergent = true;
-          R.death_r = first.r;
-          R.death_cidx = first.cidx;
-          vcols[(size_t)j].assign(1, key);
-          pivots.put(first.cidx, (int64_t)j);
-          next_commit.store(j + 1, std::memory_order_release);
-          continue;
+        if (pivots.get(S.pe.cidx, col)) {
+          const uint64_t k0 = keys[(size_t)col];
+          push_coboundary(k0 & cmask, maxr - (uint32_t)(k0 >> cbits));
+          work_v.push_back(k0);
+          for (const uint64_t vk : vextra[(size_t)col]) {
+            push_coboundary(vk & cmask, maxr - (uint32_t)(vk >> cbits));
+            work_v.push_back(vk);
+          }
+        } else {
+          const int64_t a = apparent_of(S.pe);
+          if (a < 0) break;
+          // an apparent pair has zero persistence: diam(a) = diam(pivot row)
+          push_coboundary((uint64_t)a, S.pe.r);
+          work_v.push_back(((uint64_t)(maxr - S.pe.r) << cbits) | (uint64_t)a);
         }
-        // an earlier column took that row meanwhile: reduce normally (we hold the turn)
+        ++R.adds;
+        S.have = W.pivot(S.pe.r, S.pe.cidx);
+      }
+    };
+    for (;;) {
+      const uint64_t blk = next_block.fetch_add(1, std::memory_order_relaxed);
+      if (blk >= nblocks) break;
+      const uint64_t j0 = blk * (uint64_t)B, j1 = std::min(nkeys, j0 + (uint64_t)B);
+      // phase 1: speculative, against the pivots committed so far
+      for (uint64_t j = j0; j < j1; ++j) {
+        const size_t i = (size_t)(j - j0);
+        RadixHeap<K>& W = heaps[i];
+        St& S = sts[i];
+        const uint64_t key = keys[j];
+        const uint32_t rs = maxr - (uint32_t)(key >> cbits);
+        const uint64_t sc = key & cmask;
         W.clear();
-        cx.cofacets(s, sc, rs, [&](const Entry& e) { W.push(e.r, e.cidx); return true; });
-      }
-      Entry pe{0, 0};
-      bool have = W.pivot(pe.r, pe.cidx);
-      bool my_turn = emergent;
-      for (;;) {
-        while (have) {
-          int64_t col;
-          if (pivots.get(pe.cidx, col)) {
-            for (const uint64_t vk : vcols[(size_t)col]) {
-              push_coboundary(vk & cmask, maxr - (uint32_t)(vk >> cbits));
-              work_v.push_back(vk);
-            }
-          } else {
-            const int64_t a = apparent_of(pe);
-            if (a < 0) break;
-            int fv[16];
-            cx.decode((uint64_t)a, d + 1, fv);
-            const uint32_t fr = cx.diam_rank(fv);
-            push_coboundary((uint64_t)a, fr);
-            work_v.push_back(((uint64_t)(maxr - fr) << cbits) | (uint64_t)a);
-          }
-          ++R.adds;
-          have = W.pivot(pe.r, pe.cidx);
-        }
-        if (my_turn) break;
-        wait_turn(j);  // every earlier column has committed: the pivot table is final for us
-        my_turn = true;
+        works[i].assign(1, key);
+        S.emergent = false;
+        S.have = false;
+        // emergent check on the first equal-diameter cofacet (§5.2.11)
+        bool check = true;
         int64_t col;
-        if (have && pivots.get(pe.cidx, col)) continue;
-        if (have && apparent_of(pe) >= 0) continue;
-        break;
-      }
-      if (have) {
-        R.death_r = pe.r;
-        R.death_cidx = pe.cidx;
-        auto& V = vcols[(size_t)j];
-        V.clear();
-        V.push_back(key);
-        if (work_v.size() > 1) {
-          std::sort(work_v.begin() + 1, work_v.end());
-          for (size_t i = 1; i < work_v.size();) {
-            size_t q = i;
-            while (q < work_v.size() && work_v[q] == work_v[i]) ++q;
-            if (((q - i) & 1) && work_v[i] != key) V.push_back(work_v[i]);
-            i = q;
+        if (hints) {
+          const uint64_t t = hints->first[j];
+          check = false;
+          if (t != UINT64_MAX && !hints->claimed[j] && !pivots.get(t, col)) {
+            S.first = Entry{rs, t};
+            S.emergent = true;
+            continue;  // decided at commit by one lookup
           }
         }
-        pivots.put(pe.cidx, (int64_t)j);
+        cx.decode(sc, d + 1, s);
+        cx.cofacets(s, sc, rs, [&](const Entry& e) {
+          if (check && e.r == rs) {
+            int64_t c2;
+            if (!pivots.get(e.cidx, c2) && apparent_of(e) < 0) { S.first = e; S.emergent = true; return false; }
+            check = false;
+          }
+          W.push(e.r, e.cidx);
+          return true;
+        });
+        if (S.emergent) continue;
+        S.have = W.pivot(S.pe.r, S.pe.cidx);
+        reduce(j, W, works[i], S);
       }
-      next_commit.store(j + 1, std::memory_order_release);
+      // phase 2: wait for every earlier block, then commit in order
+      if (hints)
+        for (uint64_t j = j0; j < j1; ++j)
+          if (sts[(size_t)(j - j0)].emergent) pivots.prefetch(sts[(size_t)(j - j0)].first.cidx);
+      {
+        int spins = 0;
+        while (next_commit.load(std::memory_order_acquire) != blk) {
+          if (++spins > 1024) std::this_thread::yield();
+        }
+      }
+      for (uint64_t j = j0; j < j1; ++j) {
+        const size_t i = (size_t)(j - j0);
+        RadixHeap<K>& W = heaps[i];
+        St& S = sts[i];
+        ColOut& R = res[(size_t)j];
+        const uint64_t key = keys[j];
+        if (S.emergent) {
+          if (pivots.put_if_absent(S.first.cidx, (int64_t)j)) {
+            R.emergent = true;
+            R.death_r = S.first.r;
+            R.death_cidx = S.first.cidx;
+            continue;
+          }
+          // an earlier column took that row: the full coboundary, reduced normally
+          const uint32_t rs = maxr - (uint32_t)(key >> cbits);
+          const uint64_t sc = key & cmask;
+          cx.decode(sc, d + 1, s);
+          W.clear();
+          cx.cofacets(s, sc, rs, [&](const Entry& e) { W.push(e.r, e.cidx); return true; });
+          S.have = W.pivot(S.pe.r, S.pe.cidx);
+        }
+        reduce(j, W, works[i], S);  // the table of earlier pivots is final now
+        if (S.have) {
+          R.death_r = S.pe.r;
+          R.death_cidx = S.pe.cidx;
+          auto& V = vextra[(size_t)j];
+          std::vector<uint64_t>& work_v = works[i];
+          if (work_v.size() > 1) {
+            std::sort(work_v.begin() + 1, work_v.end());
+            for (size_t a = 1; a < work_v.size();) {
+              size_t q = a;
+              while (q < work_v.size() && work_v[q] == work_v[a]) ++q;
+              if (((q - a) & 1) && work_v[a] != key) V.push_back(work_v[a]);
+              a = q;
+            }
+          }
+          pivots.put(S.pe.cidx, (int64_t)j);
+        }
+      }
+      next_commit.store(blk + 1, std::memory_order_release);
     }
   };
   std::vector<std::thread> pool;
   for (int t = 0; t < nthreads; ++t) pool.emplace_back(worker);
   for (auto& th : pool) th.join();
 
-  deaths_sorted.clear();
+  deaths.clear();
+  deaths.reserve((size_t)nkeys);
+  out.birth.reserve(out.birth.size() + (size_t)nkeys);
+  out.death.reserve(out.death.size() + (size_t)nkeys);
+  out.birth_cidx.reserve(out.birth_cidx.size() + (size_t)nkeys);
+  out.death_cidx.reserve(out.death_cidx.size() + (size_t)nkeys);
   for (uint64_t j = 0; j < nkeys; ++j) {
     const ColOut& R = res[(size_t)j];
     const uint32_t rs = maxr - (uint32_t)(keys[j] >> cbits);
@@ -708,18 +788,40 @@ void residual_reduce_par(const HostMatrix& M, int d, uint32_t maxr, int cbits, c
     stats.emergent += R.emergent;
     if (R.death_cidx != UINT64_MAX) {
       out.push(M.value[rs], M.value[R.death_r], sc, R.death_cidx);
-      deaths_sorted.push_back(R.death_cidx);
+      deaths.push_back(R.death_cidx);
     } else {
       out.push(M.value[rs], INFINITY, sc, UINT64_MAX);
     }
   }
-  std::sort(deaths_sorted.begin(), deaths_sorted.end());
 }
 
 }  // namespace
 
+void residual_hints_host(const HostMatrix& M, int d, uint32_t maxr, int cbits, const uint64_t* keys, uint64_t nkeys,
+                         uint64_t* first, uint8_t* claimed) {
+  Ctx cx(M, d);
+  const uint64_t cmask = cbits >= 64 ? ~0ull : ((1ull << cbits) - 1);
+  int s[16], t[16];
+  for (uint64_t c = 0; c < nkeys; ++c) {
+    const uint32_t rs = maxr - (uint32_t)(keys[c] >> cbits);
+    cx.decode(keys[c] & cmask, d + 1, s);
+    first[c] = UINT64_MAX;
+    claimed[c] = 0;
+    const int64_t v = cx.first_equal_cofacet_vertex(s, d + 1, rs);
+    if (v < 0) continue;
+    int m = 0, q = 0;
+    for (; q <= d && s[q] > v; ++q) t[m++] = s[q];
+    t[m++] = (int)v;
+    for (; q <= d; ++q) t[m++] = s[q];
+    uint64_t tc = 0;
+    for (int p = 0; p < m; ++p) tc += M.C(t[p], m - p);
+    first[c] = tc;
+    claimed[c] = cx.apparent_partner(tc, rs) >= 0;
+  }
+}
+
 void residual_reduce(const HostMatrix& M, int d, uint32_t maxr, int cbits, const uint64_t* keys, uint64_t nkeys, int mode,
-                     HostPairs& out, std::vector<uint64_t>& deaths_sorted, ResidualStats& st) {
+                     HostPairs& out, std::vector<uint64_t>& deaths, ResidualStats& st, const ResidualHints* hints) {
   // row keys pack (rank, ~cofacet cidx): 64 bits when they fit, else 128
   const uint64_t cof = M.C(M.n, d + 2);
   int cb = 1;
@@ -730,25 +832,25 @@ void residual_reduce(const HostMatrix& M, int d, uint32_t maxr, int cbits, const
   int nthreads = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
   if (const char* e = std::getenv("VR_RESIDUAL_THREADS")) nthreads = std::max(1, std::atoi(e));
   if (mode == 0 && nthreads > 1 && nkeys >= 64) {
-    if (rb + cb <= 64) residual_reduce_par<uint64_t>(M, d, maxr, cbits, keys, nkeys, cb, nthreads, out, deaths_sorted, st);
-    else residual_reduce_par<u128>(M, d, maxr, cbits, keys, nkeys, cb, nthreads, out, deaths_sorted, st);
+    if (rb + cb <= 64) residual_reduce_par<uint64_t>(M, d, maxr, cbits, keys, nkeys, cb, hints, nthreads, out, deaths, st);
+    else residual_reduce_par<u128>(M, d, maxr, cbits, keys, nkeys, cb, hints, nthreads, out, deaths, st);
     return;
   }
   if (rb + cb <= 64) {
     if (mode == 0) {
       RadixHeap<uint64_t> W(maxr, cb);
-      residual_reduce_t(M, d, maxr, cbits, keys, nkeys, mode, W, out, deaths_sorted, st);
+      residual_reduce_t(M, d, maxr, cbits, keys, nkeys, hints, mode, W, out, deaths, st);
     } else {
       BinHeap<uint64_t> W(maxr, cb);
-      residual_reduce_t(M, d, maxr, cbits, keys, nkeys, mode, W, out, deaths_sorted, st);
+      residual_reduce_t(M, d, maxr, cbits, keys, nkeys, hints, mode, W, out, deaths, st);
     }
   } else {
     if (mode == 0) {
       RadixHeap<u128> W(maxr, cb);
-      residual_reduce_t(M, d, maxr, cbits, keys, nkeys, mode, W, out, deaths_sorted, st);
+      residual_reduce_t(M, d, maxr, cbits, keys, nkeys, hints, mode, W, out, deaths, st);
     } else {
       BinHeap<u128> W(maxr, cb);
-      residual_reduce_t(M, d, maxr, cbits, keys, nkeys, mode, W, out, deaths_sorted, st);
+      residual_reduce_t(M, d, maxr, cbits, keys, nkeys, hints, mode, W, out, deaths, st);
     }
   }
 }

@@ -298,6 +298,8 @@ struct vr_plan {
   bool sparse = false;
   DevBuf bm, deg, deg_below, bound;  // threshold-graph bitmap (n x nw words), degrees
   int32_t nw = 0;
+  DevBuf nb_pre, nb_rank, nb_ctr;     // packed neighbour ranks for the host (residual_prep.cu)
+  DevBuf h_first, h_claimed;          // residual hints of the current dimension
   std::vector<DevBuf> rows;           // rows[d] = packed d-simplex survivors (rows of d+1)
   std::vector<uint64_t> rows_count;   // survivors written per dimension
   std::vector<uint64_t> rows_cap;
@@ -440,7 +442,7 @@ struct SectionTimer {
 };
 
 // ------------------------------------------------------------------ the run, in stages
-// stage_setup        binomials, a0 tables, host copies, dimension 0, sparse adjacency,
+// stage_setup        binomials, a0 tables, host copies, dimension 0, sparse host graph,
 //                    clearing bitmaps, dimension-1 clearing input
 // stage_dim_local    this rank's shard of dimension d on the device (enumerate, apparent,
 //                    clearing, compaction, local radix sort); leaves the sorted residual
@@ -559,10 +561,6 @@ void stage_setup(vr_plan& P) {
   // (copies on the plan's stream: a legacy-default-stream cudaMemcpy does not wait for work
   // on the non-blocking streams the library uses)
   if (P.m) CUDA_TRY(cudaMemcpyAsync(h_edges.data(), sorted, (size_t)P.m * 8, cudaMemcpyDeviceToHost, st));
-  if (D >= 1 && P.m) {
-    M.rank.resize((size_t)n * (size_t)n);
-    CUDA_TRY(cudaMemcpyAsync(M.rank.data(), P.rank.p, M.rank.size() * 4, cudaMemcpyDeviceToHost, st));
-  }
   CUDA_TRY(cudaStreamSynchronize(st));
   M.value.resize((size_t)P.m);
   for (uint64_t r = 0; r < P.m; ++r) {
@@ -570,7 +568,7 @@ void stage_setup(vr_plan& P) {
     std::memcpy(&M.value[(size_t)r], &fb, 4);
   }
   const double ms_tx0 = ms_since(tx0);
-  ST.mark("D2H edges + rank matrix");
+  ST.mark("D2H edges");
 
   // ---------------- dimension 0 (replicated on every rank: cheap, §5.2.5)
   auto t0 = std::chrono::steady_clock::now();
@@ -608,31 +606,37 @@ void stage_setup(vr_plan& P) {
       P.rows_count.assign((size_t)D + 2, 0);
       P.rows_cap.assign((size_t)D + 2, 0);
       P.next_bound.assign((size_t)D + 2, 0);
-      // the host residual walks the same threshold graph: neighbour lists (descending)
-      // from the bitmap
+      // the host residual walks the same threshold graph: the bitmap rows (64-bit words)
+      // and the packed neighbour ranks instead of the n x n rank matrix
       auto ta = std::chrono::steady_clock::now();
-      std::vector<uint32_t> hbm((size_t)n * (size_t)P.nw);
-      CUDA_TRY(cudaMemcpyAsync(hbm.data(), P.bm.p, hbm.size() * 4, cudaMemcpyDeviceToHost, st));
+      const int64_t bmw = P.nw / 2;
+      P.nb_pre.ensure((size_t)n * (size_t)bmw * 4);
+      P.nb_rank.ensure(std::max<size_t>(2 * (size_t)P.m, 1) * 4);
+      P.nb_ctr.ensure(4);
+      vr::launch_neighbour_ranks(P.rank.as<uint32_t>(), (int)n, P.bm.as<uint32_t>(), P.nw, P.deg.as<uint32_t>(),
+                                 P.nb_ctr.as<uint32_t>(), P.nb_pre.as<uint32_t>(), P.nb_rank.as<uint32_t>(), st,
+                                 &P.launches);
+      CUDA_TRY(cudaGetLastError());
+      M.bmw = bmw;
+      M.bm.resize((size_t)n * (size_t)bmw);
+      M.nb_pre.resize((size_t)n * (size_t)bmw);
+      M.nb_rank.resize(2 * (size_t)P.m);
+      CUDA_TRY(cudaMemcpyAsync(M.bm.data(), P.bm.p, M.bm.size() * 8, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaMemcpyAsync(M.nb_pre.data(), P.nb_pre.p, M.nb_pre.size() * 4, cudaMemcpyDeviceToHost, st));
+      if (P.m) CUDA_TRY(cudaMemcpyAsync(M.nb_rank.data(), P.nb_rank.p, M.nb_rank.size() * 4, cudaMemcpyDeviceToHost, st));
       CUDA_TRY(cudaStreamSynchronize(st));
-      M.adj_off.assign((size_t)n + 1, 0);
-      M.adj.clear();
-      M.adj.reserve(2 * (size_t)P.m);
-      for (int64_t v = 0; v < n; ++v) {
-        const uint32_t* row = hbm.data() + (size_t)v * (size_t)P.nw;
-        for (int k = P.nw - 1; k >= 0; --k) {
-          uint32_t x = row[k];
-          while (x) {
-            const int b = 31 - __builtin_clz(x);
-            M.adj.push_back((uint16_t)(32 * k + b));
-            x &= ~(1u << b);
-          }
-        }
-        M.adj_off[(size_t)v + 1] = (uint32_t)M.adj.size();
-      }
       R->stats[0].ms_transfer += ms_since(ta);
     }
   }
-  ST.mark("adjacency");
+  // dense mode: the host scans read the n x n rank matrix (also dumped for the tools)
+  if (D >= 1 && P.m && (!P.sparse || std::getenv("VR_DUMP_RESIDUAL"))) {
+    auto ta = std::chrono::steady_clock::now();
+    M.rank.resize((size_t)n * (size_t)n);
+    CUDA_TRY(cudaMemcpyAsync(M.rank.data(), P.rank.p, M.rank.size() * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    R->stats[0].ms_transfer += ms_since(ta);
+  }
+  ST.mark("host graph");
 
   // ---------------- clearing bitmaps (one bit per d-simplex index) where they fit
   P.dims.clear();
@@ -951,9 +955,29 @@ void apply_deaths(vr_plan& P, int d) {
   P.R->stats[(size_t)d].ms_transfer += ms_since(tx);
 }
 
+// The residual hints (residual_prep.cu) of dimension d's sorted columns dkeys (device),
+// launched on the plan's stream and copied into first/claimed (the caller synchronises).
+// VR_NO_RESIDUAL_HINTS=1: none (the host runs the emergent test itself).
+bool residual_hints(vr_plan& P, int d, const uint64_t* dkeys, uint64_t nk, std::vector<uint64_t>& first,
+                    std::vector<uint8_t>& claimed) {
+  if (std::getenv("VR_NO_RESIDUAL_HINTS") || nk == 0) return false;
+  first.resize((size_t)nk);
+  claimed.resize((size_t)nk);
+  P.h_first.ensure((size_t)nk * 8);
+  P.h_claimed.ensure((size_t)nk);
+  vr::launch_residual_hints(P.rank.as<uint32_t>(), P.binom.as<uint64_t>(), (int)P.n, P.kmax, d,
+                            P.sparse ? P.bm.as<uint32_t>() : nullptr, P.nw, dkeys, nk, P.maxr, P.dims[(size_t)d].p.cbits,
+                            P.h_first.as<uint64_t>(), P.h_claimed.as<uint8_t>(), P.st, &P.launches);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(first.data(), P.h_first.p, (size_t)nk * 8, cudaMemcpyDeviceToHost, P.st));
+  CUDA_TRY(cudaMemcpyAsync(claimed.data(), P.h_claimed.p, (size_t)nk, cudaMemcpyDeviceToHost, P.st));
+  return true;
+}
+
 // Host residual of dimension d on the sorted residual columns (all ranks' columns when
 // distributed); deaths -> the clearing input of dimension d+1.
-void stage_dim_finish(vr_plan& P, int d, const uint64_t* keys, uint64_t nkeys) {
+void stage_dim_finish(vr_plan& P, int d, const uint64_t* keys, uint64_t nkeys, const vr::ResidualHints* hints,
+                      double ms_prep) {
   SectionTimer ST;
   vr_result* R = P.R.get();
   const int D = P.D;
@@ -968,8 +992,10 @@ void stage_dim_finish(vr_plan& P, int d, const uint64_t* keys, uint64_t nkeys) {
   }
   auto tr = std::chrono::steady_clock::now();
   vr::ResidualStats rst;
-  vr::residual_reduce(P.M, d, P.maxr, dr.p.cbits, keys, nkeys, P.opt.residual_mode, P.hp[(size_t)d], P.deaths, rst);
-  stt.ms_residual = ms_since(tr);
+  vr::residual_reduce(P.M, d, P.maxr, dr.p.cbits, keys, nkeys, P.opt.residual_mode, P.hp[(size_t)d], P.deaths, rst,
+                      hints);
+  if (d < D) std::sort(P.deaths.begin(), P.deaths.end());  // the clearing input of d+1 (binary searches)
+  stt.ms_residual = ms_since(tr) + ms_prep;
   ST.mark("  residual (host)");
   if (std::getenv("VR_TIMING"))
     std::fprintf(stderr, "[vr]   residual d=%d: columns %llu emergent %lld additions %lld coboundaries %lld apparent checks %lld\n", d,
@@ -1157,12 +1183,14 @@ void run_distributed(vr_plan& P) {
     CUDA_TRY(cudaStreamSynchronize(P.st));
     double ms_x = ms_since(tx);
     if (P.rank_id == 0) {
-      std::vector<uint64_t> hkeys((size_t)total);
+      std::vector<uint64_t> hkeys((size_t)total), hfirst;
+      std::vector<uint8_t> hclaimed;
       auto tx = std::chrono::steady_clock::now();
+      const bool hinted = active && residual_hints(P, d, P.x_merged.as<uint64_t>(), total, hfirst, hclaimed);
       if (total) CUDA_TRY(cudaMemcpyAsync(hkeys.data(), P.x_merged.p, total * 8, cudaMemcpyDeviceToHost, P.st));
       CUDA_TRY(cudaStreamSynchronize(P.st));
-      P.R->stats[(size_t)d].ms_transfer += ms_since(tx);
-      stage_dim_finish(P, d, hkeys.data(), total);
+      const vr::ResidualHints hints{hfirst.data(), hclaimed.data()};
+      stage_dim_finish(P, d, hkeys.data(), total, hinted ? &hints : nullptr, ms_since(tx));
     }
     // exchange C: rank 0's deaths of dimension d to every rank
     std::vector<uint64_t> deaths;
@@ -1221,12 +1249,14 @@ void run_full(vr_plan& P) {
       else if (d < P.D) P.dims[(size_t)d + 1].ndeaths_in = 0;
       continue;
     }
-    std::vector<uint64_t> hkeys((size_t)nk);
+    std::vector<uint64_t> hkeys((size_t)nk), hfirst;
+    std::vector<uint8_t> hclaimed;
     auto tx = std::chrono::steady_clock::now();
+    const bool hinted = P.dims[(size_t)d].active && residual_hints(P, d, P.local_sorted, nk, hfirst, hclaimed);
     if (nk) CUDA_TRY(cudaMemcpyAsync(hkeys.data(), P.local_sorted, nk * 8, cudaMemcpyDeviceToHost, P.st));
     CUDA_TRY(cudaStreamSynchronize(P.st));
-    P.R->stats[(size_t)d].ms_transfer += ms_since(tx);
-    stage_dim_finish(P, d, hkeys.data(), nk);
+    const vr::ResidualHints hints{hfirst.data(), hclaimed.data()};
+    stage_dim_finish(P, d, hkeys.data(), nk, hinted ? &hints : nullptr, ms_since(tx));
   }
   stage_result(P);
 }

@@ -117,6 +117,14 @@ struct SparseRows {
 // (nw: words per row, >= ceil(n/32); the words past the last vertex are written as zeros)
 void launch_threshold_bitmap(const uint32_t* rank, int n, int nw, uint32_t* bm, uint32_t* deg, uint32_t* deg_below,
                              cudaStream_t st, int64_t* launches);
+// residual_prep.cu: the packed neighbour ranks of the threshold graph for the host, and the
+// residual columns' first equal-diameter cofacets + apparent claims (ResidualHints);
+// bm = nullptr: dense mode (scans over the rank rows)
+void launch_neighbour_ranks(const uint32_t* rank, int n, const uint32_t* bm, int nw, const uint32_t* deg,
+                            uint32_t* counter, uint32_t* nb_pre, uint32_t* nb_rank, cudaStream_t st, int64_t* launches);
+void launch_residual_hints(const uint32_t* rank, const uint64_t* binom, int n, int kmax, int d, const uint32_t* bm,
+                           int nw, const uint64_t* keys, uint64_t nkeys, uint32_t maxr, int cbits, uint64_t* first,
+                           uint8_t* claimed, cudaStream_t st, int64_t* launches);
 // two_level (d >= 2): rows are (d-2)-simplices extended by two vertices (k_enum_sparse2)
 void launch_enumerate_sparse(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
                              const SparseRows& S, bool two_level, cudaStream_t st, int64_t* launches);
@@ -194,9 +202,32 @@ struct HostMatrix {
   PinnedVec<uint32_t> rank;     // n*n
   std::vector<uint64_t> binom;  // (kmax+1)*(n+1)
   int kmax = 0;
-  // optional threshold-graph adjacency (output-sensitive mode): neighbours descending
-  std::vector<uint32_t> adj_off;  // n+1, empty = dense scans over all vertices
-  std::vector<uint16_t> adj;
+  // output-sensitive mode: the threshold graph as bitmap rows (bit v of row u = {u, v}
+  // under the threshold; empty = dense scans of the rank matrix), bmw 64-bit words per row;
+  // the scans take the AND of the simplex's rows (common neighbours).  The ranks of each
+  // row's neighbours are packed in ascending neighbour order (a few MB: they stay in the
+  // host caches, unlike the n*n matrix, which is then not copied at all), and per (row,
+  // word) nb_pre is the index in nb_rank of the word's first neighbour:
+  // R(u, v) = nb_rank[nb_pre[u*bmw + v/64] + popc(word bits below v)]
+  // (built on the device by residual_prep.cu; build_neighbour_ranks is the tools' copy).
+  std::vector<uint64_t> bm;
+  int64_t bmw = 0;
+  std::vector<uint32_t> nb_rank;
+  std::vector<uint32_t> nb_pre;
+  void build_neighbour_ranks() {
+    nb_pre.assign(bm.size(), 0);
+    nb_rank.clear();
+    for (int64_t u = 0; u < n; ++u)
+      for (int64_t w = 0; w < bmw; ++w) {
+        nb_pre[(size_t)(u * bmw + w)] = (uint32_t)nb_rank.size();
+        uint64_t x = bm[(size_t)(u * bmw + w)];
+        while (x) {
+          const int b = __builtin_ctzll(x);
+          x &= x - 1;
+          nb_rank.push_back(R(u, w * 64 + b));
+        }
+      }
+  }
   uint64_t C(int64_t v, int k) const { return binom[(size_t)k * (size_t)(n + 1) + (size_t)v]; }
   uint32_t R(int64_t i, int64_t j) const { return rank[(size_t)i * (size_t)n + (size_t)j]; }
 };
@@ -209,8 +240,21 @@ void dim0_union_find(int64_t n, const uint64_t* edges_sorted, uint64_t m, int kb
 struct ResidualStats {
   int64_t emergent = 0, additions = 0, coboundaries = 0, apparent_checks = 0;
 };
+// Per residual column c (keys order): first[c] = cidx of the first equal-diameter cofacet t
+// (the lex-greatest cofacet with diam(t) = diam(σ); UINT64_MAX if none) and claimed[c] = 1
+// iff t is the apparent cofacet of some column (Def 5.3.4).  With them the emergent check
+// (§5.2.11) is one pivot-table lookup instead of a coboundary scan.
+struct ResidualHints {
+  const uint64_t* first;
+  const uint8_t* claimed;
+};
+// deaths: the pivots (death cidx) of the columns with one, in no particular order.
 void residual_reduce(const HostMatrix& M, int d, uint32_t maxr, int cbits, const uint64_t* keys, uint64_t nkeys,
-                     int mode, HostPairs& out, std::vector<uint64_t>& deaths_sorted, ResidualStats& st);
+                     int mode, HostPairs& out, std::vector<uint64_t>& deaths, ResidualStats& st,
+                     const ResidualHints* hints = nullptr);
+// the hints on the host (checks, tools/residual_bench.cpp)
+void residual_hints_host(const HostMatrix& M, int d, uint32_t maxr, int cbits, const uint64_t* keys, uint64_t nkeys,
+                         uint64_t* first, uint8_t* claimed);
 
 // HYPHA host phase (hypha_host.cpp): compression + reduction of the unstable columns;
 // Lookup (row -> pivot column, -1) holds the GPU pivots on entry and every pivot on exit.

@@ -2,6 +2,8 @@
 // (VR_DUMP_RESIDUAL=<dir>).  Diagnostics only.
 //   g++ -O3 -std=c++17 -I /usr/local/cuda/include -I paper_2502_05063_b200/csrc tools/residual_bench.cpp
 //       paper_2502_05063_b200/csrc/host.cpp -o /tmp/residual_bench && /tmp/residual_bench <dir> <d> [mode]
+// env: VR_BM=1 output-sensitive host graph, VR_HINTS=1 residual hints (computed untimed),
+//      VR_RESIDUAL_THREADS, VR_RESIDUAL_BLOCK
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -53,18 +55,23 @@ int main(int argc, char** argv) {
       else for (int i = 1; i <= k; ++i) c = c * (unsigned __int128)(v - k + i) / (unsigned)i;
       M.binom[(size_t)k * (size_t)(n + 1) + (size_t)v] = (uint64_t)c;
     }
-  if (std::getenv("VR_ADJ")) {  // threshold-graph adjacency as the output-sensitive mode builds it
-    M.adj_off.assign((size_t)n + 1, 0);
-    for (long long v = 0; v < n; ++v) {
-      for (long long w = n - 1; w >= 0; --w)
-        if (w != v && M.rank[(size_t)v * n + w] != 0xFFFFFFFFu) M.adj.push_back((uint16_t)w);
-      M.adj_off[(size_t)v + 1] = (uint32_t)M.adj.size();
-    }
+  if (std::getenv("VR_BM")) {  // threshold-graph bitmap + packed ranks, as the output-sensitive mode builds them
+    M.bmw = (n + 63) / 64;
+    M.bm.assign((size_t)n * M.bmw, 0);
+    for (long long v = 0; v < n; ++v)
+      for (long long w = 0; w < n; ++w)
+        if (w != v && M.rank[(size_t)v * n + w] != 0xFFFFFFFFu) M.bm[(size_t)v * M.bmw + w / 64] |= 1ull << (w % 64);
+    M.build_neighbour_ranks();
   }
   auto keys = rd<uint64_t>(dir + "/keys_d" + std::to_string(d) + ".bin");
   vr::HostPairs hp; std::vector<uint64_t> deaths; vr::ResidualStats st;
+  std::vector<uint64_t> hfirst(keys.size());
+  std::vector<uint8_t> hclaimed(keys.size());
+  vr::ResidualHints hints{hfirst.data(), hclaimed.data()};
+  const bool use_hints = std::getenv("VR_HINTS") != nullptr;  // precomputed (untimed), as the GPU emits them
+  if (use_hints) vr::residual_hints_host(M, d, maxr, cbits, keys.data(), keys.size(), hfirst.data(), hclaimed.data());
   auto t0 = std::chrono::steady_clock::now();
-  vr::residual_reduce(M, d, maxr, cbits, keys.data(), keys.size(), mode, hp, deaths, st);
+  vr::residual_reduce(M, d, maxr, cbits, keys.data(), keys.size(), mode, hp, deaths, st, use_hints ? &hints : nullptr);
   double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   size_t pos = 0;
   for (size_t i = 0; i < hp.birth.size(); ++i) pos += hp.birth[i] < hp.death[i];
@@ -76,6 +83,9 @@ int main(int argc, char** argv) {
     std::printf("key rank %u\n", maxr - (unsigned)(keys[i] >> cbits));
     (void)cm;
   }
+  uint64_t h = 0;
+  for (size_t i = 0; i < hp.birth.size(); ++i) h = h * 1000003ull + hp.birth_cidx[i] * 31 + hp.death_cidx[i];
+  std::printf("hash %016llx\n", (unsigned long long)h);
   std::printf("d=%d mode=%d columns=%zu emergent=%lld additions=%lld coboundaries=%lld apparent_checks=%lld pairs=%zu positive=%zu ms=%.1f\n",
               d, mode, keys.size(), (long long)st.emergent, (long long)st.additions, (long long)st.coboundaries, (long long)st.apparent_checks,
               hp.birth.size(), pos, ms);
