@@ -831,7 +831,7 @@ void residual_reduce(const HostMatrix& M, int d, uint32_t maxr, int cbits, const
   using u128 = unsigned __int128;
   int nthreads = (int)std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency()));
   if (const char* e = std::getenv("VR_RESIDUAL_THREADS")) nthreads = std::max(1, std::atoi(e));
-  if (mode == 0 && nthreads > 1 && nkeys >= 64) {
+  if (mode == 0 && nthreads > 1 && (nkeys >= 64 || std::getenv("VR_RESIDUAL_THREADS"))) {
     if (rb + cb <= 64) residual_reduce_par<uint64_t>(M, d, maxr, cbits, keys, nkeys, cb, hints, nthreads, out, deaths, st);
     else residual_reduce_par<u128>(M, d, maxr, cbits, keys, nkeys, cb, hints, nthreads, out, deaths, st);
     return;

@@ -990,6 +990,15 @@ void stage_dim_finish(vr_plan& P, int d, const uint64_t* keys, uint64_t nkeys, c
     }
     return;
   }
+  if (hints && std::getenv("VR_CHECK_HINTS")) {  // tests: the device hints against the host's own scans
+    std::vector<uint64_t> f((size_t)nkeys);
+    std::vector<uint8_t> c((size_t)nkeys);
+    vr::residual_hints_host(P.M, d, P.maxr, dr.p.cbits, keys, nkeys, f.data(), c.data());
+    for (uint64_t i = 0; i < nkeys; ++i)
+      if (f[(size_t)i] != hints->first[i] || c[(size_t)i] != hints->claimed[i])
+        throw VrError(VR_EDEVICE, "residual hints differ from the host scan (dimension " + std::to_string(d) + ", column " +
+                                      std::to_string(i) + ")");
+  }
   auto tr = std::chrono::steady_clock::now();
   vr::ResidualStats rst;
   vr::residual_reduce(P.M, d, P.maxr, dr.p.cbits, keys, nkeys, P.opt.residual_mode, P.hp[(size_t)d], P.deaths, rst,
