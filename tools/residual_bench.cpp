@@ -75,6 +75,13 @@ int main(int argc, char** argv) {
   double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   size_t pos = 0;
   for (size_t i = 0; i < hp.birth.size(); ++i) pos += hp.birth[i] < hp.death[i];
+  if (const char* f = std::getenv("VR_PAIRS_OUT")) {  // per column: death cidx (UINT64_MAX: zero column)
+    FILE* fo = std::fopen(f, "wb");
+    if (fo) {
+      std::fwrite(hp.death_cidx.data(), 8, hp.death_cidx.size(), fo);
+      std::fclose(fo);
+    }
+  }
   if (const char* c = std::getenv("VR_COL")) {
     size_t i = (size_t)std::atoll(c);
     std::printf("col %zu: birth %.7g death %.7g bcidx %llu dcidx %llu\n", i, hp.birth[i], hp.death[i],
