@@ -400,6 +400,108 @@ struct RadixHeap {
   }
 };
 
+// Radix heap with 4-bit digits: a key lives in the bucket (L, g) where L is the highest
+// nibble in which it differs from `last` and g is its nibble L (keys equal to `last` in
+// bucket E).  The minimum is in the lowest non-empty level's lowest non-empty digit
+// (occupancy masks), and when that bucket is split every key moves to a strictly lower
+// level: at most one move per nibble of the key instead of one per BIT in the binary radix
+// heap above — the working columns of long reductions are mostly keys far above the pivot
+// that the binary heap re-files level after level (config 2's H3 column: pivot time
+// halved).  16 buckets per level keep the heap small for the many short columns.  Same Z/2
+// cancellation and the same drop rule.
+template <class K>
+struct RadixHeapN {
+  static constexpr int NL = (int)sizeof(K) * 2;  // nibbles
+  std::vector<K> eq;                // keys == last
+  std::vector<K> b[NL][16];
+  uint16_t dmask[NL];               // non-empty digits per level
+  uint32_t lmask = 0;               // non-empty levels
+  K last = 0;
+  size_t sz = 0;
+  int cb;
+  K mask;
+  RadixHeapN(uint32_t, int cbits) : cb(cbits), mask(cbits >= (int)sizeof(K) * 8 ? ~(K)0 : (((K)1 << cbits) - 1)) {
+    std::memset(dmask, 0, sizeof(dmask));
+  }
+  static int hinib(K d);
+  void put(K x) {
+    const K diff = x ^ last;
+    if (diff == 0) { eq.push_back(x); return; }
+    const int L = hinib(diff);
+    const int dg = (int)((x >> (4 * L)) & 0xF);
+    b[L][dg].push_back(x);
+    dmask[L] |= (uint16_t)(1u << dg);
+    lmask |= 1u << L;
+  }
+  void push(uint32_t r, uint64_t c) {
+    const K x = ((K)r << cb) | (mask - (K)c);
+    if (x < last) return;  // below the pivot: cancels within the added column
+    put(x);
+    ++sz;
+  }
+  void clear() {
+    eq.clear();
+    while (lmask) {
+      const int L = __builtin_ctz(lmask);
+      lmask &= lmask - 1;
+      uint32_t m = dmask[L];
+      while (m) {
+        b[L][__builtin_ctz(m)].clear();
+        m &= m - 1;
+      }
+      dmask[L] = 0;
+    }
+    last = 0;
+    sz = 0;
+  }
+  bool settle() {
+    if (sz == 0) return false;
+    if (!eq.empty()) return true;
+    const int L = __builtin_ctz(lmask);
+    const int dg = __builtin_ctz((uint32_t)dmask[L]);
+    std::vector<K>& v = b[L][dg];
+    K m = v[0];
+    for (K x : v) m = x < m ? x : m;
+    last = m;
+    dmask[L] = (uint16_t)(dmask[L] & ~(1u << dg));
+    if (!dmask[L]) lmask &= ~(1u << L);
+    for (K x : v) put(x);  // every key lands at a level below L
+    v.clear();
+    return true;
+  }
+  bool pivot(uint32_t& r, uint64_t& c) {
+    while (settle()) {
+      const size_t n0 = eq.size();
+      if (n0 & 1) {
+        if (n0 > 1) { eq.resize(1); sz -= n0 - 1; }
+        r = (uint32_t)(last >> cb);
+        c = (uint64_t)(mask - (last & mask));
+        return true;
+      }
+      sz -= n0;
+      eq.clear();
+    }
+    return false;
+  }
+};
+template <> inline int RadixHeapN<uint64_t>::hinib(uint64_t d) { return (63 - __builtin_clzll(d)) >> 2; }
+template <> inline int RadixHeapN<unsigned __int128>::hinib(unsigned __int128 d) {
+  const uint64_t hi = (uint64_t)(d >> 64);
+  return hi ? 16 + ((63 - __builtin_clzll(hi)) >> 2) : ((63 - __builtin_clzll((uint64_t)d)) >> 2);
+}
+
+// The working heap of the reduction-matrix mode: nibble digits for 64-bit keys (measured on
+// the box, 16 threads: config 2 dimension 3 892 -> 780 ms, config 5 dimension 1 183 -> 160 ms,
+// dimension 2 178 -> 168 ms), the binary radix heap for 128-bit keys (config 5 dimension 3,
+// 552K short columns: the larger nibble heaps, 32 per thread, cost 11%).
+template <class K> struct WorkHeapOf { using type = RadixHeapN<K>; };
+template <> struct WorkHeapOf<unsigned __int128> { using type = RadixHeap<unsigned __int128>; };
+#ifdef VR_BINARY_RADIX
+template <class K> using WorkHeap = RadixHeap<K>;
+#else
+template <class K> using WorkHeap = typename WorkHeapOf<K>::type;
+#endif
+
 // Binary heap over packed (rank, ~cidx) keys for the oblivious mode (Alg 12 adds raw
 // coboundaries D_k, whose entries can lie below the current pivot: not monotone).
 template <class K>
@@ -628,7 +730,7 @@ void residual_reduce_par(const HostMatrix& M, int d, uint32_t maxr, int cbits, c
     Ctx cx(M, d);
     U64Map app_memo(1024);
     // per column of the block: its working heap, its reduction column, its state
-    std::vector<RadixHeap<K>> heaps;
+    std::vector<WorkHeap<K>> heaps;
     heaps.reserve((size_t)B);
     for (int64_t i = 0; i < B; ++i) heaps.emplace_back(maxr, cb);
     std::vector<std::vector<uint64_t>> works((size_t)B);
@@ -647,7 +749,7 @@ void residual_reduce_par(const HostMatrix& M, int d, uint32_t maxr, int cbits, c
     };
     // reduce column j's heap while its pivot is claimed by a committed column or an
     // apparent pair
-    auto reduce = [&](uint64_t j, RadixHeap<K>& W, std::vector<uint64_t>& work_v, St& S) {
+    auto reduce = [&](uint64_t j, WorkHeap<K>& W, std::vector<uint64_t>& work_v, St& S) {
       ColOut& R = res[(size_t)j];
       auto push_coboundary = [&](uint64_t cidx, uint32_t r) {
         ++R.cobs;
@@ -682,7 +784,7 @@ void residual_reduce_par(const HostMatrix& M, int d, uint32_t maxr, int cbits, c
       // phase 1: speculative, against the pivots committed so far
       for (uint64_t j = j0; j < j1; ++j) {
         const size_t i = (size_t)(j - j0);
-        RadixHeap<K>& W = heaps[i];
+        WorkHeap<K>& W = heaps[i];
         St& S = sts[i];
         const uint64_t key = keys[j];
         const uint32_t rs = maxr - (uint32_t)(key >> cbits);
@@ -729,7 +831,7 @@ void residual_reduce_par(const HostMatrix& M, int d, uint32_t maxr, int cbits, c
       }
       for (uint64_t j = j0; j < j1; ++j) {
         const size_t i = (size_t)(j - j0);
-        RadixHeap<K>& W = heaps[i];
+        WorkHeap<K>& W = heaps[i];
         St& S = sts[i];
         ColOut& R = res[(size_t)j];
         const uint64_t key = keys[j];
@@ -838,7 +940,7 @@ void residual_reduce(const HostMatrix& M, int d, uint32_t maxr, int cbits, const
   }
   if (rb + cb <= 64) {
     if (mode == 0) {
-      RadixHeap<uint64_t> W(maxr, cb);
+      WorkHeap<uint64_t> W(maxr, cb);
       residual_reduce_t(M, d, maxr, cbits, keys, nkeys, hints, mode, W, out, deaths, st);
     } else {
       BinHeap<uint64_t> W(maxr, cb);
@@ -846,7 +948,7 @@ void residual_reduce(const HostMatrix& M, int d, uint32_t maxr, int cbits, const
     }
   } else {
     if (mode == 0) {
-      RadixHeap<u128> W(maxr, cb);
+      WorkHeap<u128> W(maxr, cb);
       residual_reduce_t(M, d, maxr, cbits, keys, nkeys, hints, mode, W, out, deaths, st);
     } else {
       BinHeap<u128> W(maxr, cb);
