@@ -144,6 +144,21 @@ struct Ctx {
   int64_t apparent_checks = 0;  // apparent_partner evaluations (the callers memoize)
   Ctx(const HostMatrix& m, int dd) : M(m), d(dd) {}
 
+  // the K rows a scan is about to read (bitmap words, word offsets, packed ranks): all
+  // their cache lines requested up front, so the misses overlap instead of queueing
+  // behind one another through the word loop
+  void prefetch_rows(const uint64_t* const* bw, const uint32_t* const* pre, int K) const {
+#ifdef VR_NO_PREFETCH
+    return;
+#endif
+    const int64_t W = M.bmw;
+    for (int q = 0; q < K; ++q) {
+      for (int64_t w = 0; w < W; w += 8) __builtin_prefetch(bw[q] + w);
+      for (int64_t w = 0; w < W; w += 16) __builtin_prefetch(pre[q] + w);
+      const uint32_t a = pre[q][0], b = pre[q][W - 1] + (uint32_t)__builtin_popcountll(bw[q][W - 1]);
+      for (uint32_t k = a; k < b; k += 16) __builtin_prefetch(M.nb_rank.data() + k);
+    }
+  }
   void decode(uint64_t cidx, int k /*vertices*/, int* v) const {
     int64_t hi = M.n;
     for (int p = 0; p < k; ++p) {
@@ -180,6 +195,7 @@ struct Ctx {
         pre[q] = &M.nb_pre[(size_t)s[q] * (size_t)M.bmw];
       }
       const uint32_t* NR = M.nb_rank.data();
+      prefetch_rows(bw, pre, d + 1);
       int j = 0;  // vertices of s above v
       for (int64_t w = M.bmw - 1; w >= 0; --w) {
         uint64_t x = bw[0][w];
@@ -240,6 +256,7 @@ struct Ctx {
         pre[q] = &M.nb_pre[(size_t)S[q] * (size_t)M.bmw];
       }
       const uint32_t* NR = M.nb_rank.data();
+      prefetch_rows(bw, pre, K);
       for (int64_t w = M.bmw - 1; w >= 0; --w) {
         uint64_t x = bw[0][w];
         for (int q = 1; q < K; ++q) x &= bw[q][w];
