@@ -560,7 +560,7 @@ def _sorted_bars(a):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["c2_s3_192", "c3_trefoil1000"])
+@pytest.mark.parametrize("name", ["c2_s3_192", "c3_trefoil1000", "c5_o3_4096"])
 def test_full_config_bars_equal_cpu_ripser(name):
     """Full-size barcodes, bit-exact, against cpu_ripser — the single-threaded Ripser-style
     program (implicit cohomology + clearing + emergent pairs, §5.2) that shares no
