@@ -893,6 +893,42 @@ static int sp_sms() {
   return s > 0 ? s : 148;
 }
 
+// ------------------------------------------------------------------ row order (two-level, d >= 3)
+// The work of a row τ grows with its smallest vertex u_2 (the σ = τ ∪ {x} take x < u_2), so
+// the rows are handed out by u_2 descending — largest first, no long tail at the end of the
+// launch (the vertex rows of d = 2 are taken top-down for the same reason).  Keys
+// ((0xFFFF - u_2) << 32 | row) radix-sorted on bits 32..47, then the rows gathered.
+template <int K>
+__global__ void k_row_keys(const uint4* __restrict__ rows, uint64_t n, uint64_t* __restrict__ keys) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    int t[K];
+    unpack_row<K>(rows, i, t);
+    keys[i] = ((uint64_t)(0xFFFFu - (uint32_t)t[K - 1]) << 32) | i;
+  }
+}
+__global__ void k_row_gather(const uint4* __restrict__ rows, const uint64_t* __restrict__ keys, uint64_t n,
+                             uint4* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = rows[keys[i] & 0xFFFFFFFFull];
+}
+size_t order_rows_temp_bytes(uint64_t n) { return radix_sort_temp_bytes((size_t)n); }
+void launch_order_rows(int k, const uint4* rows, uint64_t n, uint64_t* keys, uint64_t* alt, void* temp, uint4* out,
+                       cudaStream_t st, int64_t* launches) {
+  if (n == 0) return;
+  const unsigned bl = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sp_sms() * 8);
+  switch (k) {
+    case 2: k_row_keys<2><<<bl, 256, 0, st>>>(rows, n, keys); break;
+    case 3: k_row_keys<3><<<bl, 256, 0, st>>>(rows, n, keys); break;
+    case 4: k_row_keys<4><<<bl, 256, 0, st>>>(rows, n, keys); break;
+    case 5: k_row_keys<5><<<bl, 256, 0, st>>>(rows, n, keys); break;
+    default: k_row_keys<6><<<bl, 256, 0, st>>>(rows, n, keys); break;
+  }
+  const uint64_t* sorted = radix_sort_u64(keys, alt, (size_t)n, 32, 48, temp, st, launches);
+  k_row_gather<<<bl, 256, 0, st>>>(rows, sorted, n, out);
+  if (launches) *launches += 2;
+}
+
+
 void launch_threshold_bitmap(const uint32_t* rank, int n, int nw, uint32_t* bm, uint32_t* deg, uint32_t* deg_below,
                              cudaStream_t st, int64_t* launches) {
   const unsigned blocks = (unsigned)(((uint64_t)n * 32 + SP_THREADS - 1) / SP_THREADS);

@@ -299,6 +299,8 @@ struct vr_plan {
   DevBuf bm, deg, deg_below, bound;  // threshold-graph bitmap (n x nw words), degrees
   int32_t nw = 0;
   DevBuf nb_pre, nb_rank, nb_ctr;     // packed neighbour ranks for the host (residual_prep.cu)
+  DevBuf ord_keys, ord_alt, ord_tmp, ord_rows;  // two-level rows ordered by work (order_rows)
+  int ord_dim = -1;                   // the dimension whose rows ord_rows holds
   DevBuf h_first, h_claimed;          // residual hints of the current dimension
   std::vector<DevBuf> rows;           // rows[d] = packed d-simplex survivors (rows of d+1)
   std::vector<uint64_t> rows_count;   // survivors written per dimension
@@ -361,13 +363,29 @@ struct vr_plan {
       if ((dims[(size_t)k].two_level ? k - 2 : k - 1) == d) return true;
     return false;
   }
+  // Two-level rows of dimension d >= 3 (the survivors of d-2) ordered by their smallest
+  // vertex, descending: the largest rows first (sparse.cu, launch_order_rows).
+  // VR_NO_ROW_ORDER: the order the previous kernel wrote them in.
+  void order_rows(int d, cudaStream_t s) {
+    ord_dim = -1;
+    if (!sparse || d < 3 || !dims[(size_t)d].two_level || std::getenv("VR_NO_ROW_ORDER")) return;
+    const uint64_t nr = rows_count[(size_t)d - 2];
+    if (nr < 2 || nr >= (1ull << 32)) return;
+    ord_keys.ensure((size_t)nr * 8);
+    ord_alt.ensure((size_t)nr * 8);
+    ord_tmp.ensure(vr::order_rows_temp_bytes(nr));
+    ord_rows.ensure((size_t)nr * 16);
+    vr::launch_order_rows(d - 1, rows[(size_t)d - 2].as<uint4>(), nr, ord_keys.as<uint64_t>(), ord_alt.as<uint64_t>(),
+                          ord_tmp.p, ord_rows.as<uint4>(), s, &launches);
+    ord_dim = d;
+  }
   vr::SparseRows sparse_rows(int d, vr::DimCounters* ctr) {
     vr::SparseRows SR{};
     if (sparse) {
       SR.bm = bm.as<uint32_t>();
       SR.nw = nw;
       const int src = dims[(size_t)d].two_level ? d - 2 : d - 1;
-      SR.rows_in = src <= 0 ? nullptr : rows[(size_t)src].as<uint4>();
+      SR.rows_in = src <= 0 ? nullptr : (ord_dim == d ? ord_rows.as<uint4>() : rows[(size_t)src].as<uint4>());
       const bool keep = rows_needed(d);
       SR.rows_out = keep ? rows[(size_t)d].as<uint4>() : nullptr;
       SR.rows_out_cap = keep ? rows_cap[(size_t)d] : 0;
@@ -821,6 +839,7 @@ uint64_t stage_dim_local(vr_plan& P, int d) {
     vr::HotBuffers B{P.queue.as<uint64_t>(), P.qvert.as<uint4>(), P.qcap, P.resid.as<uint64_t>(), P.rcap,
                      P.clr_of(d), clr_next, dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, ctr, app_ptr, app_cap};
     P.hash_fields(B, d);
+    if (rb == 0) P.order_rows(d, st);  // (once per dimension, before its first chunk)
     vr::SparseRows SR = P.sparse_rows(d, ctr);
     p.row_begin = rb;
     p.row_end = re;
@@ -1318,6 +1337,12 @@ void replay(vr_plan& P) {
     P.hash_reset(d + 1, st);
     cudaEventRecord(e1.second, st);
     vr::DimParams p = dr.p;
+    {
+      auto& eo = ev(1);  // (timed with the enumeration stage)
+      cudaEventRecord(eo.first, st);
+      P.order_rows(d, st);
+      cudaEventRecord(eo.second, st);
+    }
     for (const Chunk& c : dr.chunks) {
       vr::HotBuffers B{P.queue.as<uint64_t>(), P.qvert.as<uint4>(), P.qcap, P.resid.as<uint64_t>(), P.rcap,
                        clr_of(d), clr_next, dr.deaths_in.as<uint64_t>(), dr.ndeaths_in, ctr, nullptr, 0};

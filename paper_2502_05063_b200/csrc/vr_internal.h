@@ -125,6 +125,12 @@ void launch_neighbour_ranks(const uint32_t* rank, int n, const uint32_t* bm, int
 void launch_residual_hints(const uint32_t* rank, const uint64_t* binom, int n, int kmax, int d, const uint32_t* bm,
                            int nw, const uint64_t* keys, uint64_t nkeys, uint32_t maxr, int cbits, uint64_t* first,
                            uint8_t* claimed, cudaStream_t st, int64_t* launches);
+// rows of k vertices (packed) -> out, ordered by their smallest vertex descending (the
+// two-level kernel's rows, largest work first); keys/alt: n u64 each, temp:
+// order_rows_temp_bytes(n)
+size_t order_rows_temp_bytes(uint64_t n);
+void launch_order_rows(int k, const uint4* rows, uint64_t n, uint64_t* keys, uint64_t* alt, void* temp, uint4* out,
+                       cudaStream_t st, int64_t* launches);
 // two_level (d >= 2): rows are (d-2)-simplices extended by two vertices (k_enum_sparse2)
 void launch_enumerate_sparse(const DimParams& p, const uint32_t* rank, const uint64_t* binom, int kmax, const HotBuffers& B,
                              const SparseRows& S, bool two_level, cudaStream_t st, int64_t* launches);
