@@ -301,6 +301,11 @@ struct vr_plan {
   DevBuf nb_pre, nb_rank, nb_ctr;     // packed neighbour ranks for the host (residual_prep.cu)
   DevBuf ord_keys, ord_alt, ord_tmp, ord_rows;  // two-level rows ordered by work (order_rows)
   int ord_dim = -1;                   // the dimension whose rows ord_rows holds
+  // replay: the ordering of dimension d's rows runs on a side stream as soon as dimension
+  // d-2 has written them, overlapping dimension d-1 (VR_NO_SIDE_ORDER: in line)
+  cudaStream_t st_side = nullptr;
+  cudaEvent_t ev_rows_ready = nullptr, ev_order_done = nullptr;
+  int side_dim = -1;
   DevBuf h_first, h_claimed;          // residual hints of the current dimension
   std::vector<DevBuf> rows;           // rows[d] = packed d-simplex survivors (rows of d+1)
   std::vector<uint64_t> rows_count;   // survivors written per dimension
@@ -317,6 +322,12 @@ struct vr_plan {
   int used_events[4] = {0, 0, 0, 0};
   ~vr_plan() {
     if (st) cudaStreamSynchronize(st);  // the device buffers go back to DevCache
+    if (st_side) {
+      cudaStreamSynchronize(st_side);
+      cudaStreamDestroy(st_side);
+    }
+    if (ev_rows_ready) cudaEventDestroy(ev_rows_ready);
+    if (ev_order_done) cudaEventDestroy(ev_order_done);
     for (auto& v : stage_ev)
       for (auto& e : v) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     for (auto& e : ev)
@@ -1340,7 +1351,13 @@ void replay(vr_plan& P) {
     {
       auto& eo = ev(1);  // (timed with the enumeration stage)
       cudaEventRecord(eo.first, st);
-      P.order_rows(d, st);
+      if (P.side_dim == d) {  // ordered on the side stream during dimension d-1
+        cudaStreamWaitEvent(st, P.ev_order_done, 0);
+        P.ord_dim = d;
+        P.side_dim = -1;
+      } else {
+        P.order_rows(d, st);
+      }
       cudaEventRecord(eo.second, st);
     }
     for (const Chunk& c : dr.chunks) {
@@ -1370,6 +1387,22 @@ void replay(vr_plan& P) {
       cudaEventRecord(ex.first, st);
       exchange_clearing(P, d, true);
       cudaEventRecord(ex.second, st);
+    }
+    // rows of dimension d are complete: order them for dimension d+2 on the side stream
+    if (d + 2 <= P.D && P.sparse && P.dims[(size_t)d + 2].two_level && !std::getenv("VR_NO_SIDE_ORDER")) {
+      if (!P.st_side) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&P.st_side, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&P.ev_rows_ready, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&P.ev_order_done, cudaEventDisableTiming));
+      }
+      cudaEventRecord(P.ev_rows_ready, st);
+      cudaStreamWaitEvent(P.st_side, P.ev_rows_ready, 0);
+      P.order_rows(d + 2, P.st_side);
+      if (P.ord_dim == d + 2) {
+        cudaEventRecord(P.ev_order_done, P.st_side);
+        P.side_dim = d + 2;
+      }
+      P.ord_dim = -1;  // (dimension d+1 reads its own rows)
     }
     auto& e4 = ev(3);
     cudaEventRecord(e4.first, st);
